@@ -1,0 +1,216 @@
+/*
+ * deltaserve_b200 - C ABI of the B200-native delta-only inference hot path.
+ *
+ * Plain pointers and sizes only (no torch types).  Every device pointer is a
+ * CUDA global-memory address; `stream` is a cudaStream_t (NULL = legacy).
+ * Return value: 0 = ok, < 0 = argument error (DS_E*), > 0 = cudaError_t or
+ * (1000 + cublasStatus_t).  Kernels never allocate and are stream ordered;
+ * capacity checks stay on the host (reference kvcache.py:116-118) so no
+ * kernel fails for capacity.
+ *
+ * Each entry point cites the reference interface it replaces
+ * (paths relative to /root/reference/pkg/src/deltaserve/).
+ */
+#ifndef DELTASERVE_B200_H
+#define DELTASERVE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* ds_stream_t;
+
+#define DS_OK 0
+#define DS_EINVAL (-1)
+#define DS_EUNSUPPORTED (-2)
+#define DS_EWORKSPACE (-3)
+
+int ds_abi_version(void);
+const char* ds_status_string(int status);
+
+/* ------------------------------------------------------------------------
+ * Integer kernels: batched device versions of deltaserve._kernels
+ * (_kernels/__init__.py:21-73, _native.pyx:18-119).  Sequence i lives at
+ * base + offsets[i] with lengths[i] int32 tokens.
+ * ---------------------------------------------------------------------- */
+
+/* fnv1a32_tokens / fnv1a64_tokens (_native.pyx:36-59), tokens hashed as 4 LE
+ * bytes; states_in (nullable) seeds each sequence (the `state=` argument).
+ * bits = 32 or 64; out[i] holds the hash (32-bit results zero-extended). */
+int ds_fnv1a_tokens(const int32_t* base, const int64_t* offsets, const int32_t* lengths, int n,
+                    int bits, const uint64_t* states_in, uint64_t* out, ds_stream_t stream);
+
+/* fnv1a32_bytes / fnv1a64_bytes (_native.pyx:18-33). */
+int ds_fnv1a_bytes(const uint8_t* base, const int64_t* offsets, const int32_t* lengths, int n,
+                   int bits, uint64_t* out, ds_stream_t stream);
+
+/* copy_continuation (_native.pyx:62-81): e_out[i] = index after the most
+ * recent earlier occurrence of the trailing min_match-gram, or -1. */
+int ds_copy_continuation(const int32_t* base, const int64_t* offsets, const int32_t* lengths,
+                         int n, int min_match, int32_t* e_out, ds_stream_t stream);
+
+/* K1 prompt-lookup n-gram matcher: longest_suffix_match (_native.pyx:84-119)
+ * for n slots at once, optionally fused with lookup_ngram's draft extraction
+ * (speculator.py:52-65): when caps != NULL, draft_out[i*max_draft + j] =
+ * ring[e + j] for j < draft_len_out[i] = min(caps[i], max_draft, len - e)
+ * (0 when no match or caps[i] <= 0). tail_base may equal ring_base. */
+int ds_longest_suffix_match(const int32_t* ring_base, const int64_t* ring_off,
+                            const int32_t* ring_len, const int32_t* tail_base,
+                            const int64_t* tail_off, const int32_t* tail_len, int n, int min_len,
+                            const int32_t* caps, int max_draft, int32_t* e_out, int32_t* len_out,
+                            int32_t* draft_out, int32_t* draft_len_out, ds_stream_t stream);
+
+/* Host-side FNV-1a used by the scheduler's own bookkeeping (Slot.prefix_hash
+ * scheduler.py:237/687/715 and _window_hash :489-490) - the same host work the
+ * reference scheduler does; not part of the device compute path. */
+uint64_t ds_host_fnv1a64_tokens(const int32_t* tokens, int64_t n, uint64_t state);
+uint32_t ds_host_fnv1a32_tokens(const int32_t* tokens, int64_t n, uint32_t state);
+
+/* ------------------------------------------------------------------------
+ * K4: paged KV store metadata (UnifiedKvCache kvcache.py:116-286).
+ * pos2cell[seq*pos_stride + p] = physical cell of logical position p;
+ * member[cell*mask_words + seq/32] bit seq%32 = sequence membership;
+ * trie_ref[cell] = references held by radix nodes (radix.py:158-159, 184).
+ * Ops are applied strictly in order by one CTA; 0 KV bytes move.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int32_t kind; /* DS_KV_MAP: pos2cell[seq][pos+i] = cell+i, set member bit;
+                   DS_KV_UNMAP: clear member bit `seq` on cells [cell, cell+len);
+                   DS_KV_TRIE_INC / DS_KV_TRIE_DEC: trie_ref[cell+i] += / -= 1 */
+  int32_t seq;
+  int32_t pos;
+  int32_t cell;
+  int32_t len;
+} ds_kv_op;
+#define DS_KV_MAP 0
+#define DS_KV_UNMAP 1
+#define DS_KV_TRIE_INC 2
+#define DS_KV_TRIE_DEC 3
+
+int ds_kv_apply(const ds_kv_op* ops_dev, int n_ops, int32_t* pos2cell, int64_t pos_stride,
+                int n_seqs, uint32_t* member, int mask_words, int32_t* trie_ref,
+                ds_stream_t stream);
+
+/* Token-history writes: segment i = {seq, start, len, src_offset} copies
+ * src[src_offset : src_offset+len] to hist[seq*pos_stride + start ...]
+ * (prompt upload at admission; pending tokens before the n-gram matcher). */
+int ds_hist_write(const int32_t* src, const int32_t* segs, int n_segs, int32_t* hist,
+                  int64_t pos_stride, ds_stream_t stream);
+
+/* Derived refcount (popcount(member) + trie_ref) and occupancy (cells with
+ * refcount > 0) - the device view of kvcache.py:91-100, 185-187. */
+int ds_kv_refcount(const uint32_t* member, int mask_words, const int32_t* trie_ref,
+                   int64_t capacity, int32_t* refcnt_out, int32_t* occupancy_out,
+                   ds_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Model forward: the device realisation of MockEngine.forward
+ * (engine.py:268-281) + LogitsBatch argmax/copy_source (engine.py:196-216)
+ * + the verify accept loop (speculator.py:99-112), for a whole batch of plan
+ * entries (scheduler.py:674-772) in one call.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int32_t layers, hidden, n_heads, n_kv_heads, head_dim, ffn, vocab;
+  float rms_eps;
+  const void* embed;      /* bf16 [vocab][hidden] */
+  const void* attn_norm;  /* bf16 [L][hidden] */
+  const void* wqkv;       /* bf16 [L][(nh+2nkv)*hd][hidden] */
+  const void* wo;         /* bf16 [L][hidden][nh*hd] */
+  const void* mlp_norm;   /* bf16 [L][hidden] */
+  const void* w_gate_up;  /* bf16 [L][2*ffn][hidden]  (gate rows first) */
+  const void* w_down;     /* bf16 [L][hidden][ffn] */
+  const void* final_norm; /* bf16 [hidden] */
+  const void* lm_head;    /* bf16 [vocab][hidden] */
+  const float* rope_cos;  /* f32 [rope_max_pos][hd/2] */
+  const float* rope_sin;
+  int32_t rope_max_pos;
+} ds_model;
+
+typedef struct {
+  void* k_pool; /* bf16 [L][capacity][nkv][hd] */
+  void* v_pool;
+  int64_t capacity;
+  int32_t* pos2cell; /* [n_seqs][pos_stride] */
+  int32_t* hist;     /* [n_seqs][pos_stride] token history */
+  int64_t pos_stride;
+  int32_t n_seqs;
+} ds_kv_store;
+
+#define DS_ENTRY_PREFILL 0 /* sample the last row (scheduler.py:721-723) */
+#define DS_ENTRY_DECODE 1  /* one row (scheduler.py:762-772) */
+#define DS_ENTRY_VERIFY 2  /* rows [last, d0..dk-1]; accept + bonus (speculator.py:77-113) */
+
+typedef struct {
+  int32_t seq;       /* sequence id (row of pos2cell / hist) */
+  int32_t past;      /* cells already resident before this batch (context length) */
+  int32_t q_len;     /* batch rows */
+  int32_t q_start;   /* first packed row */
+  int32_t kind;      /* DS_ENTRY_* */
+  int32_t n_draft;   /* k for VERIFY */
+  int32_t out_start; /* first output (sampled) row */
+  int32_t n_out;     /* sampled rows: 1 (prefill/decode) or k+1 (verify) */
+  uint64_t hash_in;  /* FNV-1a64 of the sequence's first `past` tokens */
+} ds_entry;
+
+#define DS_POLICY_COPY 0   /* reference copy-model token rule (engine.py:196-216) */
+#define DS_POLICY_ARGMAX 1 /* greedy argmax of the real logits, lowest id on ties */
+
+typedef struct {
+  int32_t n_entries, n_rows, n_out;
+  int32_t policy, copy_min_match, policy_vocab;
+  const ds_entry* entries_host; /* host copy (launch shapes) */
+  const ds_entry* entries;      /* device copy */
+  const int32_t* tokens;        /* device [n_rows] packed batch tokens */
+  const int32_t* row_seq;       /* device [n_rows] */
+  const int32_t* row_pos;       /* device [n_rows] absolute positions */
+  const int32_t* out_rows;      /* device [n_out] packed row of each sampled row */
+  int32_t* out_tok;             /* device [n_out] */
+  int32_t* out_src;             /* device [n_out] copy source or -1 */
+  int32_t* out_accept;          /* device [n_entries] accepted drafts (VERIFY) */
+  float* logits;                /* device [n_out][vocab] fp32 */
+  void* workspace;
+  size_t workspace_bytes;
+} ds_forward_args;
+
+size_t ds_forward_workspace_bytes(const ds_model* model, int max_rows, int max_out,
+                                  int max_entries);
+int ds_model_forward(const ds_model* model, const ds_kv_store* kv, const ds_forward_args* args,
+                     ds_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Individual layer kernels (exported for parity tests and microbenchmarks).
+ * ---------------------------------------------------------------------- */
+
+/* K5: RoPE (rotate-half, cos/sin table) on q (in place in qkv) and k; store k,v
+ * rows into the layer's cell pool at pos2cell[row_seq][row_pos]. */
+int ds_rope_kv_store(void* qkv, int n_rows, const int32_t* row_seq, const int32_t* row_pos,
+                     const int32_t* pos2cell, int64_t pos_stride, int n_heads, int n_kv_heads,
+                     int head_dim, const float* rope_cos, const float* rope_sin, void* k_pool_l,
+                     void* v_pool_l, ds_stream_t stream);
+
+/* K6/K7 attention over the paged store for a batch of entries.  q is the
+ * roped qkv buffer ([n_rows][(nh+2nkv)*hd], q heads first), out is
+ * [n_rows][nh*hd] bf16.  Causal over absolute positions. impl: 0 = auto,
+ * 1 = split-KV decode/verify kernel (K7), 2 = tcgen05 delta-prefill (K6). */
+size_t ds_attention_workspace_bytes(int n_rows, int n_entries, int n_heads, int head_dim);
+int ds_attention(const void* qkv, const ds_entry* entries_host, const ds_entry* entries_dev,
+                 int n_entries, int n_rows, const void* k_pool_l, const void* v_pool_l,
+                 const int32_t* pos2cell, int64_t pos_stride, int n_heads, int n_kv_heads,
+                 int head_dim, float scale, void* out, void* workspace, size_t workspace_bytes,
+                 int impl, ds_stream_t stream);
+
+int ds_rmsnorm(const void* x, const int32_t* rows, int n_rows, int hidden, const void* w,
+               float eps, void* out, ds_stream_t stream);
+int ds_silu_mul(const void* gate_up, int n_rows, int ffn, void* out, ds_stream_t stream);
+int ds_embed(const int32_t* tokens, int n_rows, const void* table, int hidden, void* out,
+             ds_stream_t stream);
+/* K8: row argmax over fp32 logits (lowest index on ties, engine.py:146-159). */
+int ds_argmax(const float* logits, int n_rows, int vocab, int32_t* out, ds_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DELTASERVE_B200_H */

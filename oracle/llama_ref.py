@@ -1,0 +1,94 @@
+"""ORACLE - CPU fp32 restatement of the decoder the GPU engine runs (test only).
+
+The reference artifact has NO model (engine.py:1-17 is a copy-model mock;
+SPEC.md:18 puts GPU execution out of scope), so attention / logits parity is
+pinned only by this restatement of standard Llama-3 math (PAPER.md:293:
+Llama-3.1-8B): RMSNorm (eps 1e-5), rotate-half RoPE (theta 500000, fp64
+angles), GQA attention, SwiGLU MLP, untied LM head.  It rounds to bf16 at
+exactly the tensor boundaries the GPU stores (residual stream, norm outputs,
+projections, roped q/k, KV cache, attention output, MLP activations) and
+accumulates in fp32 everywhere else, so the tolerance budget is only the
+accumulation-order / bf16-P difference (logits max-abs <= 1e-2).
+"""
+from __future__ import annotations
+
+import torch
+
+
+def _bf(x: torch.Tensor) -> torch.Tensor:
+    return x.to(torch.bfloat16).float()
+
+
+def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
+    inv = torch.rsqrt((x * x).mean(-1, keepdim=True) + eps)
+    return _bf(x * inv * w)
+
+
+def rope_tables(n_pos: int, head_dim: int, theta: float):
+    inv = theta ** (-torch.arange(0, head_dim, 2, dtype=torch.float64) / head_dim)
+    ang = torch.arange(n_pos, dtype=torch.float64)[:, None] * inv[None, :]
+    return torch.cos(ang).float(), torch.sin(ang).float()
+
+
+def rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
+    """x [T, H, d]; cos/sin [T, d/2] -> rotate-half RoPE rounded to bf16."""
+    half = x.shape[-1] // 2
+    x1, x2 = x[..., :half], x[..., half:]
+    c, s = cos[:, None, :], sin[:, None, :]
+    return _bf(torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], dim=-1))
+
+
+@torch.no_grad()
+def forward(w: dict, shape, tokens: list[int], out_rows: list[int] | None = None,
+            threads: int | None = None) -> torch.Tensor:
+    """Logits [len(out_rows), V] (fp32) for one causal sequence of `tokens`.
+
+    w: fp32 CPU copies of the bf16 weights (GpuEngine.weights_cpu()).
+    """
+    if threads:
+        torch.set_num_threads(threads)
+    T = len(tokens)
+    nh, nkv, d = shape.n_heads, shape.n_kv_heads, shape.head_dim
+    G = nh // nkv
+    cos, sin = rope_tables(T, d, shape.rope_theta)
+    x = w["embed"][torch.tensor(tokens, dtype=torch.long)]
+    mask = torch.full((T, T), float("-inf")).triu(1)
+    scale = 1.0 / (d ** 0.5)
+    for l in range(shape.layers):
+        h = rmsnorm(x, w["attn_norm"][l], shape.rms_eps)
+        qkv = _bf(h @ w["wqkv"][l].T)
+        q = qkv[:, : nh * d].view(T, nh, d)
+        k = qkv[:, nh * d: (nh + nkv) * d].view(T, nkv, d)
+        v = qkv[:, (nh + nkv) * d:].view(T, nkv, d)
+        q, k = rope(q, cos, sin), rope(k, cos, sin)
+        kr = k.repeat_interleave(G, dim=1)  # [T, nh, d]
+        vr = v.repeat_interleave(G, dim=1)
+        s = torch.einsum("qhd,khd->hqk", q, kr) * scale + mask
+        p = torch.softmax(s, dim=-1)
+        o = _bf(torch.einsum("hqk,khd->qhd", p, vr).reshape(T, nh * d))
+        x = _bf(x + o @ w["wo"][l].T)
+        h = rmsnorm(x, w["mlp_norm"][l], shape.rms_eps)
+        gu = _bf(h @ w["w_gate_up"][l].T)
+        g, u = gu[:, : shape.ffn], gu[:, shape.ffn:]
+        a = _bf(torch.nn.functional.silu(g) * u)
+        x = _bf(x + a @ w["w_down"][l].T)
+    rows = list(range(T)) if out_rows is None else out_rows
+    hf = rmsnorm(x[rows], w["final_norm"], shape.rms_eps)
+    return hf @ w["lm_head"].T
+
+
+@torch.no_grad()
+def paged_attention(q: torch.Tensor, k_cells: torch.Tensor, v_cells: torch.Tensor,
+                    q_pos: list[int], kv_len: int, scale: float) -> torch.Tensor:
+    """Reference attention for one sequence: q [Tq, nh, d] (roped, bf16 values),
+    k/v [kv_len, nkv, d] gathered in logical order; causal by absolute position."""
+    Tq, nh, d = q.shape
+    G = nh // k_cells.shape[1]
+    kr = k_cells.float().repeat_interleave(G, dim=1)
+    vr = v_cells.float().repeat_interleave(G, dim=1)
+    s = torch.einsum("qhd,khd->hqk", q.float(), kr) * scale
+    kpos = torch.arange(kv_len)[None, :]
+    qpos = torch.tensor(q_pos)[:, None]
+    s = s.masked_fill((kpos > qpos)[None], float("-inf"))
+    p = torch.softmax(s, dim=-1)
+    return torch.einsum("hqk,khd->qhd", p, vr)

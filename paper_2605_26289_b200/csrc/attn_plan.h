@@ -1,0 +1,69 @@
+// Split-KV work decomposition shared by host launch code and device kernels.
+// Split boundaries are a pure function of (q-blocks, kv_len): every CTA and
+// the combine kernel recompute the same plan, no extra H2D per forward.
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+#include "../../include/deltaserve_b200.h"
+
+#ifdef __CUDACC__
+#define DS_HD __host__ __device__ __forceinline__
+#else
+#define DS_HD inline
+#endif
+
+namespace ds {
+
+constexpr int kNumSMs = 148;
+constexpr int kSplitRows = 64;  // packed rows per split-kernel CTA (4 warps x 16)
+
+struct AttnSplitPlan {
+  int n_splits;
+  int split_len;
+};
+
+// n_entries: entries sharing the launch (target ~2 CTAs per SM for the batch)
+DS_HD AttnSplitPlan attn_split_plan(int qblocks, int kv_len, int nkv, int n_entries) {
+  const int ctas = qblocks * nkv * n_entries;
+  int n = (2 * kNumSMs + ctas - 1) / ctas;
+  const int by_len = (kv_len + 127) / 128;
+  if (n > by_len) n = by_len;
+  if (n > 32) n = 32;
+  if (n < 1) n = 1;
+  int split_len = ((kv_len + n - 1) / n + 63) / 64 * 64;
+  if (split_len < 64) split_len = 64;
+  n = (kv_len + split_len - 1) / split_len;
+  if (n < 1) n = 1;
+  return {n, split_len};
+}
+
+// rows of partial storage used by entries [0, e)
+DS_HD int64_t attn_partial_base(const ds_entry* entries, int e, int n_entries, int nh, int nkv) {
+  int64_t base = 0;
+  const int G = nh / nkv;
+  for (int i = 0; i < e; ++i) {
+    const int R = entries[i].q_len * G;
+    const int qb = (R + kSplitRows - 1) / kSplitRows;
+    const AttnSplitPlan p = attn_split_plan(qb, entries[i].past + entries[i].q_len, nkv,
+                                             n_entries);
+    if (p.n_splits > 1) base += static_cast<int64_t>(p.n_splits) * R;
+  }
+  return base;
+}
+
+inline int64_t attn_partial_slots(const ds_entry* entries, int n, int nh, int nkv) {
+  return attn_partial_base(entries, n, n, nh, nkv) * nkv;
+}
+
+inline size_t attn_partial_bytes(const ds_entry* entries, int n, int nh, int nkv) {
+  const int64_t slots = attn_partial_slots(entries, n, nh, nkv);
+  return static_cast<size_t>(slots) * (128 + 1) * sizeof(float);
+}
+
+// upper bound of attn_partial_bytes for any batch (sum over
+// split entries of n_splits*qblocks*nkv <= 4*kNumSMs)
+inline size_t attn_partial_bytes_bound() {
+  return static_cast<size_t>(4 * kNumSMs) * kSplitRows * (128 + 1) * sizeof(float);
+}
+
+}  // namespace ds

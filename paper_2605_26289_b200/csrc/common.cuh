@@ -1,0 +1,107 @@
+// Shared device helpers for the deltaserve B200 kernels (sm_100a only).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "deltaserve_b200 targets sm_100a only"
+#endif
+
+#define DS_DEVICE __device__ __forceinline__
+
+namespace ds {
+
+constexpr uint64_t kFnv64Offset = 0xCBF29CE484222325ull;
+constexpr uint64_t kFnv64Prime = 0x100000001B3ull;
+constexpr uint32_t kFnv32Offset = 0x811C9DC5u;
+constexpr uint32_t kFnv32Prime = 0x01000193u;
+
+DS_DEVICE uint64_t fnv64_token(uint64_t h, int32_t tok) {
+  const uint32_t t = static_cast<uint32_t>(tok);
+  h = (h ^ (t & 0xFFu)) * kFnv64Prime;
+  h = (h ^ ((t >> 8) & 0xFFu)) * kFnv64Prime;
+  h = (h ^ ((t >> 16) & 0xFFu)) * kFnv64Prime;
+  h = (h ^ (t >> 24)) * kFnv64Prime;
+  return h;
+}
+
+DS_DEVICE uint32_t fnv32_token(uint32_t h, int32_t tok) {
+  const uint32_t t = static_cast<uint32_t>(tok);
+  h = (h ^ (t & 0xFFu)) * kFnv32Prime;
+  h = (h ^ ((t >> 8) & 0xFFu)) * kFnv32Prime;
+  h = (h ^ ((t >> 16) & 0xFFu)) * kFnv32Prime;
+  h = (h ^ (t >> 24)) * kFnv32Prime;
+  return h;
+}
+
+template <typename T>
+DS_DEVICE T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+template <typename T>
+DS_DEVICE T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+DS_DEVICE uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 16-byte async global->shared copy (LDGSTS), L2-only caching.
+DS_DEVICE void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem));
+}
+DS_DEVICE void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+  const int src = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(src));
+}
+DS_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+DS_DEVICE void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+DS_DEVICE uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// ldmatrix wrappers (8x8 b16 tiles).
+DS_DEVICE void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+DS_DEVICE void ldsm_x4_t(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
+// D = A(16x16 bf16, row) * B(16x8 bf16, col) + D (fp32).
+DS_DEVICE void mma_bf16_16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+DS_DEVICE float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
+
+}  // namespace ds

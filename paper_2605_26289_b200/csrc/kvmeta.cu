@@ -1,0 +1,114 @@
+// K4: paged KV store metadata - metadata-only aliasing (0 KV bytes moved).
+//
+// The host UnifiedKvCache mirror (kvcache.py:116-286 semantics: first-fit
+// allocator, spans, refcounts) records one op per page-table mutation; a
+// flush applies the whole op list here, strictly in order, inside one CTA
+// (ops are short and few per iteration; ordering matters because a trimmed
+// cell can be re-allocated to the same sequence in the same flush).
+#include "../../include/deltaserve_b200.h"
+#include "common.cuh"
+
+namespace ds {
+
+// Sequences outside [0, n_seqs) (host-only pressure in tests) are not
+// mirrored; positions beyond pos_stride are never written.
+__global__ void __launch_bounds__(1024) kv_apply_kernel(const ds_kv_op* __restrict__ ops, int n_ops,
+                                                        int32_t* pos2cell, int64_t pos_stride,
+                                                        int n_seqs, uint32_t* member,
+                                                        int mask_words, int32_t* trie_ref) {
+  for (int i = 0; i < n_ops; ++i) {
+    const ds_kv_op op = ops[i];
+    const bool mirrored = op.seq >= 0 && op.seq < n_seqs;
+    const uint32_t bit = 1u << (op.seq & 31);
+    const int word = op.seq >> 5;
+    switch (op.kind) {
+      case DS_KV_MAP: {
+        if (!mirrored) break;
+        int32_t* row = pos2cell + static_cast<int64_t>(op.seq) * pos_stride + op.pos;
+        for (int j = threadIdx.x; j < op.len; j += blockDim.x) {
+          const int32_t c = op.cell + j;
+          if (op.pos + j < pos_stride) row[j] = c;
+          member[static_cast<int64_t>(c) * mask_words + word] |= bit;
+        }
+        break;
+      }
+      case DS_KV_UNMAP:
+        if (!mirrored) break;
+        for (int j = threadIdx.x; j < op.len; j += blockDim.x)
+          member[static_cast<int64_t>(op.cell + j) * mask_words + word] &= ~bit;
+        break;
+      case DS_KV_TRIE_INC:
+        for (int j = threadIdx.x; j < op.len; j += blockDim.x) trie_ref[op.cell + j] += 1;
+        break;
+      case DS_KV_TRIE_DEC:
+        for (int j = threadIdx.x; j < op.len; j += blockDim.x) trie_ref[op.cell + j] -= 1;
+        break;
+      default:
+        break;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void kv_refcount_kernel(const uint32_t* __restrict__ member, int mask_words,
+                                   const int32_t* __restrict__ trie_ref, int64_t capacity,
+                                   int32_t* refcnt, int32_t* occupancy) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int live = 0;
+  if (c < capacity) {
+    int r = trie_ref[c];
+    const uint32_t* m = member + c * mask_words;
+    for (int w = 0; w < mask_words; ++w) r += __popc(m[w]);
+    refcnt[c] = r;
+    live = r > 0;
+  }
+  live = __syncthreads_count(live);
+  if (threadIdx.x == 0 && live) atomicAdd(occupancy, live);
+}
+
+// Token-history writes (prompt uploads at admit, pending tokens before the
+// n-gram matcher): segment i = {seq, start, len, src_offset}.
+__global__ void hist_write_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ segs,
+                                  int32_t* hist, int64_t pos_stride) {
+  const int32_t* sg = segs + 4 * blockIdx.x;
+  int32_t* dst = hist + static_cast<int64_t>(sg[0]) * pos_stride + sg[1];
+  const int32_t* s = src + sg[3];
+  for (int j = threadIdx.x; j < sg[2]; j += blockDim.x) dst[j] = s[j];
+}
+
+}  // namespace ds
+
+extern "C" {
+
+int ds_kv_apply(const ds_kv_op* ops_dev, int n_ops, int32_t* pos2cell, int64_t pos_stride,
+                int n_seqs, uint32_t* member, int mask_words, int32_t* trie_ref,
+                ds_stream_t stream) {
+  if (n_ops < 0 || mask_words <= 0 || n_seqs > 32 * mask_words) return DS_EINVAL;
+  if (n_ops == 0) return DS_OK;
+  ds::kv_apply_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(ops_dev, n_ops, pos2cell, pos_stride,
+                                                            n_seqs, member, mask_words, trie_ref);
+  return (int)cudaGetLastError();
+}
+
+int ds_hist_write(const int32_t* src, const int32_t* segs, int n_segs, int32_t* hist,
+                  int64_t pos_stride, ds_stream_t stream) {
+  if (n_segs < 0) return DS_EINVAL;
+  if (n_segs == 0) return DS_OK;
+  ds::hist_write_kernel<<<n_segs, 256, 0, (cudaStream_t)stream>>>(src, segs, hist, pos_stride);
+  return (int)cudaGetLastError();
+}
+
+int ds_kv_refcount(const uint32_t* member, int mask_words, const int32_t* trie_ref,
+                   int64_t capacity, int32_t* refcnt_out, int32_t* occupancy_out,
+                   ds_stream_t stream) {
+  if (capacity <= 0 || mask_words <= 0) return DS_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t err = cudaMemsetAsync(occupancy_out, 0, sizeof(int32_t), s);
+  if (err != cudaSuccess) return (int)err;
+  const int blocks = static_cast<int>((capacity + 255) / 256);
+  ds::kv_refcount_kernel<<<blocks, 256, 0, s>>>(member, mask_words, trie_ref, capacity,
+                                                refcnt_out, occupancy_out);
+  return (int)cudaGetLastError();
+}
+
+}  // extern "C"

@@ -1,0 +1,183 @@
+// Element-wise / row kernels of the Llama-shaped forward: embedding gather,
+// RMSNorm, SwiGLU, and K5 (RoPE + KV store into the paged cell pool).
+// All HBM-bound; 128-bit vectorised where the row is.
+#include "../../include/deltaserve_b200.h"
+#include "common.cuh"
+
+namespace ds {
+
+__global__ void embed_kernel(const int32_t* __restrict__ tok, const uint4* __restrict__ table,
+                             int chunks, uint4* __restrict__ out) {
+  const int r = blockIdx.x;
+  const uint4* src = table + static_cast<int64_t>(tok[r]) * chunks;
+  uint4* dst = out + static_cast<int64_t>(r) * chunks;
+  for (int j = threadIdx.x; j < chunks; j += blockDim.x) dst[j] = __ldg(src + j);
+}
+
+// out[r] = x[rows[r]] * rsqrt(mean(x^2) + eps) * w   (fp32 math, one rounding)
+template <int BLOCK, int MAXC>
+__global__ void __launch_bounds__(BLOCK) rmsnorm_kernel(const uint4* __restrict__ x,
+                                                        const int32_t* __restrict__ rows,
+                                                        int chunks, const uint4* __restrict__ w,
+                                                        float eps, uint4* __restrict__ out) {
+  __shared__ float s_part[BLOCK / 32];
+  const int r = blockIdx.x;
+  const int src = rows ? rows[r] : r;
+  const uint4* xr = x + static_cast<int64_t>(src) * chunks;
+  uint4 v[MAXC];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < MAXC; ++k) {
+    const int j = threadIdx.x + k * BLOCK;
+    if (j < chunks) {
+      v[k] = __ldg(xr + j);
+      const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v[k]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(p[q]);
+        ss += f.x * f.x + f.y * f.y;
+      }
+    }
+  }
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < BLOCK / 32 ? s_part[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) s_part[0] = t;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(s_part[0] / static_cast<float>(chunks * 8) + eps);
+  uint4* orow = out + static_cast<int64_t>(r) * chunks;
+#pragma unroll
+  for (int k = 0; k < MAXC; ++k) {
+    const int j = threadIdx.x + k * BLOCK;
+    if (j < chunks) {
+      const uint4 wv = __ldg(w + j);
+      const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v[k]);
+      const __nv_bfloat162* pw = reinterpret_cast<const __nv_bfloat162*>(&wv);
+      uint4 o;
+      uint32_t* po = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(p[q]);
+        const float2 g = __bfloat1622float2(pw[q]);
+        po[q] = pack_bf16(f.x * inv * g.x, f.y * inv * g.y);
+      }
+      orow[j] = o;
+    }
+  }
+}
+
+// out[r][j] = silu(gu[r][j]) * gu[r][F + j]
+__global__ void silu_mul_kernel(const uint4* __restrict__ gu, int chunks, uint4* __restrict__ out) {
+  const int r = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= chunks) return;
+  const uint4 g = __ldg(gu + static_cast<int64_t>(r) * 2 * chunks + j);
+  const uint4 u = __ldg(gu + static_cast<int64_t>(r) * 2 * chunks + chunks + j);
+  const __nv_bfloat162* pg = reinterpret_cast<const __nv_bfloat162*>(&g);
+  const __nv_bfloat162* pu = reinterpret_cast<const __nv_bfloat162*>(&u);
+  uint4 o;
+  uint32_t* po = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 a = __bfloat1622float2(pg[q]);
+    const float2 b = __bfloat1622float2(pu[q]);
+    const float sa = a.x / (1.f + expf(-a.x));
+    const float sb = a.y / (1.f + expf(-a.y));
+    po[q] = pack_bf16(sa * b.x, sb * b.y);
+  }
+  out[static_cast<int64_t>(r) * chunks + j] = o;
+}
+
+// K5: rotate-half RoPE on q (in place) and k, store k and v rows into the
+// cell pool (layout [cell][kv_head][head_dim]).  One CTA per batch row.
+__global__ void rope_kv_store_kernel(__nv_bfloat16* __restrict__ qkv, const int32_t* row_seq,
+                                     const int32_t* row_pos, const int32_t* __restrict__ pos2cell,
+                                     int64_t pos_stride, int nh, int nkv, int hd,
+                                     const float* __restrict__ rope_cos,
+                                     const float* __restrict__ rope_sin,
+                                     __nv_bfloat16* __restrict__ k_pool,
+                                     __nv_bfloat16* __restrict__ v_pool) {
+  const int r = blockIdx.x;
+  const int pos = row_pos[r];
+  const int64_t cell = pos2cell[static_cast<int64_t>(row_seq[r]) * pos_stride + pos];
+  const int half = hd / 2;
+  const int width = (nh + 2 * nkv) * hd;
+  __nv_bfloat16* row = qkv + static_cast<int64_t>(r) * width;
+  const float* cs = rope_cos + static_cast<int64_t>(pos) * half;
+  const float* sn = rope_sin + static_cast<int64_t>(pos) * half;
+  const int n_pairs = (nh + nkv) * half;
+  for (int idx = threadIdx.x; idx < n_pairs; idx += blockDim.x) {
+    const int head = idx / half;
+    const int i = idx - head * half;
+    __nv_bfloat16* x = row + head * hd;
+    const float x1 = __bfloat162float(x[i]);
+    const float x2 = __bfloat162float(x[i + half]);
+    const float c = __ldg(cs + i), s = __ldg(sn + i);
+    const __nv_bfloat16 y1 = __float2bfloat16_rn(x1 * c - x2 * s);
+    const __nv_bfloat16 y2 = __float2bfloat16_rn(x2 * c + x1 * s);
+    x[i] = y1;
+    x[i + half] = y2;
+    if (head >= nh) {
+      __nv_bfloat16* kd = k_pool + (cell * nkv + (head - nh)) * hd;
+      kd[i] = y1;
+      kd[i + half] = y2;
+    }
+  }
+  // v: 16-byte chunks
+  const int vchunks = nkv * hd / 8;
+  const uint4* vsrc = reinterpret_cast<const uint4*>(row + (nh + nkv) * hd);
+  uint4* vdst = reinterpret_cast<uint4*>(v_pool + cell * nkv * hd);
+  for (int j = threadIdx.x; j < vchunks; j += blockDim.x) vdst[j] = vsrc[j];
+}
+
+}  // namespace ds
+
+extern "C" {
+
+int ds_embed(const int32_t* tokens, int n_rows, const void* table, int hidden, void* out,
+             ds_stream_t stream) {
+  if (n_rows < 0 || hidden % 8) return DS_EINVAL;
+  if (n_rows == 0) return DS_OK;
+  ds::embed_kernel<<<n_rows, 128, 0, (cudaStream_t)stream>>>(
+      tokens, static_cast<const uint4*>(table), hidden / 8, static_cast<uint4*>(out));
+  return (int)cudaGetLastError();
+}
+
+int ds_rmsnorm(const void* x, const int32_t* rows, int n_rows, int hidden, const void* w,
+               float eps, void* out, ds_stream_t stream) {
+  if (n_rows < 0 || hidden % 8 || hidden > 8 * 256 * 4) return DS_EINVAL;
+  if (n_rows == 0) return DS_OK;
+  ds::rmsnorm_kernel<256, 4><<<n_rows, 256, 0, (cudaStream_t)stream>>>(
+      static_cast<const uint4*>(x), rows, hidden / 8, static_cast<const uint4*>(w), eps,
+      static_cast<uint4*>(out));
+  return (int)cudaGetLastError();
+}
+
+int ds_silu_mul(const void* gate_up, int n_rows, int ffn, void* out, ds_stream_t stream) {
+  if (n_rows < 0 || ffn % 8) return DS_EINVAL;
+  if (n_rows == 0) return DS_OK;
+  const int chunks = ffn / 8;
+  dim3 grid((chunks + 127) / 128, n_rows);
+  ds::silu_mul_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(static_cast<const uint4*>(gate_up),
+                                                              chunks, static_cast<uint4*>(out));
+  return (int)cudaGetLastError();
+}
+
+int ds_rope_kv_store(void* qkv, int n_rows, const int32_t* row_seq, const int32_t* row_pos,
+                     const int32_t* pos2cell, int64_t pos_stride, int n_heads, int n_kv_heads,
+                     int head_dim, const float* rope_cos, const float* rope_sin, void* k_pool_l,
+                     void* v_pool_l, ds_stream_t stream) {
+  if (n_rows < 0 || head_dim % 16) return DS_EINVAL;
+  if (n_rows == 0) return DS_OK;
+  ds::rope_kv_store_kernel<<<n_rows, 256, 0, (cudaStream_t)stream>>>(
+      static_cast<__nv_bfloat16*>(qkv), row_seq, row_pos, pos2cell, pos_stride, n_heads,
+      n_kv_heads, head_dim, rope_cos, rope_sin, static_cast<__nv_bfloat16*>(k_pool_l),
+      static_cast<__nv_bfloat16*>(v_pool_l));
+  return (int)cudaGetLastError();
+}
+
+}  // extern "C"

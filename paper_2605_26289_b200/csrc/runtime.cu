@@ -1,0 +1,255 @@
+// Native forward runtime: one C call runs a whole plan batch through the
+// Llama-shaped decoder (cuBLAS bf16 GEMMs for the plain projections, our
+// kernels for everything else) and finishes with the token policy + verify
+// accept on device.  Realises engine.forward (engine.py:268-281) for all
+// entries of a BatchPlan (scheduler.py:652-772) without materialising the
+// context on the host: the context is the resident paged KV store.
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "../../include/deltaserve_b200.h"
+#include "attn_plan.h"
+#include "common.cuh"
+#include "internal.h"
+
+namespace ds {
+
+int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_entry* entries_dev,
+                      int n_entries, const void* k_pool, const void* v_pool,
+                      const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv, int hd,
+                      float scale, void* out, void* workspace, size_t ws_bytes,
+                      cudaStream_t stream);
+int launch_attn_prefill_sm100(const void* qkv, const ds_entry* entries_host,
+                              const ds_entry* entries_dev, int n_entries, const void* k_pool,
+                              const void* v_pool, const int32_t* pos2cell, int64_t pos_stride,
+                              int nh, int nkv, int hd, float scale, void* out,
+                              cudaStream_t stream);
+
+namespace {
+
+constexpr size_t kAlign = 256;
+constexpr size_t kCublasWs = 32u << 20;
+
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Runtime {
+  cublasHandle_t blas = nullptr;
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  int device = -1;
+};
+
+Runtime& runtime() {
+  static thread_local Runtime rt;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (rt.device != dev) {
+    if (rt.blas) cublasDestroy(rt.blas);
+    cublasCreate(&rt.blas);
+    cublasSetMathMode(rt.blas, CUBLAS_DEFAULT_MATH);
+    cudaStreamCreateWithFlags(&rt.side, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&rt.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&rt.join, cudaEventDisableTiming);
+    rt.device = dev;
+  }
+  return rt;
+}
+
+struct Carve {
+  uint8_t* p;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t bytes) {
+    T* r = reinterpret_cast<T*>(p + off);
+    off += align_up(bytes);
+    return r;
+  }
+};
+
+struct Buffers {
+  __nv_bfloat16 *x, *h, *qkv, *attn, *gu, *act, *hf;
+  uint64_t* row_hash;
+  void* attn_ws;
+  size_t attn_ws_bytes;
+  void* blas_ws;
+};
+
+size_t layout(const ds_model* m, int rows, int outs, Buffers* b, uint8_t* base) {
+  Carve c{base};
+  const size_t H = m->hidden, F = m->ffn;
+  const size_t QKV = static_cast<size_t>(m->n_heads + 2 * m->n_kv_heads) * m->head_dim;
+  const size_t A = static_cast<size_t>(m->n_heads) * m->head_dim;
+  Buffers t{};
+  t.x = c.take<__nv_bfloat16>(rows * H * 2);
+  t.h = c.take<__nv_bfloat16>(rows * H * 2);
+  t.qkv = c.take<__nv_bfloat16>(rows * QKV * 2);
+  t.attn = c.take<__nv_bfloat16>(rows * A * 2);
+  t.gu = c.take<__nv_bfloat16>(rows * 2 * F * 2);
+  t.act = c.take<__nv_bfloat16>(rows * F * 2);
+  t.hf = c.take<__nv_bfloat16>(static_cast<size_t>(outs) * H * 2);
+  t.row_hash = c.take<uint64_t>(static_cast<size_t>(outs) * 8);
+  t.attn_ws_bytes = attn_partial_bytes_bound();
+  t.attn_ws = c.take<uint8_t>(t.attn_ws_bytes);
+  t.blas_ws = c.take<uint8_t>(kCublasWs);
+  if (b) *b = t;
+  return c.off;
+}
+
+// Y[M][N] (row-major) = X[M][K] . W[N][K]^T  (+ beta*Y)
+cublasStatus_t gemm(cublasHandle_t h, const void* X, const void* W, void* Y, int M, int N, int K,
+                    float beta, cudaDataType_t ytype) {
+  const float alpha = 1.f;
+  return cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, &alpha, W, CUDA_R_16BF, K, X,
+                      CUDA_R_16BF, K, &beta, Y, ytype, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+}
+
+__global__ void scatter_tokens_kernel(const int32_t* tok, const int32_t* row_seq,
+                                      const int32_t* row_pos, int n, int32_t* hist,
+                                      int64_t stride) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) hist[static_cast<int64_t>(row_seq[r]) * stride + row_pos[r]] = tok[r];
+}
+
+}  // namespace
+}  // namespace ds
+
+using namespace ds;
+
+#define DS_CUDA(x)                                 \
+  do {                                             \
+    cudaError_t e_ = (x);                          \
+    if (e_ != cudaSuccess) return static_cast<int>(e_); \
+  } while (0)
+#define DS_BLAS(x)                                              \
+  do {                                                          \
+    cublasStatus_t s_ = (x);                                    \
+    if (s_ != CUBLAS_STATUS_SUCCESS) return 1000 + static_cast<int>(s_); \
+  } while (0)
+#define DS_CHECK(x)        \
+  do {                     \
+    int r_ = (x);          \
+    if (r_ != 0) return r_; \
+  } while (0)
+
+extern "C" {
+
+int ds_abi_version(void) { return 1; }
+
+const char* ds_status_string(int status) {
+  if (status == DS_OK) return "ok";
+  if (status == DS_EINVAL) return "invalid argument";
+  if (status == DS_EUNSUPPORTED) return "unsupported shape";
+  if (status == DS_EWORKSPACE) return "workspace too small";
+  if (status >= 1000) return "cublas error";
+  return cudaGetErrorString(static_cast<cudaError_t>(status));
+}
+
+size_t ds_attention_workspace_bytes(int n_rows, int n_entries, int n_heads, int head_dim) {
+  (void)n_rows;
+  (void)n_entries;
+  (void)n_heads;
+  (void)head_dim;
+  return attn_partial_bytes_bound();
+}
+
+int ds_attention(const void* qkv, const ds_entry* entries_host, const ds_entry* entries_dev,
+                 int n_entries, int n_rows, const void* k_pool_l, const void* v_pool_l,
+                 const int32_t* pos2cell, int64_t pos_stride, int n_heads, int n_kv_heads,
+                 int head_dim, float scale, void* out, void* workspace, size_t workspace_bytes,
+                 int impl, ds_stream_t stream) {
+  (void)n_rows;
+  if (n_entries <= 0 || n_kv_heads <= 0 || n_heads % n_kv_heads) return DS_EINVAL;
+  int max_q = 0;
+  for (int e = 0; e < n_entries; ++e) max_q = entries_host[e].q_len > max_q ? entries_host[e].q_len : max_q;
+  if (impl == 0) impl = 1;
+  if (impl == 2)
+    return launch_attn_prefill_sm100(qkv, entries_host, entries_dev, n_entries, k_pool_l, v_pool_l,
+                                     pos2cell, pos_stride, n_heads, n_kv_heads, head_dim, scale,
+                                     out, (cudaStream_t)stream);
+  return launch_attn_split(qkv, entries_host, entries_dev, n_entries, k_pool_l, v_pool_l, pos2cell,
+                           pos_stride, n_heads, n_kv_heads, head_dim, scale, out, workspace,
+                           workspace_bytes, (cudaStream_t)stream);
+}
+
+size_t ds_forward_workspace_bytes(const ds_model* model, int max_rows, int max_out,
+                                  int max_entries) {
+  (void)max_entries;
+  return layout(model, max_rows, max_out, nullptr, nullptr) + kAlign;
+}
+
+int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_args* a,
+                     ds_stream_t stream_) {
+  if (!m || !kv || !a || a->n_rows <= 0 || a->n_entries <= 0 || a->n_out <= 0) return DS_EINVAL;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  Runtime& rt = runtime();
+  uint8_t* base = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(a->workspace) + kAlign - 1) / kAlign * kAlign);
+  Buffers b;
+  const size_t need = layout(m, a->n_rows, a->n_out, &b, base);
+  if (need + kAlign > a->workspace_bytes) return DS_EWORKSPACE;
+
+  const int T = a->n_rows, H = m->hidden, L = m->layers, hd = m->head_dim;
+  const int nh = m->n_heads, nkv = m->n_kv_heads, F = m->ffn;
+  const int QKV = (nh + 2 * nkv) * hd;
+  const float scale = 1.f / sqrtf(static_cast<float>(hd));
+  const size_t kv_layer = static_cast<size_t>(kv->capacity) * nkv * hd;  // elements per layer
+  int max_q = 0;
+  for (int e = 0; e < a->n_entries; ++e)
+    max_q = a->entries_host[e].q_len > max_q ? a->entries_host[e].q_len : max_q;
+  const int attn_impl = 1;
+
+  DS_BLAS(cublasSetStream(rt.blas, stream));
+  DS_BLAS(cublasSetWorkspace(rt.blas, b.blas_ws, kCublasWs));
+
+  // batch tokens -> sequence history (the copy rule scans it), then the
+  // per-row FNV states on a side stream (overlaps the layer stack).
+  scatter_tokens_kernel<<<(T + 127) / 128, 128, 0, stream>>>(a->tokens, a->row_seq, a->row_pos, T,
+                                                             kv->hist, kv->pos_stride);
+  DS_CUDA(cudaGetLastError());
+  DS_CUDA(cudaEventRecord(rt.fork, stream));
+  DS_CUDA(cudaStreamWaitEvent(rt.side, rt.fork, 0));
+  launch_row_hash(a, kv, b.row_hash, rt.side);
+  DS_CUDA(cudaGetLastError());
+  DS_CUDA(cudaEventRecord(rt.join, rt.side));
+
+  DS_CHECK(ds_embed(a->tokens, T, m->embed, H, b.x, stream));
+  const __nv_bfloat16* wqkv = static_cast<const __nv_bfloat16*>(m->wqkv);
+  const __nv_bfloat16* wo = static_cast<const __nv_bfloat16*>(m->wo);
+  const __nv_bfloat16* wgu = static_cast<const __nv_bfloat16*>(m->w_gate_up);
+  const __nv_bfloat16* wd = static_cast<const __nv_bfloat16*>(m->w_down);
+  const __nv_bfloat16* an = static_cast<const __nv_bfloat16*>(m->attn_norm);
+  const __nv_bfloat16* mn = static_cast<const __nv_bfloat16*>(m->mlp_norm);
+  __nv_bfloat16* kp = static_cast<__nv_bfloat16*>(kv->k_pool);
+  __nv_bfloat16* vp = static_cast<__nv_bfloat16*>(kv->v_pool);
+  for (int l = 0; l < L; ++l) {
+    DS_CHECK(ds_rmsnorm(b.x, nullptr, T, H, an + static_cast<size_t>(l) * H, m->rms_eps, b.h, stream));
+    DS_BLAS(gemm(rt.blas, b.h, wqkv + static_cast<size_t>(l) * QKV * H, b.qkv, T, QKV, H, 0.f,
+                 CUDA_R_16BF));
+    DS_CHECK(ds_rope_kv_store(b.qkv, T, a->row_seq, a->row_pos, kv->pos2cell, kv->pos_stride, nh,
+                              nkv, hd, m->rope_cos, m->rope_sin, kp + l * kv_layer,
+                              vp + l * kv_layer, stream));
+    DS_CHECK(ds_attention(b.qkv, a->entries_host, a->entries, a->n_entries, T, kp + l * kv_layer,
+                          vp + l * kv_layer, kv->pos2cell, kv->pos_stride, nh, nkv, hd, scale,
+                          b.attn, b.attn_ws, b.attn_ws_bytes, attn_impl, stream));
+    DS_BLAS(gemm(rt.blas, b.attn, wo + static_cast<size_t>(l) * H * nh * hd, b.x, T, H, nh * hd,
+                 1.f, CUDA_R_16BF));
+    DS_CHECK(ds_rmsnorm(b.x, nullptr, T, H, mn + static_cast<size_t>(l) * H, m->rms_eps, b.h, stream));
+    DS_BLAS(gemm(rt.blas, b.h, wgu + static_cast<size_t>(l) * 2 * F * H, b.gu, T, 2 * F, H, 0.f,
+                 CUDA_R_16BF));
+    DS_CHECK(ds_silu_mul(b.gu, T, F, b.act, stream));
+    DS_BLAS(gemm(rt.blas, b.act, wd + static_cast<size_t>(l) * H * F, b.x, T, H, F, 1.f,
+                 CUDA_R_16BF));
+  }
+  // final norm on sampled rows only, LM head in fp32
+  DS_CHECK(ds_rmsnorm(b.x, a->out_rows, a->n_out, H, m->final_norm, m->rms_eps, b.hf, stream));
+  DS_BLAS(gemm(rt.blas, b.hf, m->lm_head, a->logits, a->n_out, m->vocab, H, 0.f, CUDA_R_32F));
+
+  DS_CUDA(cudaStreamWaitEvent(stream, rt.join, 0));
+  launch_token_policy(a, kv, b.row_hash, nullptr, m->vocab, rt.side, stream);
+  DS_CUDA(cudaGetLastError());
+  return DS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,469 @@
+"""GpuEngine: the device realisation of the reference engine boundary.
+
+The reference ``MockEngine.forward(context, batch)`` (engine.py:268-281)
+materialises the whole context on the host every call.  Here the context is
+the resident paged KV store and the sequence's token history on the device;
+a forward ships only the batch tokens plus a few int32 of metadata (one
+pinned H2D), runs the whole Llama-shaped decoder in ONE native call
+(``ds_model_forward``: cuBLAS GEMMs + our sm_100a kernels), evaluates the
+token policy and the verify accept loop on device, and returns only the
+chosen ids, copy sources and accept counts (one small D2H).
+
+Token policies:
+* ``copy``   - the reference copy-model rule (engine.py:196-216) evaluated by
+  the K2 kernel over the device token history: bit-exact transcripts versus
+  the reference InferenceCore while every FLOP and byte of the real model runs.
+* ``argmax`` - greedy argmax of the real logits (K8, lowest id on ties).
+
+The ledger keeps the reference's per-entry semantics (engine.py:72-102).
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib
+from .config import CoreConfig
+from .kernels import FNV64_OFFSET, host_fnv1a64_tokens
+from .kvcache import UnifiedKvCache
+
+_ENTRY_DT = np.dtype([("seq", "<i4"), ("past", "<i4"), ("q_len", "<i4"), ("q_start", "<i4"),
+                      ("kind", "<i4"), ("n_draft", "<i4"), ("out_start", "<i4"),
+                      ("n_out", "<i4"), ("hash_in", "<u8")])
+assert _ENTRY_DT.itemsize == 40
+
+
+class CostLedger:
+    """Monotonic forward-pass counters (engine.py:72-102)."""
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self.prefill_tokens = 0
+        self.decode_passes = 0
+        self.forward_calls = 0
+        self.batch_tokens = 0
+
+    def count_forward(self, batch_size: int) -> None:
+        with self._lock:
+            self.forward_calls += 1
+            self.batch_tokens += batch_size
+
+    def charge_prefill(self, n: int) -> None:
+        with self._lock:
+            self.prefill_tokens += n
+
+    def charge_decode(self) -> None:
+        with self._lock:
+            self.decode_passes += 1
+
+    def snapshot(self) -> dict:
+        with self._lock:
+            return {"prefill_tokens": self.prefill_tokens, "decode_passes": self.decode_passes,
+                    "forward_calls": self.forward_calls, "batch_tokens": self.batch_tokens}
+
+
+@dataclass
+class RowResult:
+    """One sampled position: the reference Logits' argmax_id / copy_source."""
+
+    argmax_id: int
+    copy_source: int | None
+
+
+@dataclass
+class VerifyResult:
+    accepted: int
+    rows: list
+
+
+@dataclass
+class EntryRequest:
+    """One plan entry for a (possibly batched) forward."""
+
+    kind: int          # _lib.ENTRY_*
+    seq: int
+    past: int
+    batch: list        # tokens forwarded
+    tokens: list       # full committed token list of the slot (for the prefix hash)
+    n_draft: int = 0
+
+
+class _Staging:
+    """Growable pinned-host + device int32 buffer; one H2D per flush."""
+
+    def __init__(self, device, words: int = 1 << 16):
+        self.device = device
+        self._alloc(words)
+        self.reset()
+
+    def _alloc(self, words):
+        self.host = torch.empty(words, dtype=torch.int32, pin_memory=True)
+        self.host_np = self.host.numpy()
+        self.dev = torch.empty(words, dtype=torch.int32, device=self.device)
+
+    def reset(self):
+        self.parts: list[tuple[int, np.ndarray]] = []
+        self.n = 0
+
+    def add(self, arr: np.ndarray) -> int:
+        a = np.ascontiguousarray(arr).view(np.int32).reshape(-1)
+        off = self.n
+        self.parts.append((off, a))
+        self.n = off + ((a.size + 3) // 4) * 4  # 16-byte aligned parts
+        return off
+
+    def upload(self) -> None:
+        if self.n > self.host.numel():
+            torch.cuda.current_stream().synchronize()
+            self._alloc(max(self.n, 2 * self.host.numel()))
+        for off, a in self.parts:
+            self.host_np[off:off + a.size] = a
+        if self.n:
+            self.dev[: self.n].copy_(self.host[: self.n], non_blocking=True)
+
+    def dptr(self, off: int) -> int:
+        return self.dev.data_ptr() + 4 * off
+
+    def hptr(self, off: int) -> int:
+        return self.host.data_ptr() + 4 * off
+
+
+class GpuEngine:
+    """Weights, paged KV store and the per-forward plumbing on one B200."""
+
+    def __init__(self, cfg: CoreConfig, kv: UnifiedKvCache, n_seqs: int, device=None,
+                 weights: dict | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("GpuEngine needs a CUDA device (no CPU fallback)")
+        self.cfg = cfg
+        self.shape = s = cfg.shape
+        self.kv = kv
+        kv.record_ops = True
+        self.ledger = CostLedger()
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.policy = {"copy": _lib.POLICY_COPY, "argmax": _lib.POLICY_ARGMAX}[cfg.token_policy]
+        self.n_seqs = n_seqs
+        self.capacity = kv.capacity_cells
+        self.pos_stride = self.capacity
+        dev = self.device
+        L = lib()
+
+        # ---- weights (random init N(0, 0.02), norms = 1) ----
+        self.w = weights if weights is not None else self._init_weights(cfg.seed)
+        # ---- RoPE tables (float64 angles -> fp32) ----
+        inv = cfg.shape.rope_theta ** (-torch.arange(0, s.head_dim, 2, dtype=torch.float64,
+                                                      device=dev) / s.head_dim)
+        pos = torch.arange(self.pos_stride, dtype=torch.float64, device=dev)
+        ang = pos[:, None] * inv[None, :]
+        self.rope_cos = torch.cos(ang).float().contiguous()
+        self.rope_sin = torch.sin(ang).float().contiguous()
+        del ang, pos
+        # ---- paged KV store ----
+        cell = s.n_kv_heads * s.head_dim
+        self.k_pool = torch.zeros((s.layers, self.capacity, cell), dtype=torch.bfloat16, device=dev)
+        self.v_pool = torch.zeros_like(self.k_pool)
+        self.pos2cell = torch.zeros((n_seqs, self.pos_stride), dtype=torch.int32, device=dev)
+        self.hist = torch.zeros((n_seqs, self.pos_stride), dtype=torch.int32, device=dev)
+        self.mask_words = (n_seqs + 31) // 32
+        self.member = torch.zeros((self.capacity, self.mask_words), dtype=torch.int32, device=dev)
+        self.trie_ref = torch.zeros(self.capacity, dtype=torch.int32, device=dev)
+
+        # ---- per-forward buffers ----
+        self.max_out = (cfg.spec_max_lookahead + 1) * (n_seqs if cfg.batched_forward else 1)
+        self.max_entries = n_seqs if cfg.batched_forward else 1
+        self.max_rows = cfg.n_batch + self.max_out
+        self.logits = torch.empty((self.max_out, s.vocab), dtype=torch.float32, device=dev)
+        self.res_dev = torch.zeros(2 * self.max_out + self.max_entries, dtype=torch.int32, device=dev)
+        self.res_host = torch.zeros_like(self.res_dev, device="cpu").pin_memory()
+        self.stage = _Staging(dev)
+        self.k1_dev = torch.zeros(4 * n_seqs + n_seqs * cfg.spec_max_lookahead + 16,
+                                  dtype=torch.int32, device=dev)
+        self.k1_host = torch.zeros_like(self.k1_dev, device="cpu").pin_memory()
+
+        self.model_c = _lib.Model(
+            s.layers, s.hidden, s.n_heads, s.n_kv_heads, s.head_dim, s.ffn, s.vocab, s.rms_eps,
+            self.w["embed"].data_ptr(), self.w["attn_norm"].data_ptr(), self.w["wqkv"].data_ptr(),
+            self.w["wo"].data_ptr(), self.w["mlp_norm"].data_ptr(), self.w["w_gate_up"].data_ptr(),
+            self.w["w_down"].data_ptr(), self.w["final_norm"].data_ptr(),
+            self.w["lm_head"].data_ptr(), self.rope_cos.data_ptr(), self.rope_sin.data_ptr(),
+            self.pos_stride)
+        self.kv_c = _lib.KvStore(self.k_pool.data_ptr(), self.v_pool.data_ptr(), self.capacity,
+                                 self.pos2cell.data_ptr(), self.hist.data_ptr(), self.pos_stride,
+                                 n_seqs)
+        ws = L.ds_forward_workspace_bytes(ctypes.byref(self.model_c), self.max_rows,
+                                          self.max_out, self.max_entries)
+        self.workspace = torch.empty(ws, dtype=torch.uint8, device=dev)
+        self._hash: dict[int, tuple[int, int]] = {}   # seq -> (length, FNV64 of hist[:length])
+        self._pending_hist: list[tuple[int, int, np.ndarray]] = []
+        self.gpu_launches = 0
+        self._ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        self.reset_counters()
+
+    # -- instrumentation ------------------------------------------------------------
+
+    def reset_counters(self) -> None:
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+        self._fwd = {"prefill": [0, 0.0, 0, 0], "decode": [0, 0.0, 0, 0]}  # n, s, rows, kv
+
+    def device_seconds(self) -> float:
+        return sum(v[1] for v in self._fwd.values())
+
+    def forward_stats(self) -> dict:
+        return {k: {"n": v[0], "seconds": v[1], "rows": v[2],
+                    "mean_kv_len": (v[3] / v[0]) if v[0] else 0.0} for k, v in self._fwd.items()}
+
+    # -- weights ------------------------------------------------------------------
+
+    def _init_weights(self, seed: int) -> dict:
+        s, dev = self.shape, self.device
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+
+        def randn(*shape):
+            t = torch.empty(shape, dtype=torch.bfloat16, device=dev)
+            t.normal_(0.0, 0.02, generator=g)
+            return t
+
+        ones = lambda *shape: torch.ones(shape, dtype=torch.bfloat16, device=dev)  # noqa: E731
+        return {
+            "embed": randn(s.vocab, s.hidden),
+            "attn_norm": ones(s.layers, s.hidden),
+            "wqkv": randn(s.layers, s.qkv_width, s.hidden),
+            "wo": randn(s.layers, s.hidden, s.n_heads * s.head_dim),
+            "mlp_norm": ones(s.layers, s.hidden),
+            "w_gate_up": randn(s.layers, 2 * s.ffn, s.hidden),
+            "w_down": randn(s.layers, s.hidden, s.ffn),
+            "final_norm": ones(s.hidden),
+            "lm_head": randn(s.vocab, s.hidden),
+        }
+
+    # -- host-side state ------------------------------------------------------------
+
+    def load_prompt(self, seq: int, tokens, cursor: int, prefix_hash: int) -> None:
+        """New request on `seq`: its token history is (re)uploaded with the next
+        flush; the committed-prefix hash restarts from the scheduler's
+        prefix_hash (scheduler.py:237)."""
+        self._pending_hist.append((seq, 0, np.asarray(tokens, dtype=np.int32)))
+        self._hash[seq] = (cursor, prefix_hash)
+
+    def _hash_in(self, seq: int, past: int, tokens) -> int:
+        ln, st = self._hash.get(seq, (0, FNV64_OFFSET))
+        if ln > past:
+            ln, st = 0, FNV64_OFFSET
+        if past > ln:
+            st = host_fnv1a64_tokens(tokens[ln:past], st)
+        self._hash[seq] = (past, st)
+        return st
+
+    def _stage_metadata(self) -> tuple[int, int, int, int]:
+        """Queue pending hist writes and kv ops; returns offsets for the flush."""
+        segs_off = ops_off = -1
+        n_segs = n_ops = 0
+        if self._pending_hist:
+            segs = np.zeros((len(self._pending_hist), 4), dtype=np.int32)
+            data = []
+            cur = 0
+            for i, (seq, start, toks) in enumerate(self._pending_hist):
+                segs[i] = (seq, start, len(toks), cur)
+                data.append(toks)
+                cur += len(toks)
+            data_off = self.stage.add(np.concatenate(data) if cur else np.zeros(1, np.int32))
+            segs[:, 3] += data_off
+            segs_off = self.stage.add(segs)
+            n_segs = len(segs)
+            self._pending_hist = []
+        ops = self.kv.take_ops()
+        if ops:
+            ops_off = self.stage.add(np.asarray(ops, dtype=np.int32))
+            n_ops = len(ops)
+        return segs_off, n_segs, ops_off, n_ops
+
+    def _apply_metadata(self, segs_off, n_segs, ops_off, n_ops, stream) -> None:
+        L = lib()
+        if n_segs:
+            check(L.ds_hist_write(self.stage.dev.data_ptr(), self.stage.dptr(segs_off), n_segs,
+                                  self.hist.data_ptr(), self.pos_stride, stream), "ds_hist_write")
+            self.gpu_launches += 1
+        if n_ops:
+            check(L.ds_kv_apply(self.stage.dptr(ops_off), n_ops, self.pos2cell.data_ptr(),
+                                self.pos_stride, self.n_seqs, self.member.data_ptr(),
+                                self.mask_words, self.trie_ref.data_ptr(), stream), "ds_kv_apply")
+            self.gpu_launches += 1
+
+    def flush(self) -> None:
+        """Push pending metadata (page-table ops, history writes) to the device."""
+        stream = torch.cuda.current_stream()
+        self.stage.reset()
+        meta = self._stage_metadata()
+        self.stage.upload()
+        self._apply_metadata(*meta, stream.cuda_stream)
+
+    # -- forward -------------------------------------------------------------------
+
+    def run(self, reqs: list[EntryRequest]) -> list:
+        """Execute entries in one native forward; returns RowResult / VerifyResult."""
+        n_e = len(reqs)
+        if n_e == 0:
+            return []
+        if n_e > self.max_entries:
+            raise ValueError(f"{n_e} entries > engine max {self.max_entries}")
+        ents = np.zeros(n_e, dtype=_ENTRY_DT)
+        toks, rseq, rpos, orow = [], [], [], []
+        q_start = out_start = 0
+        for i, r in enumerate(reqs):
+            q = len(r.batch)
+            if q == 0:
+                raise ValueError("batch must be non-empty")
+            n_out = q if r.kind == _lib.ENTRY_VERIFY else 1
+            ents[i] = (r.seq, r.past, q, q_start, r.kind, r.n_draft, out_start, n_out,
+                       self._hash_in(r.seq, r.past, r.tokens))
+            toks.append(np.asarray(r.batch, dtype=np.int32))
+            rseq.append(np.full(q, r.seq, dtype=np.int32))
+            rpos.append(np.arange(r.past, r.past + q, dtype=np.int32))
+            orow.append(np.arange(q_start + q - n_out, q_start + q, dtype=np.int32))
+            q_start += q
+            out_start += n_out
+            self.ledger.count_forward(q)
+        if q_start > self.max_rows or out_start > self.max_out:
+            raise ValueError("forward exceeds engine buffers")
+        st = self.stage
+        st.reset()
+        meta = self._stage_metadata()
+        o_ent = st.add(ents.view(np.int32))
+        o_tok = st.add(np.concatenate(toks))
+        o_seq = st.add(np.concatenate(rseq))
+        o_pos = st.add(np.concatenate(rpos))
+        o_out = st.add(np.concatenate(orow))
+        st.upload()
+        self.h2d_bytes += 4 * st.n
+        stream = torch.cuda.current_stream()
+        sp = stream.cuda_stream
+        self._apply_metadata(*meta, sp)
+        res = self.res_dev
+        self._ev[0].record(stream)
+        args = _lib.ForwardArgs(
+            n_e, q_start, out_start, self.policy, self.cfg.copy_min_match, self.cfg.vocab,
+            st.hptr(o_ent), st.dptr(o_ent), st.dptr(o_tok), st.dptr(o_seq), st.dptr(o_pos),
+            st.dptr(o_out), res.data_ptr(), res.data_ptr() + 4 * self.max_out,
+            res.data_ptr() + 8 * self.max_out, self.logits.data_ptr(),
+            self.workspace.data_ptr(), self.workspace.numel())
+        check(lib().ds_model_forward(ctypes.byref(self.model_c), ctypes.byref(self.kv_c),
+                                     ctypes.byref(args), sp), "ds_model_forward")
+        self.gpu_launches += self.launches_per_forward(reqs)
+        self._ev[1].record(stream)
+        self.res_host.copy_(res, non_blocking=True)
+        self.d2h_bytes += 4 * res.numel()
+        stream.synchronize()
+        kind = "prefill" if any(r.kind == _lib.ENTRY_PREFILL for r in reqs) else "decode"
+        f = self._fwd[kind]
+        f[0] += 1
+        f[1] += self._ev[0].elapsed_time(self._ev[1]) / 1000.0
+        f[2] += q_start
+        f[3] += sum(r.past + len(r.batch) for r in reqs)
+        h = self.res_host.numpy()
+        tok, src, acc = h[: self.max_out], h[self.max_out: 2 * self.max_out], h[2 * self.max_out:]
+        out = []
+        for i, r in enumerate(reqs):
+            o0, n_out = int(ents[i]["out_start"]), int(ents[i]["n_out"])
+            rows = [RowResult(int(tok[o0 + j]), None if src[o0 + j] < 0 else int(src[o0 + j]))
+                    for j in range(n_out)]
+            out.append(VerifyResult(int(acc[i]), rows) if r.kind == _lib.ENTRY_VERIFY else rows[0])
+        return out
+
+    def launches_per_forward(self, reqs) -> int:
+        """Our kernels per ds_model_forward (cuBLAS GEMMs not counted): scatter,
+        row-hash, embed; per layer 2 rmsnorm + rope/kv-store + attention (+combine)
+        + silu_mul; final rmsnorm, token policy, verify-accept."""
+        per_layer = 5 + (1 if any(r.past + len(r.batch) > 128 for r in reqs) else 0)
+        return 3 + self.shape.layers * per_layer + 3
+
+    # convenience wrappers used by the scheduler (one entry per call)
+    def forward_prefill(self, seq, past, batch, tokens) -> RowResult:
+        return self.run([EntryRequest(_lib.ENTRY_PREFILL, seq, past, list(batch), tokens)])[0]
+
+    def forward_decode(self, seq, past, token, tokens) -> RowResult:
+        return self.run([EntryRequest(_lib.ENTRY_DECODE, seq, past, [token], tokens)])[0]
+
+    def forward_verify(self, seq, past, batch, tokens, hash_in=None) -> VerifyResult:
+        return self.run([EntryRequest(_lib.ENTRY_VERIFY, seq, past, list(batch), tokens,
+                                      n_draft=len(batch) - 1)])[0]
+
+    # -- K1: batched prompt-lookup proposals -----------------------------------------
+
+    def propose(self, slots: list[tuple[int, list, int]], window: int, min_match: int) -> list:
+        """Drafts for many decoding slots in one launch.
+
+        slots: (seq, tokens, cap) with tokens the full committed list (its last
+        element is pending, not yet in the device history).  The ring is
+        tokens[-window:] and the tail is the ring (scheduler.py:531-532).
+        """
+        n = len(slots)
+        if n == 0:
+            return []
+        for seq, tokens, _ in slots:
+            self._pending_hist.append((seq, len(tokens) - 1, np.asarray(tokens[-1:], np.int32)))
+        offs = np.zeros(n, dtype=np.int64)
+        lens = np.zeros(n, dtype=np.int32)
+        caps = np.zeros(n, dtype=np.int32)
+        for i, (seq, tokens, cap) in enumerate(slots):
+            ln = min(len(tokens), window)
+            offs[i] = seq * self.pos_stride + len(tokens) - ln
+            lens[i] = ln
+            caps[i] = cap
+        max_draft = max(1, int(caps.max()))
+        st = self.stage
+        st.reset()
+        meta = self._stage_metadata()
+        o_off = st.add(offs.view(np.int32))
+        o_len = st.add(lens)
+        o_cap = st.add(caps)
+        st.upload()
+        self.h2d_bytes += 4 * st.n
+        stream = torch.cuda.current_stream()
+        sp = stream.cuda_stream
+        self._apply_metadata(*meta, sp)
+        k1 = self.k1_dev
+        need = 3 * n + n * max_draft
+        if need > k1.numel():
+            raise ValueError("too many slots for the K1 buffer")
+        e_p, l_p, dl_p, d_p = (k1.data_ptr(), k1.data_ptr() + 4 * n, k1.data_ptr() + 8 * n,
+                               k1.data_ptr() + 12 * n)
+        hp = self.hist.data_ptr()
+        check(lib().ds_longest_suffix_match(hp, st.dptr(o_off), st.dptr(o_len), hp,
+                                            st.dptr(o_off), st.dptr(o_len), n, min_match,
+                                            st.dptr(o_cap), max_draft, e_p, l_p, d_p, dl_p, sp),
+              "ds_longest_suffix_match")
+        self.gpu_launches += 1
+        self.k1_host[:need].copy_(k1[:need], non_blocking=True)
+        self.d2h_bytes += 4 * need
+        stream.synchronize()
+        h = self.k1_host.numpy()
+        dl = h[2 * n: 3 * n]
+        d = h[3 * n: 3 * n + n * max_draft].reshape(n, max_draft)
+        return [d[i, : dl[i]].tolist() for i in range(n)]
+
+    # -- diagnostics -------------------------------------------------------------------
+
+    def device_refcounts(self) -> tuple[np.ndarray, int]:
+        """popcount(member)+trie_ref per cell and the device occupancy."""
+        self.flush()
+        rc = torch.empty(self.capacity, dtype=torch.int32, device=self.device)
+        occ = torch.zeros(1, dtype=torch.int32, device=self.device)
+        check(lib().ds_kv_refcount(self.member.data_ptr(), self.mask_words,
+                                   self.trie_ref.data_ptr(), self.capacity, rc.data_ptr(),
+                                   occ.data_ptr(), torch.cuda.current_stream().cuda_stream),
+              "ds_kv_refcount")
+        return rc.cpu().numpy(), int(occ.item())
+
+    def device_cells(self, seq: int, n: int) -> list[int]:
+        self.flush()
+        return self.pos2cell[seq, :n].cpu().tolist()
+
+    def weights_cpu(self) -> dict:
+        return {k: v.float().cpu() for k, v in self.w.items()}

@@ -1,0 +1,133 @@
+"""Synthetic multi-turn workloads: replay of reference-generated traces.
+
+The traces under tests/golden/traces/ were produced by driving the reference
+InferenceCore with its own scenario generators (scenarios.py:121-188; see
+tests/golden/make_golden.py).  Each request carries its full prompt token ids
+and pieces (delta coded per conversation stream), its parameters, the wave it
+was submitted in, and the reference's result counters.  Under the copy token
+policy our engine regenerates the reference transcripts, so replaying the
+recorded prompts is the same conversation; the recorded results are the
+parity oracle.
+"""
+from __future__ import annotations
+
+import gzip
+import json
+import os
+import time
+from dataclasses import dataclass
+
+from .kernels import prompt_seed
+
+TRACE_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests",
+                         "golden", "traces")
+
+RESULT_FIELDS = ("generated", "finish_reason", "n_t", "cached_prompt_tokens", "prefill_tokens",
+                 "decode_passes", "spec_proposed", "spec_accepted", "spec_rejected",
+                 "aliased_cells", "early_stopped", "text")
+
+
+@dataclass
+class TraceRequest:
+    id: str
+    wave: int
+    stream: str
+    tokens: list
+    pieces: list
+    max_tokens: int
+    tools: frozenset
+    expect: dict
+
+
+def load_trace(name: str) -> dict:
+    path = name if os.path.exists(name) else os.path.join(TRACE_DIR, f"{name}.json.gz")
+    with gzip.open(path, "rb") as fh:
+        tr = json.loads(fh.read())
+    last: dict[str, tuple[list, list]] = {}
+    reqs = []
+    for r in tr["requests"]:
+        pt, pp = last.get(r["stream"], ([], []))
+        toks = pt[: r["common"]] + r["tokens"]
+        pieces = pp[: r["common"]] + r["pieces"]
+        last[r["stream"]] = (toks, pieces)
+        reqs.append(TraceRequest(r["id"], r["wave"], r["stream"], toks, pieces, r["max_tokens"],
+                                 frozenset(r["tools"]), r.get("expect", {})))
+    tr["reqs"] = reqs
+    return tr
+
+
+def waves(trace: dict) -> list[list[TraceRequest]]:
+    out: dict[int, list] = {}
+    for r in trace["reqs"]:
+        out.setdefault(r.wave, []).append(r)
+    return [out[k] for k in sorted(out)]
+
+
+@dataclass
+class TurnRecord:
+    req: TraceRequest
+    result: object
+    latency_ms: float
+
+
+def replay(core, trace: dict, wave_limit: int | None = None, max_iters: int = 200_000,
+           rid_suffix: str = "") -> list[TurnRecord]:
+    """Submit each wave's requests together and step the core until they finish."""
+    from .scheduler import GenerationRequest, RequestHandle
+
+    records: list[TurnRecord] = []
+    for wi, wave in enumerate(waves(trace)):
+        if wave_limit is not None and wi >= wave_limit:
+            break
+        handles = []
+        for r in wave:
+            guard = core.pool.acquire("transient", timeout=1.0)
+            req = GenerationRequest(request_id=r.id + rid_suffix, prompt_tokens=list(r.tokens),
+                                    prompt_pieces=list(r.pieces), max_tokens=r.max_tokens,
+                                    temperature=0.0, seed=prompt_seed(r.tokens),
+                                    declared_tools=r.tools, guard=guard)
+            h = RequestHandle(req)
+            core.submit(h)
+            handles.append((r, h))
+        pending = [h for _, h in handles]
+        it = 0
+        while pending:
+            core.step()
+            it += 1
+            now = time.monotonic()
+            still = []
+            for h in pending:
+                if h.wait(timeout=0):
+                    h.completed_at = h.completed_at or now
+                else:
+                    still.append(h)
+            pending = still
+            if it > max_iters:
+                raise RuntimeError("wave did not complete")
+        for r, h in handles:
+            if h.error is not None:
+                raise h.error
+            records.append(TurnRecord(r, h.result, (h.completed_at - h.submitted_at) * 1000.0))
+    return records
+
+
+def mismatches(records: list[TurnRecord]) -> list[str]:
+    """Field-by-field comparison with the reference results (empty = parity)."""
+    bad = []
+    for rec in records:
+        exp = rec.req.expect
+        for f in RESULT_FIELDS:
+            got = getattr(rec.result, f)
+            if f in exp and got != exp[f]:
+                bad.append(f"{rec.req.id}.{f}: got {str(got)[:120]} expected {str(exp[f])[:120]}")
+        if "finalize" in exp and rec.result.finalize.kind != exp["finalize"]:
+            bad.append(f"{rec.req.id}.finalize: {rec.result.finalize.kind} != {exp['finalize']}")
+    return bad
+
+
+def core_config_for(trace: dict, **overrides):
+    """CoreConfig with the reference ServerConfig overrides the trace ran with."""
+    from .config import CoreConfig
+
+    cfg = CoreConfig().with_overrides(**trace["config"])
+    return cfg.with_overrides(**overrides) if overrides else cfg

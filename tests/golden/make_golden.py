@@ -1,0 +1,469 @@
+"""Generate the golden fixtures under tests/golden/ from the REFERENCE itself.
+
+Run here (the reference exists only in this container):
+
+    bash oracle/build_ref.sh && python tests/golden/make_golden.py
+
+It imports the unmodified reference (``deltaserve`` built into oracle/_ref from
+/root/reference/pkg) and records its outputs on seeded inputs:
+
+* ``kernels.json``   - FNV-1a 32/64, copy_continuation, longest_suffix_match,
+                       lookup_ngram and copy-policy rows
+                       (reference: _kernels/_native.pyx:18-119, engine.py:196-216,
+                       speculator.py:52-65).
+* ``kvcache_ops.json`` - random UnifiedKvCache op sequences with every observable
+                       after each op (kvcache.py:71-293).
+* ``radix_ops.json``  - random RadixTrie save/lookup/evict sequences (radix.py:81-222).
+* ``traces/*.json.gz`` - scenario transcripts driven through the reference
+                       ``InferenceCore`` (scheduler.py) for BASELINE configs C1-C5:
+                       every request's prompt (delta coded), pieces, parameters and
+                       the reference's result counters; used both for transcript
+                       parity and as the bench workload.
+
+The fixtures are committed; nothing on the GPU box reads /root/reference.
+"""
+from __future__ import annotations
+
+import gzip
+import json
+import os
+import random
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
+
+import numpy as np  # noqa: E402
+
+from deltaserve import _kernels as K  # noqa: E402
+from deltaserve.caches import prompt_seed  # noqa: E402
+from deltaserve.config import ServerConfig  # noqa: E402
+from deltaserve.engine import MockEngine, ModelConfig  # noqa: E402
+from deltaserve.kvcache import CapacityExhausted, DonorRangeInvalid, UnifiedKvCache  # noqa: E402
+from deltaserve.radix import BudgetExceeded, RadixTrie  # noqa: E402
+from deltaserve.scenarios import (  # noqa: E402
+    Scenario,
+    agent_scenario,
+    agentic_6turn,
+    burst_prompts,
+    deep_workflow,
+    turn_tool_result,
+)
+from deltaserve.scheduler import GenerationRequest, InferenceCore, RequestHandle  # noqa: E402
+from deltaserve.speculator import lookup_ngram  # noqa: E402
+
+assert K.BACKEND == "native"
+
+
+def dump(name, obj, gz=False):
+    path = os.path.join(HERE, name)
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    data = json.dumps(obj, separators=(",", ":")).encode()
+    if gz:
+        with gzip.GzipFile(path, "wb", mtime=0) as fh:
+            fh.write(data)
+    else:
+        with open(path, "wb") as fh:
+            fh.write(data)
+    print(f"wrote {path} ({len(data)} bytes raw)")
+
+
+# ---------------------------------------------------------------------------
+# kernels
+# ---------------------------------------------------------------------------
+
+def rand_tokens(rng, n, alpha):
+    return [rng.randrange(alpha) for _ in range(n)]
+
+
+def gen_kernels():
+    rng = random.Random(20251017)
+    out = {"fnv_bytes": [], "fnv_tokens": [], "copy_continuation": [], "suffix_match": [],
+           "lookup_ngram": [], "copy_policy": []}
+    for data in [b"", b"a", b"hello world", bytes(range(256)), b'{"name"']:
+        out["fnv_bytes"].append({"hex": data.hex(), "f32": K.fnv1a32_bytes(data),
+                                 "f64": K.fnv1a64_bytes(data)})
+    tok_cases = [[], [1], [70000], [-1, 0, 2**31 - 1, -2**31], [5, 6, 7, 5, 6]]
+    for _ in range(60):
+        tok_cases.append(rand_tokens(rng, rng.randrange(0, 300), rng.choice([8, 1000, 2**31 - 1])))
+    for toks in tok_cases:
+        st32 = rng.randrange(2**32)
+        st64 = rng.randrange(2**64)
+        out["fnv_tokens"].append({
+            "tokens": toks, "f32": K.fnv1a32_tokens(toks), "f64": K.fnv1a64_tokens(toks),
+            "state32": st32, "f32s": K.fnv1a32_tokens(toks, st32),
+            "state64": st64, "f64s": K.fnv1a64_tokens(toks, st64)})
+    # copy_continuation: known answer + random (sizes up to 4096)
+    cc = [([5, 6, 7, 5, 6], 2), ([], 3), ([1, 2, 3], 3), ([1, 1, 1, 1], 0), ([7, 8, 9, 7, 8], 2)]
+    for _ in range(400):
+        n = rng.randrange(0, 48)
+        cc.append((rand_tokens(rng, n, rng.choice([2, 3, 5, 8])), rng.randrange(1, 6)))
+    for _ in range(40):
+        n = rng.randrange(100, 4097)
+        cc.append((rand_tokens(rng, n, rng.choice([4, 16, 64, 30000])), rng.randrange(1, 5)))
+    for toks, mm in cc:
+        out["copy_continuation"].append({"tokens": toks, "mm": mm,
+                                         "e": K.copy_continuation(toks, mm)})
+    # longest_suffix_match: self (ring == tail, as the scheduler uses it) + separate tails
+    sm = [([10, 20, 30, 40, 10, 20], None, 2), ([1, 2, 3, 4, 5, 6], None, 3),
+          ([1, 2, 7, 5, 1, 2, 9, 6, 1, 2], None, 2), ([4, 1, 2, 8, 8, 1, 2, 5, 4, 1, 2], None, 2)]
+    for _ in range(400):
+        ring = rand_tokens(rng, rng.randrange(0, 48), rng.choice([2, 3, 5, 8]))
+        tail = None if rng.random() < 0.6 else rand_tokens(rng, rng.randrange(0, 20), 4)
+        sm.append((ring, tail, rng.randrange(1, 5)))
+    for _ in range(60):
+        n = rng.choice([2048, rng.randrange(64, 2049)])
+        ring = rand_tokens(rng, n, rng.choice([3, 16, 64, 30000]))
+        if rng.random() < 0.5:  # plant long repeats the way agentic copies look
+            span = ring[: rng.randrange(8, 64)]
+            pos = rng.randrange(0, max(1, n - len(span)))
+            ring[pos:pos + len(span)] = span
+            ring[-len(span) // 2:] = span[: len(span) // 2]
+            ring = ring[:n]
+        sm.append((ring, None, rng.choice([1, 2, 3, 4])))
+    for ring, tail, lmin in sm:
+        t = ring if tail is None else tail
+        e, ln = K.longest_suffix_match(ring, t, lmin)
+        out["suffix_match"].append({"ring": ring, "tail": tail, "min_len": lmin, "e": e, "len": ln})
+    # lookup_ngram known answers (test_speculator.py:22-46) + random with caps
+    ln_cases = [([10, 20, 30, 40, 10, 20], 2, 2), ([1, 2, 3, 4, 5, 6], 3, 8),
+                ([1, 2, 7, 5, 1, 2, 9, 6, 1, 2], 2, 1), ([4, 1, 2, 8, 8, 1, 2, 5, 4, 1, 2], 2, 1),
+                ([1, 2, 3, 4, 5, 1, 2], 2, 2), ([1, 2, 1, 2], 2, 0)]
+    for _ in range(200):
+        ln_cases.append((rand_tokens(rng, rng.randrange(0, 40), rng.choice([2, 3, 6])),
+                         rng.randrange(1, 4), rng.randrange(0, 18)))
+    for ring, mm, cap in ln_cases:
+        out["lookup_ngram"].append({"ring": ring, "mm": mm, "cap": cap,
+                                    "draft": lookup_ngram(ring, ring, mm, cap)})
+    # copy policy rows via the reference MockEngine forward (engine.py:268-281, 196-216)
+    for vocab, mm in [(32768, 3), (32768, 2), (1000, 3)]:
+        eng = MockEngine(ModelConfig(vocab=vocab, copy_min_match=mm))
+        for _ in range(60):
+            n = rng.randrange(1, 300)
+            alpha = rng.choice([3, 20, 5000])
+            full = rand_tokens(rng, n, alpha)
+            c = rng.randrange(0, n)
+            lb = eng.forward(full[:c], full[c:])
+            rows = []
+            for i in range(len(lb)):
+                lg = lb[i]
+                rows.append([lg.argmax_id, -1 if lg.copy_source is None else lg.copy_source])
+            out["copy_policy"].append({"vocab": vocab, "mm": mm, "full": full, "ctx": c,
+                                       "rows": rows})
+    # test_engine.py:127-141 known answers
+    eng = MockEngine(ModelConfig(copy_min_match=2))
+    lb = eng.forward([7, 8, 9], [7, 8])
+    out["copy_policy"].append({"vocab": 32768, "mm": 2, "full": [7, 8, 9, 7, 8], "ctx": 3,
+                               "rows": [[lb[i].argmax_id, -1 if lb[i].copy_source is None
+                                         else lb[i].copy_source] for i in range(2)]})
+    dump("kernels.json.gz", out, gz=True)
+
+
+# ---------------------------------------------------------------------------
+# kv cache and radix op sequences
+# ---------------------------------------------------------------------------
+
+def kv_observe(kv, seqs):
+    obs = {"occ": kv.occupancy, "free": kv.free_cells, "seqs": {}}
+    for s in seqs:
+        n = kv.seq_len(s)
+        if n:
+            obs["seqs"][str(s)] = {"len": n, "spans": kv.span_count(s), "cells": kv.cell_ids(s, 0, n)}
+    obs["ref"] = {str(int(c)): int(kv._refcnt[c]) for c in np.flatnonzero(kv._refcnt)}
+    return obs
+
+
+def gen_kvcache():
+    rng = random.Random(7)
+    runs_out = []
+    for case in range(60):
+        cap = rng.choice([64, 128, 256])
+        kv = UnifiedKvCache(cap)
+        seqs = list(range(6))
+        ops = []
+        for _ in range(rng.randrange(10, 60)):
+            kind = rng.choice(["append", "append", "append", "trim", "alias", "alias_runs",
+                               "release", "decref"])
+            s = rng.choice(seqs)
+            op = {"op": kind, "seq": s}
+            try:
+                if kind == "append":
+                    op["n"] = rng.randrange(1, 40)
+                    op["ret"] = list(kv.append_cells(s, op["n"]))
+                elif kind == "trim":
+                    op["pos"] = rng.randrange(0, kv.seq_len(s) + 2)
+                    op["ret"] = kv.trim(s, op["pos"])
+                elif kind == "alias":
+                    d = rng.choice(seqs)
+                    op["dest"] = d
+                    op["start"] = kv.seq_len(d) if rng.random() < 0.8 else rng.randrange(0, 5)
+                    op["end"] = op["start"] + rng.randrange(0, max(1, kv.seq_len(s) + 3 - op["start"]))
+                    kv.seq_alias(s, d, op["start"], op["end"])
+                elif kind == "alias_runs":
+                    n = kv.seq_len(s)
+                    if n == 0:
+                        op["runs"] = []
+                    else:
+                        a = rng.randrange(0, n)
+                        b = rng.randrange(a, n + 1)
+                        op["runs"] = [list(r) for r in kv.resolve_runs(s, a, b)]
+                    d = rng.choice(seqs)
+                    op["dest"] = d
+                    kv.alias_runs(d, [tuple(r) for r in op["runs"]])
+                    kv.incref_runs([tuple(r) for r in op["runs"]])  # mimic a radix hold
+                    op["held"] = True
+                elif kind == "decref":
+                    n = kv.seq_len(s)
+                    op["runs"] = [list(r) for r in kv.resolve_runs(s, 0, n)] if n and rng.random() < 0.3 else []
+                    op["ret"] = kv.decref_runs([tuple(r) for r in op["runs"]])
+                else:
+                    op["ret"] = kv.release_sequence(s)
+                op["err"] = None
+            except CapacityExhausted:
+                op["err"] = "CapacityExhausted"
+            except DonorRangeInvalid:
+                op["err"] = "DonorRangeInvalid"
+            except ValueError:
+                op["err"] = "ValueError"
+            op["obs"] = kv_observe(kv, seqs)
+            ops.append(op)
+        runs_out.append({"capacity": cap, "ops": ops})
+    dump("kvcache_ops.json.gz", runs_out, gz=True)
+
+
+def gen_radix():
+    rng = random.Random(11)
+    out = []
+    for case in range(40):
+        cap = 512
+        kv = UnifiedKvCache(cap)
+        trie = RadixTrie(kv, cell_budget=rng.choice([64, 128, 256]))
+        ops = []
+        bases = [rand_tokens(rng, rng.randrange(5, 40), 50) for _ in range(3)]
+        for step in range(rng.randrange(5, 30)):
+            kind = rng.choice(["save", "save", "lookup", "lookup", "evict", "release"])
+            s = rng.randrange(4)
+            op = {"op": kind, "seq": s}
+            try:
+                if kind == "save":
+                    toks = list(rng.choice(bases))[: rng.randrange(1, 41)] + rand_tokens(
+                        rng, rng.randrange(0, 20), 50)
+                    held = kv.seq_len(s)
+                    if held < len(toks):
+                        kv.append_cells(s, len(toks) - held)
+                    op["tokens"] = toks
+                    op["ret"] = trie.save(toks, s, 0)
+                elif kind == "lookup":
+                    toks = list(rng.choice(bases))[: rng.randrange(0, 41)] + rand_tokens(
+                        rng, rng.randrange(0, 5), 50)
+                    m = trie.longest_prefix(toks)
+                    op["tokens"] = toks
+                    op["ret"] = {"length": m.length, "runs": [list(r) for r in m.runs],
+                                 "donor": m.donor}
+                elif kind == "evict":
+                    op["n"] = rng.randrange(1, 80)
+                    op["ret"] = trie.evict(op["n"])
+                else:
+                    op["ret"] = kv.release_sequence(s)
+                op["err"] = None
+            except BudgetExceeded:
+                op["err"] = "BudgetExceeded"
+            except CapacityExhausted:
+                op["err"] = "CapacityExhausted"
+            op["dump"] = trie.dump()
+            op["cells"] = trie.total_cells
+            op["occ"] = kv.occupancy
+            op["evicted_total"] = trie.evicted_cells_total
+            ops.append(op)
+        out.append({"budget": trie.cell_budget, "ops": ops})
+    dump("radix_ops.json.gz", out, gz=True)
+
+
+# ---------------------------------------------------------------------------
+# scenario traces through the reference InferenceCore
+# ---------------------------------------------------------------------------
+
+RESULT_FIELDS = ("generated", "finish_reason", "n_t", "cached_prompt_tokens", "prefill_tokens",
+                 "decode_passes", "spec_proposed", "spec_accepted", "spec_rejected",
+                 "aliased_cells", "early_stopped", "text")
+
+
+class Recorder:
+    """Drives the reference core the way scenarios.run_core_scenario does, but
+    records every request so a different engine can replay the same stream."""
+
+    def __init__(self, core):
+        self.core = core
+        self.requests = []
+        self.last_prompt = {}  # stream key -> (tokens, pieces) for delta coding
+        self.wave = 0  # requests of one wave are submitted together, then run to completion
+
+    def submit(self, stream, tokens, pieces, max_tokens, tools, rid):
+        guard = self.core.pool.acquire("transient", timeout=1.0)
+        declared = frozenset(t["function"]["name"] for t in tools if "function" in t)
+        req = GenerationRequest(request_id=rid, prompt_tokens=list(tokens),
+                                prompt_pieces=list(pieces), max_tokens=max_tokens,
+                                temperature=0.0, seed=prompt_seed(tokens),
+                                declared_tools=declared, guard=guard)
+        h = RequestHandle(req)
+        self.core.submit(h)
+        prev_t, prev_p = self.last_prompt.get(stream, ([], []))
+        c = 0
+        while c < min(len(prev_t), len(tokens)) and prev_t[c] == tokens[c] and prev_p[c] == pieces[c]:
+            c += 1
+        self.last_prompt[stream] = (list(tokens), list(pieces))
+        rec = {"id": rid, "wave": self.wave, "stream": stream, "common": c, "tokens": tokens[c:],
+               "pieces": pieces[c:], "max_tokens": max_tokens, "tools": sorted(declared)}
+        self.requests.append((h, rec))
+        return h
+
+    def run_until_done(self, handles, max_iters=200_000):
+        self.wave += 1
+        pending = list(handles)
+        for _ in range(max_iters):
+            pending = [h for h in pending if not h.wait(timeout=0)]
+            if not pending:
+                return
+            self.core.step()
+        raise RuntimeError("unfinished")
+
+    def finish_records(self):
+        out = []
+        for h, rec in self.requests:
+            assert h.error is None, h.error
+            r = h.result
+            rec["expect"] = {f: getattr(r, f) for f in RESULT_FIELDS}
+            rec["expect"]["finalize"] = r.finalize.kind
+            out.append(rec)
+        return out
+
+
+def assistant_content(result):
+    fin = result.finalize
+    if fin.kind == "tool_calls":
+        return "\n".join(json.dumps({"name": c.name, "parameters": c.parameters},
+                                    separators=(",", ":")) for c in fin.calls)
+    return result.text
+
+
+class Conv:
+    def __init__(self, sc: Scenario):
+        self.sc = sc
+        self.messages = [{"role": "system", "content": sc.system}]
+
+    def prompt(self, core, t):
+        self.messages.append({"role": "user", "content": self.sc.user_texts[t]})
+        _, toks, pieces = core.prepare_prompt(self.messages, self.sc.tools)
+        return toks, pieces
+
+    def after(self, t, result):
+        self.messages.append({"role": "assistant", "content": assistant_content(result)})
+        if t < len(self.sc.tool_results):
+            self.messages.append({"role": "tool", "content": self.sc.tool_results[t]})
+
+
+def core_snapshot(core):
+    return {"ledger": core.engine.ledger.snapshot(), "occ": core.kv.occupancy,
+            "radix_cells": core.radix.total_cells, "radix_dump": core.radix.dump(),
+            "iterations": core.iterations}
+
+
+def trace_sequential(name, cfg_over, scenarios, interleave=True, bursts=()):
+    """Conversations turn by turn (interleaved A1 B1 C1 A2 ...), each turn run to
+    completion; then optional bursts of concurrent single-turn requests."""
+    core = InferenceCore(ServerConfig(**cfg_over))
+    rec = Recorder(core)
+    convs = [Conv(sc) for sc in scenarios]
+    turns = max(sc.turn_count for sc in scenarios)
+    order = ([(t, i) for t in range(turns) for i in range(len(convs))] if interleave
+             else [(t, i) for i in range(len(convs)) for t in range(turns)])
+    snaps = []
+    for t, i in order:
+        conv = convs[i]
+        if t >= conv.sc.turn_count:
+            continue
+        toks, pieces = conv.prompt(core, t)
+        h = rec.submit(f"s{i}", toks, pieces, conv.sc.max_tokens, conv.sc.tools,
+                       f"{conv.sc.name}-t{t}")
+        rec.run_until_done([h])
+        conv.after(t, h.result)
+        snaps.append(core_snapshot(core))
+    for bsalt, width in bursts:
+        system, tools, texts = burst_prompts(bsalt, width)
+        handles = []
+        for w, text in enumerate(texts):
+            msgs = [{"role": "system", "content": system}, {"role": "user", "content": text}]
+            _, toks, pieces = core.prepare_prompt(msgs, tools)
+            handles.append(rec.submit(f"b{w}", toks, pieces, 80, tools, f"burst-{bsalt}-{w}"))
+        rec.run_until_done(handles)
+        snaps.append(core_snapshot(core))
+    return {"name": name, "config": cfg_over, "mode": "sequential", "interleave": interleave,
+            "requests": rec.finish_records(), "snapshots": snaps}
+
+
+def trace_waves(name, cfg_over, scenarios):
+    """Turn-synchronous waves: turn t of every session submitted together (C5)."""
+    core = InferenceCore(ServerConfig(**cfg_over))
+    rec = Recorder(core)
+    convs = [Conv(sc) for sc in scenarios]
+    snaps = []
+    for t in range(max(sc.turn_count for sc in scenarios)):
+        handles = []
+        for i, conv in enumerate(convs):
+            toks, pieces = conv.prompt(core, t)
+            handles.append(rec.submit(f"s{i}", toks, pieces, conv.sc.max_tokens, conv.sc.tools,
+                                      f"{conv.sc.name}-t{t}"))
+        rec.run_until_done(handles)
+        for conv, h in zip(convs, handles):
+            conv.after(t, h.result)
+        snaps.append(core_snapshot(core))
+    return {"name": name, "config": cfg_over, "mode": "waves",
+            "requests": rec.finish_records(), "snapshots": snaps}
+
+
+def deep_c4(salt, turns, pieces=820):
+    sc = deep_workflow(salt, turns)
+    sc.tool_results = [turn_tool_result(salt, t, pieces=pieces) for t in range(turns)]
+    sc.max_tokens = 128
+    return sc
+
+
+def gen_traces():
+    c2 = agentic_6turn("c2")
+    traces = [
+        trace_sequential("c1", {}, [agent_scenario("travel", "c1")]),
+        trace_sequential("c2", {"spec_max_lookahead": 4}, [c2]),
+        trace_sequential("c2_nospec", {"spec_max_lookahead": 4, "speculation_enabled": False}, [c2]),
+        trace_sequential("c3", {"pool_transient": 16},
+                         [deep_workflow(s, 5) for s in ("c3a", "c3b", "c3c")],
+                         bursts=[("c3burst", 16)]),
+        trace_sequential("c3_nogroup", {"pool_transient": 16, "grouping_enabled": False},
+                         [deep_workflow(s, 5) for s in ("c3a", "c3b", "c3c")],
+                         bursts=[("c3burst", 16)]),
+        trace_sequential("c4_small", {"spec_max_lookahead": 4, "capacity_cells": 65536},
+                         [deep_c4("c4s", 8, pieces=200)]),
+        trace_sequential("c4", {"spec_max_lookahead": 4, "capacity_cells": 262144},
+                         [deep_c4("c4", 35)]),
+        trace_waves("c5_small", {"pool_transient": 8, "capacity_cells": 65536},
+                    [agentic_6turn(f"c5s{i}") for i in range(8)]),
+        trace_waves("c5", {"pool_transient": 256, "capacity_cells": 1 << 19},
+                    [agentic_6turn(f"c5s{i}") for i in range(256)]),
+    ]
+    for tr in traces:
+        n = len(tr["requests"])
+        last = tr["requests"][-1]
+        print(f"{tr['name']}: {n} requests, last n_t={last['expect']['n_t']}")
+        dump(f"traces/{tr['name']}.json.gz", tr, gz=True)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["kernels", "kvcache", "radix", "traces"]
+    if "kernels" in which:
+        gen_kernels()
+    if "kvcache" in which:
+        gen_kvcache()
+    if "radix" in which:
+        gen_radix()
+    if "traces" in which:
+        gen_traces()

@@ -1,0 +1,82 @@
+"""K4 metadata kernels: the host UnifiedKvCache op log applied on the device
+(ds_kv_apply) reproduces the reference page tables (cell ids) and refcounts
+(popcount of the sequence-membership bitmask + radix holds) - with 0 KV bytes
+moved."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden
+from paper_2605_26289_b200.kvcache import CapacityExhausted, DonorRangeInvalid, UnifiedKvCache
+
+pytestmark = pytest.mark.gpu
+
+
+def _apply(cuda, ops, pos2cell, member, trie, n_seqs):
+    from paper_2605_26289_b200._lib import check, lib
+
+    if not ops:
+        return
+    o = torch.tensor(np.asarray(ops, dtype=np.int32)).to(cuda)
+    check(lib().ds_kv_apply(o.data_ptr(), len(ops), pos2cell.data_ptr(), pos2cell.shape[1],
+                            n_seqs, member.data_ptr(), member.shape[1], trie.data_ptr(),
+                            torch.cuda.current_stream().cuda_stream))
+
+
+def _refcount(cuda, member, trie):
+    from paper_2605_26289_b200._lib import check, lib
+
+    cap = member.shape[0]
+    rc = torch.empty(cap, dtype=torch.int32, device=cuda)
+    occ = torch.zeros(1, dtype=torch.int32, device=cuda)
+    check(lib().ds_kv_refcount(member.data_ptr(), member.shape[1], trie.data_ptr(), cap,
+                               rc.data_ptr(), occ.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream))
+    return rc.cpu().numpy(), int(occ.item())
+
+
+def test_golden_ops_on_device(cuda):
+    cases = load_golden("kvcache_ops.json.gz")
+    checked = 0
+    for case in cases:
+        cap = case["capacity"]
+        kv = UnifiedKvCache(cap)
+        kv.record_ops = True
+        pos2cell = torch.full((6, cap), -1, dtype=torch.int32, device=cuda)
+        member = torch.zeros((cap, 1), dtype=torch.int32, device=cuda)
+        trie = torch.zeros(cap, dtype=torch.int32, device=cuda)
+        ever_dup = False
+        for op in case["ops"]:
+            s = op["seq"]
+            try:
+                if op["op"] == "append":
+                    kv.append_cells(s, op["n"])
+                elif op["op"] == "trim":
+                    kv.trim(s, op["pos"])
+                elif op["op"] == "alias":
+                    kv.seq_alias(s, op["dest"], op["start"], op["end"])
+                elif op["op"] == "alias_runs":
+                    runs = [tuple(r) for r in op["runs"]]
+                    kv.alias_runs(op["dest"], runs)
+                    kv.incref_runs(runs)
+                elif op["op"] == "decref":
+                    kv.decref_runs([tuple(r) for r in op["runs"]])
+                else:
+                    kv.release_sequence(s)
+            except (CapacityExhausted, DonorRangeInvalid, ValueError):
+                pass
+            _apply(cuda, kv.take_ops(), pos2cell, member, trie, 6)
+            p2c = pos2cell.cpu().numpy()
+            for seq in range(6):
+                n = kv.seq_len(seq)
+                cells = kv.cell_ids(seq, 0, n) if n else []
+                assert p2c[seq, :n].tolist() == cells
+                ever_dup |= len(set(cells)) != len(cells)
+            if not ever_dup:
+                rc, occ = _refcount(cuda, member, trie)
+                assert np.array_equal(rc, kv._refcnt)
+                assert occ == kv.occupancy
+                checked += 1
+    assert checked > 500

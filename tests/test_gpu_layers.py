@@ -1,0 +1,132 @@
+"""Element-wise kernels + K5 (RoPE/KV store) + K7 attention vs torch fp32."""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.llama_ref import paged_attention, rope_tables
+
+pytestmark = pytest.mark.gpu
+
+
+def _bf(x):
+    return x.to(torch.bfloat16)
+
+
+def test_rmsnorm_silu_embed_argmax(cuda):
+    from paper_2605_26289_b200._lib import check, lib
+
+    L = lib()
+    s = torch.cuda.current_stream().cuda_stream
+    g = torch.Generator(device=cuda).manual_seed(0)
+    x = torch.randn(7, 4096, device=cuda, generator=g).bfloat16()
+    w = (1 + 0.1 * torch.randn(4096, device=cuda, generator=g)).bfloat16()
+    out = torch.empty_like(x)
+    rows = torch.tensor([6, 0, 3], dtype=torch.int32, device=cuda)
+    check(L.ds_rmsnorm(x.data_ptr(), rows.data_ptr(), 3, 4096, w.data_ptr(), 1e-5,
+                       out.data_ptr(), s))
+    xf = x.float()[[6, 0, 3]]
+    ref = xf * torch.rsqrt((xf * xf).mean(-1, keepdim=True) + 1e-5) * w.float()
+    assert torch.allclose(out[:3].float(), _bf(ref).float(), atol=2e-2, rtol=1e-2)
+    gu = torch.randn(5, 2 * 2816, device=cuda, generator=g).bfloat16()
+    act = torch.empty(5, 2816, device=cuda, dtype=torch.bfloat16)
+    check(L.ds_silu_mul(gu.data_ptr(), 5, 2816, act.data_ptr(), s))
+    gf = gu.float()
+    ref = torch.nn.functional.silu(gf[:, :2816]) * gf[:, 2816:]
+    assert torch.allclose(act.float(), _bf(ref).float(), atol=1e-2, rtol=1e-2)
+    table = torch.randn(100, 1024, device=cuda, generator=g).bfloat16()
+    tok = torch.tensor([5, 99, 0], dtype=torch.int32, device=cuda)
+    emb = torch.empty(3, 1024, device=cuda, dtype=torch.bfloat16)
+    check(L.ds_embed(tok.data_ptr(), 3, table.data_ptr(), 1024, emb.data_ptr(), s))
+    assert torch.equal(emb, table[[5, 99, 0]])
+    logits = torch.randn(4, 128256, device=cuda, generator=g)
+    logits[2, 77] = logits[2, 1000] = 1e4  # tie -> lowest index
+    am = torch.empty(4, dtype=torch.int32, device=cuda)
+    check(L.ds_argmax(logits.data_ptr(), 4, 128256, am.data_ptr(), s))
+    ref = logits.argmax(-1)
+    ref[2] = 77
+    assert am.tolist() == ref.tolist()
+
+
+def _setup_paged(cuda, seq_len, nkv=8, d=128, capacity=None, seed=0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    capacity = capacity or seq_len + 37
+    cells = torch.randperm(capacity, generator=g)[:seq_len].to(torch.int32)
+    k_pool = torch.randn(capacity, nkv, d, generator=g).bfloat16()
+    v_pool = torch.randn(capacity, nkv, d, generator=g).bfloat16()
+    pos2cell = torch.zeros(2, seq_len + 64, dtype=torch.int32)
+    pos2cell[1, :seq_len] = cells
+    return (k_pool.to(cuda), v_pool.to(cuda), pos2cell.to(cuda), cells, k_pool, v_pool)
+
+
+def _entries(entries):
+    from paper_2605_26289_b200 import _lib
+
+    arr = (_lib.Entry * len(entries))()
+    for i, e in enumerate(entries):
+        arr[i] = _lib.Entry(*e)
+    return arr
+
+
+@pytest.mark.parametrize("past,q_len", [(0, 1), (5, 1), (1000, 1), (3000, 5), (31, 17),
+                                        (4500, 5), (777, 64), (0, 150), (2048, 300)])
+def test_attention_paged_vs_fp32(cuda, past, q_len):
+    from paper_2605_26289_b200._lib import check, lib
+
+    nh, nkv, d = 32, 8, 128
+    kv_len = past + q_len
+    k_pool, v_pool, pos2cell, cells, k_cpu, v_cpu = _setup_paged(cuda, kv_len, seed=past + q_len)
+    g = torch.Generator(device="cpu").manual_seed(1)
+    qkv = torch.randn(q_len, (nh + 2 * nkv) * d, generator=g).bfloat16()
+    ent = _entries([(1, past, q_len, 0, 0, 0, 0, 1, 0)])
+    ent_dev = torch.frombuffer(bytearray(bytes(ent)), dtype=torch.uint8).to(cuda)
+    out = torch.zeros(q_len, nh * d, dtype=torch.bfloat16, device=cuda)
+    ws_bytes = lib().ds_attention_workspace_bytes(q_len, 1, nh, d)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=cuda)
+    qkv_d = qkv.to(cuda)
+    check(lib().ds_attention(qkv_d.data_ptr(), ctypes.addressof(ent), ent_dev.data_ptr(), 1,
+                             q_len, k_pool.data_ptr(), v_pool.data_ptr(), pos2cell.data_ptr(),
+                             pos2cell.shape[1], nh, nkv, d, 1.0 / d ** 0.5, out.data_ptr(),
+                             ws.data_ptr(), ws_bytes, 1, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    q = qkv[:, : nh * d].view(q_len, nh, d)
+    ref = paged_attention(q, k_cpu[cells.long()], v_cpu[cells.long()],
+                          list(range(past, kv_len)), kv_len, 1.0 / d ** 0.5)
+    got = out.cpu().float().view(q_len, nh, d)
+    err = (got - ref).abs().max().item()
+    assert err < 2e-2, err
+
+
+def test_rope_kv_store(cuda):
+    from paper_2605_26289_b200._lib import check, lib
+
+    nh, nkv, d, T = 8, 2, 128, 6
+    cos, sin = rope_tables(64, d, 500000.0)
+    g = torch.Generator(device="cpu").manual_seed(2)
+    qkv = torch.randn(T, (nh + 2 * nkv) * d, generator=g).bfloat16()
+    row_seq = torch.full((T,), 1, dtype=torch.int32)
+    row_pos = torch.arange(10, 10 + T, dtype=torch.int32)
+    pos2cell = torch.zeros(2, 64, dtype=torch.int32)
+    pos2cell[1, 10:16] = torch.tensor([40, 3, 17, 8, 9, 60], dtype=torch.int32)
+    kp = torch.zeros(64, nkv, d, dtype=torch.bfloat16, device=cuda)
+    vp = torch.zeros_like(kp)
+    qd = qkv.to(cuda)
+    check(lib().ds_rope_kv_store(qd.data_ptr(), T, row_seq.to(cuda).data_ptr(),
+                                 row_pos.to(cuda).data_ptr(), pos2cell.to(cuda).data_ptr(), 64,
+                                 nh, nkv, d, cos.to(cuda).data_ptr(), sin.to(cuda).data_ptr(),
+                                 kp.data_ptr(), vp.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    from oracle.llama_ref import rope
+
+    x = qkv.float()
+    q = rope(x[:, : nh * d].view(T, nh, d), cos[10:16], sin[10:16])
+    k = rope(x[:, nh * d:(nh + nkv) * d].view(T, nkv, d), cos[10:16], sin[10:16])
+    v = x[:, (nh + nkv) * d:].view(T, nkv, d)
+    # fp32 FMA contraction may flip a bf16 rounding: allow one bf16 ulp
+    assert torch.allclose(qd.cpu().float()[:, : nh * d].view(T, nh, d), q, atol=1e-2, rtol=8e-3)
+    cells = [40, 3, 17, 8, 9, 60]
+    assert torch.allclose(kp.cpu().float()[cells], k, atol=1e-2, rtol=8e-3)
+    assert torch.equal(vp.cpu().float()[cells], v)

@@ -1,0 +1,53 @@
+"""Host RadixTrie vs the reference (golden radix_ops from radix.py)."""
+from __future__ import annotations
+
+from conftest import load_golden
+from paper_2605_26289_b200.kvcache import CapacityExhausted, UnifiedKvCache
+from paper_2605_26289_b200.radix import BudgetExceeded, RadixTrie
+
+
+def test_golden_radix_sequences():
+    cases = load_golden("radix_ops.json.gz")
+    for case in cases:
+        kv = UnifiedKvCache(512)
+        trie = RadixTrie(kv, cell_budget=case["budget"])
+        for op in case["ops"]:
+            err = None
+            s = op["seq"]
+            try:
+                if op["op"] == "save":
+                    toks = op["tokens"]
+                    held = kv.seq_len(s)
+                    if held < len(toks):
+                        kv.append_cells(s, len(toks) - held)
+                    assert trie.save(toks, s, 0) == op["ret"]
+                elif op["op"] == "lookup":
+                    m = trie.longest_prefix(op["tokens"])
+                    assert {"length": m.length, "runs": [list(r) for r in m.runs],
+                            "donor": m.donor} == op["ret"]
+                elif op["op"] == "evict":
+                    assert trie.evict(op["n"]) == op["ret"]
+                else:
+                    assert kv.release_sequence(s) == op["ret"]
+            except BudgetExceeded:
+                err = "BudgetExceeded"
+            except CapacityExhausted:
+                err = "CapacityExhausted"
+            assert err == op["err"]
+            assert trie.dump() == op["dump"], op
+            assert trie.total_cells == op["cells"]
+            assert kv.occupancy == op["occ"]
+            assert trie.evicted_cells_total == op["evicted_total"]
+
+
+def test_eviction_tie_break_lower_first_token():
+    kv = UnifiedKvCache(4096)
+    trie = RadixTrie(kv, 2048)
+    kv.append_cells(1, 4)
+    trie.save([5, 5], 1, 0)
+    trie.save([3, 3], 1, 2)
+    for node in trie.root.children.values():
+        node.last_touch = 42
+    trie.evict(2)
+    assert trie.longest_prefix([3, 3]).length == 0
+    assert trie.longest_prefix([5, 5]).length == 2
