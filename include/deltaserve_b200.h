@@ -202,11 +202,13 @@ int ds_attention(const void* qkv, const ds_entry* entries_host, const ds_entry* 
                  int head_dim, float scale, void* out, void* workspace, size_t workspace_bytes,
                  int impl, ds_stream_t stream);
 
-int ds_rmsnorm(const void* x, const int32_t* rows, int n_rows, int hidden, const void* w,
-               float eps, void* out, ds_stream_t stream);
+/* RMSNorm of rows (nullable = identity) of the bf16 (x_f32=0) or fp32 residual
+ * stream -> bf16: out = x * rsqrt(mean(x^2) + eps) * w, fp32 math. */
+int ds_rmsnorm(const void* x, int x_f32, const int32_t* rows, int n_rows, int hidden,
+               const void* w, float eps, void* out, ds_stream_t stream);
 int ds_silu_mul(const void* gate_up, int n_rows, int ffn, void* out, ds_stream_t stream);
 int ds_embed(const int32_t* tokens, int n_rows, const void* table, int hidden, void* out,
-             ds_stream_t stream);
+             int out_f32, ds_stream_t stream);
 /* K8: row argmax over fp32 logits (lowest index on ties, engine.py:146-159). */
 int ds_argmax(const float* logits, int n_rows, int vocab, int32_t* out, ds_stream_t stream);
 

@@ -5,9 +5,9 @@ SPEC.md:18 puts GPU execution out of scope), so attention / logits parity is
 pinned only by this restatement of standard Llama-3 math (PAPER.md:293:
 Llama-3.1-8B): RMSNorm (eps 1e-5), rotate-half RoPE (theta 500000, fp64
 angles), GQA attention, SwiGLU MLP, untied LM head.  It rounds to bf16 at
-exactly the tensor boundaries the GPU stores (residual stream, norm outputs,
-projections, roped q/k, KV cache, attention output, MLP activations) and
-accumulates in fp32 everywhere else, so the tolerance budget is only the
+exactly the tensor boundaries the GPU stores (norm outputs, projections,
+roped q/k, KV cache, attention output, MLP activations) and keeps the
+residual stream and every accumulation in fp32, so the tolerance budget is only the
 accumulation-order / bf16-P difference (logits max-abs <= 1e-2).
 """
 from __future__ import annotations
@@ -66,12 +66,12 @@ def forward(w: dict, shape, tokens: list[int], out_rows: list[int] | None = None
         s = torch.einsum("qhd,khd->hqk", q, kr) * scale + mask
         p = torch.softmax(s, dim=-1)
         o = _bf(torch.einsum("hqk,khd->qhd", p, vr).reshape(T, nh * d))
-        x = _bf(x + o @ w["wo"][l].T)
+        x = x + o @ w["wo"][l].T  # fp32 residual stream
         h = rmsnorm(x, w["mlp_norm"][l], shape.rms_eps)
         gu = _bf(h @ w["w_gate_up"][l].T)
         g, u = gu[:, : shape.ffn], gu[:, shape.ffn:]
         a = _bf(torch.nn.functional.silu(g) * u)
-        x = _bf(x + a @ w["w_down"][l].T)
+        x = x + a @ w["w_down"][l].T
     rows = list(range(T)) if out_rows is None else out_rows
     hf = rmsnorm(x[rows], w["final_norm"], shape.rms_eps)
     return hf @ w["lm_head"].T

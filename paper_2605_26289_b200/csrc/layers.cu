@@ -6,37 +6,64 @@
 
 namespace ds {
 
+// out[r] = table[tok[r]] as bf16 (out_f32=0) or widened to fp32 (residual stream)
 __global__ void embed_kernel(const int32_t* __restrict__ tok, const uint4* __restrict__ table,
-                             int chunks, uint4* __restrict__ out) {
+                             int chunks, void* __restrict__ out, int out_f32) {
   const int r = blockIdx.x;
   const uint4* src = table + static_cast<int64_t>(tok[r]) * chunks;
-  uint4* dst = out + static_cast<int64_t>(r) * chunks;
-  for (int j = threadIdx.x; j < chunks; j += blockDim.x) dst[j] = __ldg(src + j);
+  for (int j = threadIdx.x; j < chunks; j += blockDim.x) {
+    const uint4 v = __ldg(src + j);
+    if (out_f32) {
+      const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+      float4* dst = reinterpret_cast<float4*>(out) + (static_cast<int64_t>(r) * chunks + j) * 2;
+      const float2 a = __bfloat1622float2(p[0]), b = __bfloat1622float2(p[1]);
+      const float2 c = __bfloat1622float2(p[2]), d = __bfloat1622float2(p[3]);
+      dst[0] = make_float4(a.x, a.y, b.x, b.y);
+      dst[1] = make_float4(c.x, c.y, d.x, d.y);
+    } else {
+      reinterpret_cast<uint4*>(out)[static_cast<int64_t>(r) * chunks + j] = v;
+    }
+  }
 }
 
 // out[r] = x[rows[r]] * rsqrt(mean(x^2) + eps) * w   (fp32 math, one rounding)
+// x is the bf16 or fp32 residual stream; 8 elements per chunk.
+DS_DEVICE void load8(const void* x, int64_t idx, bool f32, float* f) {
+  if (f32) {
+    const float4* p = reinterpret_cast<const float4*>(x) + idx * 2;
+    const float4 a = __ldg(p), b = __ldg(p + 1);
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  } else {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(x) + idx);
+    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 t = __bfloat1622float2(p[q]);
+      f[2 * q] = t.x;
+      f[2 * q + 1] = t.y;
+    }
+  }
+}
+
 template <int BLOCK, int MAXC>
-__global__ void __launch_bounds__(BLOCK) rmsnorm_kernel(const uint4* __restrict__ x,
+__global__ void __launch_bounds__(BLOCK) rmsnorm_kernel(const void* __restrict__ x,
                                                         const int32_t* __restrict__ rows,
-                                                        int chunks, const uint4* __restrict__ w,
-                                                        float eps, uint4* __restrict__ out) {
+                                                        int chunks, int x_f32,
+                                                        const uint4* __restrict__ w, float eps,
+                                                        uint4* __restrict__ out) {
   __shared__ float s_part[BLOCK / 32];
   const int r = blockIdx.x;
-  const int src = rows ? rows[r] : r;
-  const uint4* xr = x + static_cast<int64_t>(src) * chunks;
-  uint4 v[MAXC];
+  const int64_t src = rows ? rows[r] : r;
+  float v[MAXC][8];
   float ss = 0.f;
 #pragma unroll
   for (int k = 0; k < MAXC; ++k) {
     const int j = threadIdx.x + k * BLOCK;
     if (j < chunks) {
-      v[k] = __ldg(xr + j);
-      const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v[k]);
+      load8(x, src * chunks + j, x_f32 != 0, v[k]);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float2 f = __bfloat1622float2(p[q]);
-        ss += f.x * f.x + f.y * f.y;
-      }
+      for (int q = 0; q < 8; ++q) ss += v[k][q] * v[k][q];
     }
   }
   ss = warp_sum(ss);
@@ -55,15 +82,13 @@ __global__ void __launch_bounds__(BLOCK) rmsnorm_kernel(const uint4* __restrict_
     const int j = threadIdx.x + k * BLOCK;
     if (j < chunks) {
       const uint4 wv = __ldg(w + j);
-      const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v[k]);
       const __nv_bfloat162* pw = reinterpret_cast<const __nv_bfloat162*>(&wv);
       uint4 o;
       uint32_t* po = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const float2 f = __bfloat1622float2(p[q]);
         const float2 g = __bfloat1622float2(pw[q]);
-        po[q] = pack_bf16(f.x * inv * g.x, f.y * inv * g.y);
+        po[q] = pack_bf16(v[k][2 * q] * inv * g.x, v[k][2 * q + 1] * inv * g.y);
       }
       orow[j] = o;
     }
@@ -139,21 +164,20 @@ __global__ void rope_kv_store_kernel(__nv_bfloat16* __restrict__ qkv, const int3
 extern "C" {
 
 int ds_embed(const int32_t* tokens, int n_rows, const void* table, int hidden, void* out,
-             ds_stream_t stream) {
+             int out_f32, ds_stream_t stream) {
   if (n_rows < 0 || hidden % 8) return DS_EINVAL;
   if (n_rows == 0) return DS_OK;
   ds::embed_kernel<<<n_rows, 128, 0, (cudaStream_t)stream>>>(
-      tokens, static_cast<const uint4*>(table), hidden / 8, static_cast<uint4*>(out));
+      tokens, static_cast<const uint4*>(table), hidden / 8, out, out_f32);
   return (int)cudaGetLastError();
 }
 
-int ds_rmsnorm(const void* x, const int32_t* rows, int n_rows, int hidden, const void* w,
-               float eps, void* out, ds_stream_t stream) {
+int ds_rmsnorm(const void* x, int x_f32, const int32_t* rows, int n_rows, int hidden,
+               const void* w, float eps, void* out, ds_stream_t stream) {
   if (n_rows < 0 || hidden % 8 || hidden > 8 * 256 * 4) return DS_EINVAL;
   if (n_rows == 0) return DS_OK;
   ds::rmsnorm_kernel<256, 4><<<n_rows, 256, 0, (cudaStream_t)stream>>>(
-      static_cast<const uint4*>(x), rows, hidden / 8, static_cast<const uint4*>(w), eps,
-      static_cast<uint4*>(out));
+      x, rows, hidden / 8, x_f32, static_cast<const uint4*>(w), eps, static_cast<uint4*>(out));
   return (int)cudaGetLastError();
 }
 

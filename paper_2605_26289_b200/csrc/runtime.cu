@@ -69,7 +69,8 @@ struct Carve {
 };
 
 struct Buffers {
-  __nv_bfloat16 *x, *h, *qkv, *attn, *gu, *act, *hf;
+  float* x;  // fp32 residual stream
+  __nv_bfloat16 *h, *qkv, *attn, *gu, *act, *hf;
   uint64_t* row_hash;
   void* attn_ws;
   size_t attn_ws_bytes;
@@ -82,7 +83,7 @@ size_t layout(const ds_model* m, int rows, int outs, Buffers* b, uint8_t* base) 
   const size_t QKV = static_cast<size_t>(m->n_heads + 2 * m->n_kv_heads) * m->head_dim;
   const size_t A = static_cast<size_t>(m->n_heads) * m->head_dim;
   Buffers t{};
-  t.x = c.take<__nv_bfloat16>(rows * H * 2);
+  t.x = c.take<float>(rows * H * 4);
   t.h = c.take<__nv_bfloat16>(rows * H * 2);
   t.qkv = c.take<__nv_bfloat16>(rows * QKV * 2);
   t.attn = c.take<__nv_bfloat16>(rows * A * 2);
@@ -214,7 +215,7 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
   DS_CUDA(cudaGetLastError());
   DS_CUDA(cudaEventRecord(rt.join, rt.side));
 
-  DS_CHECK(ds_embed(a->tokens, T, m->embed, H, b.x, stream));
+  DS_CHECK(ds_embed(a->tokens, T, m->embed, H, b.x, 1, stream));
   const __nv_bfloat16* wqkv = static_cast<const __nv_bfloat16*>(m->wqkv);
   const __nv_bfloat16* wo = static_cast<const __nv_bfloat16*>(m->wo);
   const __nv_bfloat16* wgu = static_cast<const __nv_bfloat16*>(m->w_gate_up);
@@ -224,7 +225,8 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
   __nv_bfloat16* kp = static_cast<__nv_bfloat16*>(kv->k_pool);
   __nv_bfloat16* vp = static_cast<__nv_bfloat16*>(kv->v_pool);
   for (int l = 0; l < L; ++l) {
-    DS_CHECK(ds_rmsnorm(b.x, nullptr, T, H, an + static_cast<size_t>(l) * H, m->rms_eps, b.h, stream));
+    DS_CHECK(ds_rmsnorm(b.x, 1, nullptr, T, H, an + static_cast<size_t>(l) * H, m->rms_eps, b.h,
+                        stream));
     DS_BLAS(gemm(rt.blas, b.h, wqkv + static_cast<size_t>(l) * QKV * H, b.qkv, T, QKV, H, 0.f,
                  CUDA_R_16BF));
     DS_CHECK(ds_rope_kv_store(b.qkv, T, a->row_seq, a->row_pos, kv->pos2cell, kv->pos_stride, nh,
@@ -234,16 +236,17 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
                           vp + l * kv_layer, kv->pos2cell, kv->pos_stride, nh, nkv, hd, scale,
                           b.attn, b.attn_ws, b.attn_ws_bytes, attn_impl, stream));
     DS_BLAS(gemm(rt.blas, b.attn, wo + static_cast<size_t>(l) * H * nh * hd, b.x, T, H, nh * hd,
-                 1.f, CUDA_R_16BF));
-    DS_CHECK(ds_rmsnorm(b.x, nullptr, T, H, mn + static_cast<size_t>(l) * H, m->rms_eps, b.h, stream));
+                 1.f, CUDA_R_32F));
+    DS_CHECK(ds_rmsnorm(b.x, 1, nullptr, T, H, mn + static_cast<size_t>(l) * H, m->rms_eps, b.h,
+                        stream));
     DS_BLAS(gemm(rt.blas, b.h, wgu + static_cast<size_t>(l) * 2 * F * H, b.gu, T, 2 * F, H, 0.f,
                  CUDA_R_16BF));
     DS_CHECK(ds_silu_mul(b.gu, T, F, b.act, stream));
     DS_BLAS(gemm(rt.blas, b.act, wd + static_cast<size_t>(l) * H * F, b.x, T, H, F, 1.f,
-                 CUDA_R_16BF));
+                 CUDA_R_32F));
   }
   // final norm on sampled rows only, LM head in fp32
-  DS_CHECK(ds_rmsnorm(b.x, a->out_rows, a->n_out, H, m->final_norm, m->rms_eps, b.hf, stream));
+  DS_CHECK(ds_rmsnorm(b.x, 1, a->out_rows, a->n_out, H, m->final_norm, m->rms_eps, b.hf, stream));
   DS_BLAS(gemm(rt.blas, b.hf, m->lm_head, a->logits, a->n_out, m->vocab, H, 0.f, CUDA_R_32F));
 
   DS_CUDA(cudaStreamWaitEvent(stream, rt.join, 0));

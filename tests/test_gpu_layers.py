@@ -26,8 +26,14 @@ def test_rmsnorm_silu_embed_argmax(cuda):
     w = (1 + 0.1 * torch.randn(4096, device=cuda, generator=g)).bfloat16()
     out = torch.empty_like(x)
     rows = torch.tensor([6, 0, 3], dtype=torch.int32, device=cuda)
-    check(L.ds_rmsnorm(x.data_ptr(), rows.data_ptr(), 3, 4096, w.data_ptr(), 1e-5,
+    check(L.ds_rmsnorm(x.data_ptr(), 0, rows.data_ptr(), 3, 4096, w.data_ptr(), 1e-5,
                        out.data_ptr(), s))
+    out32 = torch.empty_like(x)
+    x32 = x.float().contiguous()
+    check(L.ds_rmsnorm(x32.data_ptr(), 1, rows.data_ptr(), 3, 4096,
+                       w.data_ptr(), 1e-5, out32.data_ptr(), s))
+    torch.cuda.synchronize()
+    assert torch.equal(out32[:3], out[:3])
     xf = x.float()[[6, 0, 3]]
     ref = xf * torch.rsqrt((xf * xf).mean(-1, keepdim=True) + 1e-5) * w.float()
     assert torch.allclose(out[:3].float(), _bf(ref).float(), atol=2e-2, rtol=1e-2)
@@ -40,8 +46,11 @@ def test_rmsnorm_silu_embed_argmax(cuda):
     table = torch.randn(100, 1024, device=cuda, generator=g).bfloat16()
     tok = torch.tensor([5, 99, 0], dtype=torch.int32, device=cuda)
     emb = torch.empty(3, 1024, device=cuda, dtype=torch.bfloat16)
-    check(L.ds_embed(tok.data_ptr(), 3, table.data_ptr(), 1024, emb.data_ptr(), s))
+    check(L.ds_embed(tok.data_ptr(), 3, table.data_ptr(), 1024, emb.data_ptr(), 0, s))
     assert torch.equal(emb, table[[5, 99, 0]])
+    emb32 = torch.empty(3, 1024, device=cuda, dtype=torch.float32)
+    check(L.ds_embed(tok.data_ptr(), 3, table.data_ptr(), 1024, emb32.data_ptr(), 1, s))
+    assert torch.equal(emb32, table[[5, 99, 0]].float())
     logits = torch.randn(4, 128256, device=cuda, generator=g)
     logits[2, 77] = logits[2, 1000] = 1e4  # tie -> lowest index
     am = torch.empty(4, dtype=torch.int32, device=cuda)
@@ -114,10 +123,11 @@ def test_rope_kv_store(cuda):
     kp = torch.zeros(64, nkv, d, dtype=torch.bfloat16, device=cuda)
     vp = torch.zeros_like(kp)
     qd = qkv.to(cuda)
-    check(lib().ds_rope_kv_store(qd.data_ptr(), T, row_seq.to(cuda).data_ptr(),
-                                 row_pos.to(cuda).data_ptr(), pos2cell.to(cuda).data_ptr(), 64,
-                                 nh, nkv, d, cos.to(cuda).data_ptr(), sin.to(cuda).data_ptr(),
-                                 kp.data_ptr(), vp.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    keep = [t.to(cuda) for t in (row_seq, row_pos, pos2cell, cos, sin)]  # keep alive
+    rs, rp, p2c, cd, sd = keep
+    check(lib().ds_rope_kv_store(qd.data_ptr(), T, rs.data_ptr(), rp.data_ptr(), p2c.data_ptr(),
+                                 64, nh, nkv, d, cd.data_ptr(), sd.data_ptr(), kp.data_ptr(),
+                                 vp.data_ptr(), torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     from oracle.llama_ref import rope
 
