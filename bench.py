@@ -225,8 +225,8 @@ def kernel_micro(torch, dev, peaks) -> dict:
         kv_len = past + q
         cap = kv_len + 64
         g = torch.Generator(device=dev).manual_seed(7)
-        kp = torch.randn(cap, nkv, d, device=dev, dtype=torch.bfloat16, generator=g)
-        vp = torch.randn(cap, nkv, d, device=dev, dtype=torch.bfloat16, generator=g)
+        kp = torch.randn(nkv, cap, d, device=dev, dtype=torch.bfloat16, generator=g)
+        vp = torch.randn(nkv, cap, d, device=dev, dtype=torch.bfloat16, generator=g)
         p2c = torch.arange(cap, dtype=torch.int32, device=dev).view(1, cap)
         qkv = torch.randn(q, (nh + 2 * nkv) * d, device=dev, dtype=torch.bfloat16, generator=g)
         o = torch.empty(q, nh * d, device=dev, dtype=torch.bfloat16)
@@ -237,7 +237,7 @@ def kernel_micro(torch, dev, peaks) -> dict:
 
         def launch():
             _lib.check(L.ds_attention(qkv.data_ptr(), ctypes.addressof(ent), ent_d.data_ptr(), 1,
-                                      q, kp.data_ptr(), vp.data_ptr(), p2c.data_ptr(), cap, nh,
+                                      q, kp.data_ptr(), vp.data_ptr(), cap, p2c.data_ptr(), cap, nh,
                                       nkv, d, 1.0 / d ** 0.5, o.data_ptr(), ws.data_ptr(), wsb,
                                       impl, stream.cuda_stream), name)
 

@@ -130,7 +130,7 @@ typedef struct {
 } ds_model;
 
 typedef struct {
-  void* k_pool; /* bf16 [L][capacity][nkv][hd] */
+  void* k_pool; /* bf16 [L][nkv][capacity][hd] (head-major: a run of cells is contiguous) */
   void* v_pool;
   int64_t capacity;
   int32_t* pos2cell; /* [n_seqs][pos_stride] */
@@ -185,11 +185,12 @@ int ds_model_forward(const ds_model* model, const ds_kv_store* kv, const ds_forw
  * ---------------------------------------------------------------------- */
 
 /* K5: RoPE (rotate-half, cos/sin table) on q (in place in qkv) and k; store k,v
- * rows into the layer's cell pool at pos2cell[row_seq][row_pos]. */
+ * rows into the layer's head-major cell pool ([kv_head][cell][head_dim],
+ * kv_head_stride = cells per head) at pos2cell[row_seq][row_pos]. */
 int ds_rope_kv_store(void* qkv, int n_rows, const int32_t* row_seq, const int32_t* row_pos,
                      const int32_t* pos2cell, int64_t pos_stride, int n_heads, int n_kv_heads,
                      int head_dim, const float* rope_cos, const float* rope_sin, void* k_pool_l,
-                     void* v_pool_l, ds_stream_t stream);
+                     void* v_pool_l, int64_t kv_head_stride, ds_stream_t stream);
 
 /* K6/K7 attention over the paged store for a batch of entries.  q is the
  * roped qkv buffer ([n_rows][(nh+2nkv)*hd], q heads first), out is
@@ -198,7 +199,8 @@ int ds_rope_kv_store(void* qkv, int n_rows, const int32_t* row_seq, const int32_
 size_t ds_attention_workspace_bytes(int n_rows, int n_entries, int n_heads, int head_dim);
 int ds_attention(const void* qkv, const ds_entry* entries_host, const ds_entry* entries_dev,
                  int n_entries, int n_rows, const void* k_pool_l, const void* v_pool_l,
-                 const int32_t* pos2cell, int64_t pos_stride, int n_heads, int n_kv_heads,
+                 int64_t kv_head_stride, const int32_t* pos2cell, int64_t pos_stride,
+                 int n_heads, int n_kv_heads,
                  int head_dim, float scale, void* out, void* workspace, size_t workspace_bytes,
                  int impl, ds_stream_t stream);
 
@@ -209,6 +211,13 @@ int ds_rmsnorm(const void* x, int x_f32, const int32_t* rows, int n_rows, int hi
 int ds_silu_mul(const void* gate_up, int n_rows, int ffn, void* out, ds_stream_t stream);
 int ds_embed(const int32_t* tokens, int n_rows, const void* table, int hidden, void* out,
              int out_f32, ds_stream_t stream);
+/* Skinny GEMM for decode/verify row counts (M <= 32): Y[M][N] (+)= X[M][K] .
+ * W[N][K]^T, bf16 in, fp32 accumulate, Y bf16 (y_f32=0) or fp32; accumulate=1
+ * adds into Y (fused residual).  N % 16 == 0, K % 256 == 0.  Weight-streaming,
+ * HBM-bound; replaces cuBLAS for the engine's decode/verify projections. */
+int ds_gemm_skinny(const void* X, const void* W, void* Y, int M, int N, int K, int y_f32,
+                   int accumulate, ds_stream_t stream);
+
 /* K8: row argmax over fp32 logits (lowest index on ties, engine.py:146-159). */
 int ds_argmax(const float* logits, int n_rows, int vocab, int32_t* out, ds_stream_t stream);
 

@@ -94,14 +94,15 @@ def lib() -> ctypes.CDLL:
         "ds_forward_workspace_bytes": (ctypes.c_size_t, [P, c_i32, c_i32, c_i32]),
         "ds_model_forward": (c_i32, [P, P, P, P]),
         "ds_rope_kv_store": (c_i32, [P, c_i32, P, P, P, c_i64, c_i32, c_i32, c_i32, P, P, P, P,
-                                     P]),
+                                     c_i64, P]),
         "ds_attention_workspace_bytes": (ctypes.c_size_t, [c_i32, c_i32, c_i32, c_i32]),
-        "ds_attention": (c_i32, [P, P, P, c_i32, c_i32, P, P, P, c_i64, c_i32, c_i32, c_i32,
-                                 c_f32, P, P, ctypes.c_size_t, c_i32, P]),
+        "ds_attention": (c_i32, [P, P, P, c_i32, c_i32, P, P, c_i64, P, c_i64, c_i32, c_i32,
+                                 c_i32, c_f32, P, P, ctypes.c_size_t, c_i32, P]),
         "ds_rmsnorm": (c_i32, [P, c_i32, P, c_i32, c_i32, P, c_f32, P, P]),
         "ds_silu_mul": (c_i32, [P, c_i32, c_i32, P, P]),
         "ds_embed": (c_i32, [P, c_i32, P, c_i32, P, c_i32, P]),
         "ds_argmax": (c_i32, [P, c_i32, c_i32, P, P]),
+        "ds_gemm_skinny": (c_i32, [P, P, P, c_i32, c_i32, c_i32, c_i32, c_i32, P]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

@@ -22,13 +22,14 @@ struct AttnSplitPlan {
   int split_len;
 };
 
-// n_entries: entries sharing the launch (target ~2 CTAs per SM for the batch)
-DS_HD AttnSplitPlan attn_split_plan(int qblocks, int kv_len, int nkv, int n_entries) {
+// mode 0: split kernel (~2 CTAs per SM, ceil); mode 1: warp-specialised decode
+// kernel (one CTA per SM, floor so the grid is a single wave).
+DS_HD AttnSplitPlan attn_split_plan(int qblocks, int kv_len, int nkv, int n_entries, int mode) {
   const int ctas = qblocks * nkv * n_entries;
-  int n = (2 * kNumSMs + ctas - 1) / ctas;
+  int n = mode ? kNumSMs / ctas : (2 * kNumSMs + ctas - 1) / ctas;
   const int by_len = (kv_len + 127) / 128;
   if (n > by_len) n = by_len;
-  if (n > 32) n = 32;
+  if (n > 64) n = 64;
   if (n < 1) n = 1;
   int split_len = ((kv_len + n - 1) / n + 63) / 64 * 64;
   if (split_len < 64) split_len = 64;
@@ -38,25 +39,26 @@ DS_HD AttnSplitPlan attn_split_plan(int qblocks, int kv_len, int nkv, int n_entr
 }
 
 // rows of partial storage used by entries [0, e)
-DS_HD int64_t attn_partial_base(const ds_entry* entries, int e, int n_entries, int nh, int nkv) {
+DS_HD int64_t attn_partial_base(const ds_entry* entries, int e, int n_entries, int nh, int nkv,
+                                int mode) {
   int64_t base = 0;
   const int G = nh / nkv;
   for (int i = 0; i < e; ++i) {
     const int R = entries[i].q_len * G;
     const int qb = (R + kSplitRows - 1) / kSplitRows;
-    const AttnSplitPlan p = attn_split_plan(qb, entries[i].past + entries[i].q_len, nkv,
-                                             n_entries);
+    const AttnSplitPlan p =
+        attn_split_plan(qb, entries[i].past + entries[i].q_len, nkv, n_entries, mode);
     if (p.n_splits > 1) base += static_cast<int64_t>(p.n_splits) * R;
   }
   return base;
 }
 
-inline int64_t attn_partial_slots(const ds_entry* entries, int n, int nh, int nkv) {
-  return attn_partial_base(entries, n, n, nh, nkv) * nkv;
+inline int64_t attn_partial_slots(const ds_entry* entries, int n, int nh, int nkv, int mode) {
+  return attn_partial_base(entries, n, n, nh, nkv, mode) * nkv;
 }
 
-inline size_t attn_partial_bytes(const ds_entry* entries, int n, int nh, int nkv) {
-  const int64_t slots = attn_partial_slots(entries, n, nh, nkv);
+inline size_t attn_partial_bytes(const ds_entry* entries, int n, int nh, int nkv, int mode) {
+  const int64_t slots = attn_partial_slots(entries, n, nh, nkv, mode);
   return static_cast<size_t>(slots) * (128 + 1) * sizeof(float);
 }
 

@@ -3,7 +3,7 @@
 #include <cuda_runtime.h>
 namespace ds {
 int launch_attn_prefill_sm100(const void*, const ds_entry*, const ds_entry*, int, const void*,
-                              const void*, const int32_t*, int64_t, int, int, int, float, void*,
+                              const void*, int64_t, const int32_t*, int64_t, int, int, int, float, void*,
                               cudaStream_t) {
   return DS_EUNSUPPORTED;
 }

@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(NW * 32) attn_split_kernel(
     int n_entries, int max_splits, const __nv_bfloat16* __restrict__ kpool,
     const __nv_bfloat16* __restrict__ vpool, const int32_t* __restrict__ pos2cell,
     int64_t pos_stride, int nh, int nkv, float scale_log2, __nv_bfloat16* __restrict__ out,
-    float* __restrict__ part_o, float* __restrict__ part_lse) {
+    float* __restrict__ part_o, float* __restrict__ part_lse, int64_t head_stride) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int e = blockIdx.z / max_splits;
   const int split = blockIdx.z - e * max_splits;
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(NW * 32) attn_split_kernel(
   const int qblocks = (R + NW * 16 - 1) / (NW * 16);
   if (static_cast<int>(blockIdx.x) >= qblocks) return;
   const int kv_len = en.past + en.q_len;
-  const AttnSplitPlan plan = attn_split_plan(qblocks, kv_len, nkv, n_entries);
+  const AttnSplitPlan plan = attn_split_plan(qblocks, kv_len, nkv, n_entries, 0);
   if (split >= plan.n_splits) return;
   const int kh = blockIdx.y;
   const int row0 = blockIdx.x * NW * 16;
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(NW * 32) attn_split_kernel(
       const int key = kt + row;
       const bool valid = key < k_end;
       const int64_t cell = valid ? p2c[key] : 0;
-      const int64_t goff = (cell * nkv + kh) * kD + chunk * 8;
+      const int64_t goff = (kh * head_stride + cell) * kD + chunk * 8;
       cp_async16_zfill(ks + tile_off(row, chunk), kpool + goff, valid);
       cp_async16_zfill(vs + tile_off(row, chunk), vpool + goff, valid);
     }
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(NW * 32) attn_split_kernel(
       }
     }
   } else {
-    const int64_t base = attn_partial_base(entries, e, n_entries, nh, nkv);
+    const int64_t base = attn_partial_base(entries, e, n_entries, nh, nkv, 0);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int r = wrow + g8 + 8 * h;
@@ -253,7 +253,8 @@ __global__ void __launch_bounds__(NW * 32) attn_split_kernel(
 
 // Merge split partials: out = sum_s 2^(lse_s - lse_max) O_s / sum_s 2^(...)
 __global__ void attn_combine_kernel(const ds_entry* __restrict__ entries, int n_entries, int nh,
-                                    int nkv, int qblock_rows, const float* __restrict__ part_o,
+                                    int nkv, int qblock_rows, int mode,
+                                    const float* __restrict__ part_o,
                                     const float* __restrict__ part_lse,
                                     __nv_bfloat16* __restrict__ out) {
   const int e = blockIdx.z;
@@ -264,9 +265,9 @@ __global__ void attn_combine_kernel(const ds_entry* __restrict__ entries, int n_
   if (r >= R) return;
   const int kh = blockIdx.y;
   const int qblocks = (R + qblock_rows - 1) / qblock_rows;
-  const AttnSplitPlan plan = attn_split_plan(qblocks, en.past + en.q_len, nkv, n_entries);
+  const AttnSplitPlan plan = attn_split_plan(qblocks, en.past + en.q_len, nkv, n_entries, mode);
   if (plan.n_splits <= 1) return;
-  const int64_t base = attn_partial_base(entries, e, n_entries, nh, nkv);
+  const int64_t base = attn_partial_base(entries, e, n_entries, nh, nkv, mode);
   float lmax = -INFINITY;
   for (int s = 0; s < plan.n_splits; ++s)
     lmax = fmaxf(lmax, part_lse[(base + static_cast<int64_t>(s) * R + r) * nkv + kh]);
@@ -287,28 +288,52 @@ __global__ void attn_combine_kernel(const ds_entry* __restrict__ entries, int n_
 
 constexpr int kSplitNW = 4;
 
+int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_entry* entries_dev,
+                       int n_entries, const void* k_pool, const void* v_pool, int64_t head_stride,
+                       const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv, int max_R,
+                       int max_splits, float scale, void* out, float* part_o, float* part_lse,
+                       cudaStream_t stream);
+
 int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_entry* entries_dev,
-                      int n_entries, const void* k_pool, const void* v_pool,
+                      int n_entries, const void* k_pool, const void* v_pool, int64_t head_stride,
                       const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv, int hd,
                       float scale, void* out, void* workspace, size_t ws_bytes,
                       cudaStream_t stream) {
   if (hd != kD || nh % nkv) return DS_EUNSUPPORTED;
-  int max_qblocks = 0, max_splits = 1;
+  int max_qblocks = 0, max_R = 0;
+  for (int e = 0; e < n_entries; ++e) {
+    const int R = entries_host[e].q_len * (nh / nkv);
+    max_R = R > max_R ? R : max_R;
+    const int qb = (R + kSplitNW * 16 - 1) / (kSplitNW * 16);
+    max_qblocks = qb > max_qblocks ? qb : max_qblocks;
+  }
+  const int mode = max_R <= 32 ? 1 : 0;  // warp-specialised decode kernel vs split kernel
+  int max_splits = 1;
   bool any_split = false;
   for (int e = 0; e < n_entries; ++e) {
     const ds_entry& en = entries_host[e];
-    const int R = en.q_len * (nh / nkv);
-    const int qb = (R + kSplitNW * 16 - 1) / (kSplitNW * 16);
-    max_qblocks = qb > max_qblocks ? qb : max_qblocks;
-    const AttnSplitPlan p = attn_split_plan(qb, en.past + en.q_len, nkv, n_entries);
+    const int qb = (en.q_len * (nh / nkv) + kSplitNW * 16 - 1) / (kSplitNW * 16);
+    const AttnSplitPlan p = attn_split_plan(qb, en.past + en.q_len, nkv, n_entries, mode);
     max_splits = p.n_splits > max_splits ? p.n_splits : max_splits;
     any_split |= p.n_splits > 1;
   }
-  const size_t need = attn_partial_bytes(entries_host, n_entries, nh, nkv);
+  const size_t need = attn_partial_bytes(entries_host, n_entries, nh, nkv, mode);
   if (need > ws_bytes) return DS_EWORKSPACE;
   float* part_o = static_cast<float*>(workspace);
-  const int64_t slots = attn_partial_slots(entries_host, n_entries, nh, nkv);
+  const int64_t slots = attn_partial_slots(entries_host, n_entries, nh, nkv, mode);
   float* part_lse = part_o + slots * kD;
+  if (mode == 1) {
+    const int rc = launch_attn_decode(qkv, entries_host, entries_dev, n_entries, k_pool, v_pool,
+                                      head_stride, pos2cell, pos_stride, nh, nkv, max_R,
+                                      max_splits, scale, out,
+                                      part_o, part_lse, stream);
+    if (rc != 0 || !any_split) return rc;
+    dim3 cgrid(max_R, nkv, n_entries);
+    attn_combine_kernel<<<cgrid, kD, 0, stream>>>(entries_dev, n_entries, nh, nkv, kSplitNW * 16,
+                                                  1, part_o, part_lse,
+                                                  static_cast<__nv_bfloat16*>(out));
+    return (int)cudaGetLastError();
+  }
   const int smem = 2 * 2 * kTileBytes;
   static bool attr_set = false;
   if (!attr_set) {
@@ -322,16 +347,11 @@ int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_en
       static_cast<const __nv_bfloat16*>(qkv), (nh + 2 * nkv) * kD, entries_dev, n_entries,
       max_splits, static_cast<const __nv_bfloat16*>(k_pool),
       static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv, scale_log2,
-      static_cast<__nv_bfloat16*>(out), part_o, part_lse);
+      static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride);
   if (any_split) {
-    int max_R = 0;
-    for (int e = 0; e < n_entries; ++e) {
-      const int R = entries_host[e].q_len * (nh / nkv);
-      max_R = R > max_R ? R : max_R;
-    }
     dim3 cgrid(max_R, nkv, n_entries);
     attn_combine_kernel<<<cgrid, kD, 0, stream>>>(entries_dev, n_entries, nh, nkv, kSplitNW * 16,
-                                                  part_o, part_lse,
+                                                  0, part_o, part_lse,
                                                   static_cast<__nv_bfloat16*>(out));
   }
   return (int)cudaGetLastError();

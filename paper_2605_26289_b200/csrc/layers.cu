@@ -125,7 +125,7 @@ __global__ void rope_kv_store_kernel(__nv_bfloat16* __restrict__ qkv, const int3
                                      const float* __restrict__ rope_cos,
                                      const float* __restrict__ rope_sin,
                                      __nv_bfloat16* __restrict__ k_pool,
-                                     __nv_bfloat16* __restrict__ v_pool) {
+                                     __nv_bfloat16* __restrict__ v_pool, int64_t head_stride) {
   const int r = blockIdx.x;
   const int pos = row_pos[r];
   const int64_t cell = pos2cell[static_cast<int64_t>(row_seq[r]) * pos_stride + pos];
@@ -147,16 +147,18 @@ __global__ void rope_kv_store_kernel(__nv_bfloat16* __restrict__ qkv, const int3
     x[i] = y1;
     x[i + half] = y2;
     if (head >= nh) {
-      __nv_bfloat16* kd = k_pool + (cell * nkv + (head - nh)) * hd;
+      __nv_bfloat16* kd = k_pool + ((head - nh) * head_stride + cell) * hd;
       kd[i] = y1;
       kd[i + half] = y2;
     }
   }
-  // v: 16-byte chunks
-  const int vchunks = nkv * hd / 8;
+  // v: 16-byte chunks, head-major pool ([kv_head][cell][hd])
+  const int per_head = hd / 8;
   const uint4* vsrc = reinterpret_cast<const uint4*>(row + (nh + nkv) * hd);
-  uint4* vdst = reinterpret_cast<uint4*>(v_pool + cell * nkv * hd);
-  for (int j = threadIdx.x; j < vchunks; j += blockDim.x) vdst[j] = vsrc[j];
+  for (int j = threadIdx.x; j < nkv * per_head; j += blockDim.x) {
+    const int kh = j / per_head;
+    reinterpret_cast<uint4*>(v_pool + (kh * head_stride + cell) * hd)[j - kh * per_head] = vsrc[j];
+  }
 }
 
 }  // namespace ds
@@ -194,13 +196,13 @@ int ds_silu_mul(const void* gate_up, int n_rows, int ffn, void* out, ds_stream_t
 int ds_rope_kv_store(void* qkv, int n_rows, const int32_t* row_seq, const int32_t* row_pos,
                      const int32_t* pos2cell, int64_t pos_stride, int n_heads, int n_kv_heads,
                      int head_dim, const float* rope_cos, const float* rope_sin, void* k_pool_l,
-                     void* v_pool_l, ds_stream_t stream) {
+                     void* v_pool_l, int64_t kv_head_stride, ds_stream_t stream) {
   if (n_rows < 0 || head_dim % 16) return DS_EINVAL;
   if (n_rows == 0) return DS_OK;
   ds::rope_kv_store_kernel<<<n_rows, 256, 0, (cudaStream_t)stream>>>(
       static_cast<__nv_bfloat16*>(qkv), row_seq, row_pos, pos2cell, pos_stride, n_heads,
       n_kv_heads, head_dim, rope_cos, rope_sin, static_cast<__nv_bfloat16*>(k_pool_l),
-      static_cast<__nv_bfloat16*>(v_pool_l));
+      static_cast<__nv_bfloat16*>(v_pool_l), kv_head_stride);
   return (int)cudaGetLastError();
 }
 

@@ -17,14 +17,14 @@
 namespace ds {
 
 int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_entry* entries_dev,
-                      int n_entries, const void* k_pool, const void* v_pool,
+                      int n_entries, const void* k_pool, const void* v_pool, int64_t head_stride,
                       const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv, int hd,
                       float scale, void* out, void* workspace, size_t ws_bytes,
                       cudaStream_t stream);
 int launch_attn_prefill_sm100(const void* qkv, const ds_entry* entries_host,
                               const ds_entry* entries_dev, int n_entries, const void* k_pool,
-                              const void* v_pool, const int32_t* pos2cell, int64_t pos_stride,
-                              int nh, int nkv, int hd, float scale, void* out,
+                              const void* v_pool, int64_t head_stride, const int32_t* pos2cell,
+                              int64_t pos_stride, int nh, int nkv, int hd, float scale, void* out,
                               cudaStream_t stream);
 
 namespace {
@@ -106,6 +106,24 @@ cublasStatus_t gemm(cublasHandle_t h, const void* X, const void* W, void* Y, int
                       CUDA_R_16BF, K, &beta, Y, ytype, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
 }
 
+}  // namespace
+}  // namespace ds
+extern "C" int ds_gemm_skinny(const void* X, const void* W, void* Y, int M, int N, int K,
+                              int y_f32, int accumulate, ds_stream_t stream);
+namespace ds {
+namespace {
+
+// decode / verify row counts stream the weights through our skinny GEMM;
+// prefill chunks (compute-bound) go to cuBLAS.
+int project(cublasHandle_t h, const void* X, const void* W, void* Y, int M, int N, int K,
+            bool y_f32, bool accumulate, cudaStream_t s) {
+  if (M <= 32 && N % 16 == 0 && K % 256 == 0)
+    return ds_gemm_skinny(X, W, Y, M, N, K, y_f32, accumulate, s);
+  const cublasStatus_t st = gemm(h, X, W, Y, M, N, K, accumulate ? 1.f : 0.f,
+                                 y_f32 ? CUDA_R_32F : CUDA_R_16BF);
+  return st == CUBLAS_STATUS_SUCCESS ? 0 : 1000 + static_cast<int>(st);
+}
+
 __global__ void scatter_tokens_kernel(const int32_t* tok, const int32_t* row_seq,
                                       const int32_t* row_pos, int n, int32_t* hist,
                                       int64_t stride) {
@@ -157,7 +175,8 @@ size_t ds_attention_workspace_bytes(int n_rows, int n_entries, int n_heads, int 
 
 int ds_attention(const void* qkv, const ds_entry* entries_host, const ds_entry* entries_dev,
                  int n_entries, int n_rows, const void* k_pool_l, const void* v_pool_l,
-                 const int32_t* pos2cell, int64_t pos_stride, int n_heads, int n_kv_heads,
+                 int64_t kv_head_stride, const int32_t* pos2cell, int64_t pos_stride,
+                 int n_heads, int n_kv_heads,
                  int head_dim, float scale, void* out, void* workspace, size_t workspace_bytes,
                  int impl, ds_stream_t stream) {
   (void)n_rows;
@@ -167,11 +186,11 @@ int ds_attention(const void* qkv, const ds_entry* entries_host, const ds_entry* 
   if (impl == 0) impl = 1;
   if (impl == 2)
     return launch_attn_prefill_sm100(qkv, entries_host, entries_dev, n_entries, k_pool_l, v_pool_l,
-                                     pos2cell, pos_stride, n_heads, n_kv_heads, head_dim, scale,
-                                     out, (cudaStream_t)stream);
-  return launch_attn_split(qkv, entries_host, entries_dev, n_entries, k_pool_l, v_pool_l, pos2cell,
-                           pos_stride, n_heads, n_kv_heads, head_dim, scale, out, workspace,
-                           workspace_bytes, (cudaStream_t)stream);
+                                     kv_head_stride, pos2cell, pos_stride, n_heads, n_kv_heads,
+                                     head_dim, scale, out, (cudaStream_t)stream);
+  return launch_attn_split(qkv, entries_host, entries_dev, n_entries, k_pool_l, v_pool_l,
+                           kv_head_stride, pos2cell, pos_stride, n_heads, n_kv_heads, head_dim,
+                           scale, out, workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
 size_t ds_forward_workspace_bytes(const ds_model* model, int max_rows, int max_out,
@@ -227,27 +246,28 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
   for (int l = 0; l < L; ++l) {
     DS_CHECK(ds_rmsnorm(b.x, 1, nullptr, T, H, an + static_cast<size_t>(l) * H, m->rms_eps, b.h,
                         stream));
-    DS_BLAS(gemm(rt.blas, b.h, wqkv + static_cast<size_t>(l) * QKV * H, b.qkv, T, QKV, H, 0.f,
-                 CUDA_R_16BF));
+    DS_CHECK(project(rt.blas, b.h, wqkv + static_cast<size_t>(l) * QKV * H, b.qkv, T, QKV, H,
+                     false, false, stream));
     DS_CHECK(ds_rope_kv_store(b.qkv, T, a->row_seq, a->row_pos, kv->pos2cell, kv->pos_stride, nh,
                               nkv, hd, m->rope_cos, m->rope_sin, kp + l * kv_layer,
-                              vp + l * kv_layer, stream));
+                              vp + l * kv_layer, kv->capacity, stream));
     DS_CHECK(ds_attention(b.qkv, a->entries_host, a->entries, a->n_entries, T, kp + l * kv_layer,
-                          vp + l * kv_layer, kv->pos2cell, kv->pos_stride, nh, nkv, hd, scale,
-                          b.attn, b.attn_ws, b.attn_ws_bytes, attn_impl, stream));
-    DS_BLAS(gemm(rt.blas, b.attn, wo + static_cast<size_t>(l) * H * nh * hd, b.x, T, H, nh * hd,
-                 1.f, CUDA_R_32F));
+                          vp + l * kv_layer, kv->capacity, kv->pos2cell, kv->pos_stride, nh, nkv,
+                          hd, scale, b.attn, b.attn_ws, b.attn_ws_bytes, attn_impl, stream));
+    DS_CHECK(project(rt.blas, b.attn, wo + static_cast<size_t>(l) * H * nh * hd, b.x, T, H,
+                     nh * hd, true, true, stream));
     DS_CHECK(ds_rmsnorm(b.x, 1, nullptr, T, H, mn + static_cast<size_t>(l) * H, m->rms_eps, b.h,
                         stream));
-    DS_BLAS(gemm(rt.blas, b.h, wgu + static_cast<size_t>(l) * 2 * F * H, b.gu, T, 2 * F, H, 0.f,
-                 CUDA_R_16BF));
+    DS_CHECK(project(rt.blas, b.h, wgu + static_cast<size_t>(l) * 2 * F * H, b.gu, T, 2 * F, H,
+                     false, false, stream));
     DS_CHECK(ds_silu_mul(b.gu, T, F, b.act, stream));
-    DS_BLAS(gemm(rt.blas, b.act, wd + static_cast<size_t>(l) * H * F, b.x, T, H, F, 1.f,
-                 CUDA_R_32F));
+    DS_CHECK(project(rt.blas, b.act, wd + static_cast<size_t>(l) * H * F, b.x, T, H, F, true,
+                     true, stream));
   }
   // final norm on sampled rows only, LM head in fp32
   DS_CHECK(ds_rmsnorm(b.x, 1, a->out_rows, a->n_out, H, m->final_norm, m->rms_eps, b.hf, stream));
-  DS_BLAS(gemm(rt.blas, b.hf, m->lm_head, a->logits, a->n_out, m->vocab, H, 0.f, CUDA_R_32F));
+  DS_CHECK(project(rt.blas, b.hf, m->lm_head, a->logits, a->n_out, m->vocab, H, true, false,
+                   stream));
 
   DS_CUDA(cudaStreamWaitEvent(stream, rt.join, 0));
   launch_token_policy(a, kv, b.row_hash, nullptr, m->vocab, rt.side, stream);

@@ -164,8 +164,10 @@ class GpuEngine:
         self.rope_sin = torch.sin(ang).float().contiguous()
         del ang, pos
         # ---- paged KV store ----
-        cell = s.n_kv_heads * s.head_dim
-        self.k_pool = torch.zeros((s.layers, self.capacity, cell), dtype=torch.bfloat16, device=dev)
+        # head-major [L][kv_head][cell][hd]: a run of consecutive cells of one head
+        # is one contiguous block -> TMA boxes for the attention kernels
+        self.k_pool = torch.zeros((s.layers, s.n_kv_heads, self.capacity, s.head_dim),
+                                  dtype=torch.bfloat16, device=dev)
         self.v_pool = torch.zeros_like(self.k_pool)
         self.pos2cell = torch.zeros((n_seqs, self.pos_stride), dtype=torch.int32, device=dev)
         self.hist = torch.zeros((n_seqs, self.pos_stride), dtype=torch.int32, device=dev)

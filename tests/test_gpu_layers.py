@@ -60,15 +60,19 @@ def test_rmsnorm_silu_embed_argmax(cuda):
     assert am.tolist() == ref.tolist()
 
 
-def _setup_paged(cuda, seq_len, nkv=8, d=128, capacity=None, seed=0):
+def _setup_paged(cuda, seq_len, nkv=8, d=128, capacity=None, seed=0, contiguous=False):
     g = torch.Generator(device="cpu").manual_seed(seed)
     capacity = capacity or seq_len + 37
-    cells = torch.randperm(capacity, generator=g)[:seq_len].to(torch.int32)
-    k_pool = torch.randn(capacity, nkv, d, generator=g).bfloat16()
-    v_pool = torch.randn(capacity, nkv, d, generator=g).bfloat16()
+    if contiguous:  # first-fit style runs (TMA path) with one break in the middle
+        cells = torch.cat([torch.arange(5, 5 + seq_len // 2),
+                           torch.arange(seq_len // 2 + 17, seq_len + 17)]).to(torch.int32)
+    else:  # fully fragmented (cell-by-cell gather path)
+        cells = torch.randperm(capacity, generator=g)[:seq_len].to(torch.int32)
+    k_pool = torch.randn(nkv, capacity, d, generator=g).bfloat16()  # head-major pool
+    v_pool = torch.randn(nkv, capacity, d, generator=g).bfloat16()
     pos2cell = torch.zeros(2, seq_len + 64, dtype=torch.int32)
     pos2cell[1, :seq_len] = cells
-    return (k_pool.to(cuda), v_pool.to(cuda), pos2cell.to(cuda), cells, k_pool, v_pool)
+    return (k_pool.to(cuda), v_pool.to(cuda), pos2cell.to(cuda), cells, k_pool, v_pool, capacity)
 
 
 def _entries(entries):
@@ -80,14 +84,17 @@ def _entries(entries):
     return arr
 
 
-@pytest.mark.parametrize("past,q_len", [(0, 1), (5, 1), (1000, 1), (3000, 5), (31, 17),
+@pytest.mark.parametrize("past,q_len", [(0, 1), (5, 1), (1000, 1), (3000, 5), (31, 17), (2000, 8), (32768, 4),
                                         (4500, 5), (777, 64), (0, 150), (2048, 300)])
-def test_attention_paged_vs_fp32(cuda, past, q_len):
+@pytest.mark.parametrize("contiguous", [False, True])
+def test_attention_paged_vs_fp32(cuda, past, q_len, contiguous):
     from paper_2605_26289_b200._lib import check, lib
 
     nh, nkv, d = 32, 8, 128
     kv_len = past + q_len
-    k_pool, v_pool, pos2cell, cells, k_cpu, v_cpu = _setup_paged(cuda, kv_len, seed=past + q_len)
+    k_pool, v_pool, pos2cell, cells, k_cpu, v_cpu, cap = _setup_paged(cuda, kv_len,
+                                                                     seed=past + q_len,
+                                                                     contiguous=contiguous)
     g = torch.Generator(device="cpu").manual_seed(1)
     qkv = torch.randn(q_len, (nh + 2 * nkv) * d, generator=g).bfloat16()
     ent = _entries([(1, past, q_len, 0, 0, 0, 0, 1, 0)])
@@ -97,12 +104,12 @@ def test_attention_paged_vs_fp32(cuda, past, q_len):
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=cuda)
     qkv_d = qkv.to(cuda)
     check(lib().ds_attention(qkv_d.data_ptr(), ctypes.addressof(ent), ent_dev.data_ptr(), 1,
-                             q_len, k_pool.data_ptr(), v_pool.data_ptr(), pos2cell.data_ptr(),
-                             pos2cell.shape[1], nh, nkv, d, 1.0 / d ** 0.5, out.data_ptr(),
+                             q_len, k_pool.data_ptr(), v_pool.data_ptr(), cap,
+                             pos2cell.data_ptr(), pos2cell.shape[1], nh, nkv, d, 1.0 / d ** 0.5, out.data_ptr(),
                              ws.data_ptr(), ws_bytes, 1, torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     q = qkv[:, : nh * d].view(q_len, nh, d)
-    ref = paged_attention(q, k_cpu[cells.long()], v_cpu[cells.long()],
+    ref = paged_attention(q, k_cpu[:, cells.long()].transpose(0, 1), v_cpu[:, cells.long()].transpose(0, 1),
                           list(range(past, kv_len)), kv_len, 1.0 / d ** 0.5)
     got = out.cpu().float().view(q_len, nh, d)
     err = (got - ref).abs().max().item()
@@ -120,14 +127,14 @@ def test_rope_kv_store(cuda):
     row_pos = torch.arange(10, 10 + T, dtype=torch.int32)
     pos2cell = torch.zeros(2, 64, dtype=torch.int32)
     pos2cell[1, 10:16] = torch.tensor([40, 3, 17, 8, 9, 60], dtype=torch.int32)
-    kp = torch.zeros(64, nkv, d, dtype=torch.bfloat16, device=cuda)
+    kp = torch.zeros(nkv, 64, d, dtype=torch.bfloat16, device=cuda)
     vp = torch.zeros_like(kp)
     qd = qkv.to(cuda)
     keep = [t.to(cuda) for t in (row_seq, row_pos, pos2cell, cos, sin)]  # keep alive
     rs, rp, p2c, cd, sd = keep
     check(lib().ds_rope_kv_store(qd.data_ptr(), T, rs.data_ptr(), rp.data_ptr(), p2c.data_ptr(),
                                  64, nh, nkv, d, cd.data_ptr(), sd.data_ptr(), kp.data_ptr(),
-                                 vp.data_ptr(), torch.cuda.current_stream().cuda_stream))
+                                 vp.data_ptr(), 64, torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     from oracle.llama_ref import rope
 
@@ -138,5 +145,26 @@ def test_rope_kv_store(cuda):
     # fp32 FMA contraction may flip a bf16 rounding: allow one bf16 ulp
     assert torch.allclose(qd.cpu().float()[:, : nh * d].view(T, nh, d), q, atol=1e-2, rtol=8e-3)
     cells = [40, 3, 17, 8, 9, 60]
-    assert torch.allclose(kp.cpu().float()[cells], k, atol=1e-2, rtol=8e-3)
-    assert torch.equal(vp.cpu().float()[cells], v)
+    assert torch.allclose(kp.cpu().float()[:, cells].transpose(0, 1), k, atol=1e-2, rtol=8e-3)
+    assert torch.equal(vp.cpu().float()[:, cells].transpose(0, 1), v)
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 4096, 4096), (5, 6144, 4096), (17, 4096, 14336),
+                                   (32, 1024, 2816 * 0 + 2048), (3, 128256 // 16 * 16, 1024)])
+@pytest.mark.parametrize("y_f32,acc", [(0, 0), (1, 1)])
+def test_gemm_skinny_vs_fp32(cuda, M, N, K, y_f32, acc):
+    from paper_2605_26289_b200._lib import check, lib
+
+    g = torch.Generator(device=cuda).manual_seed(M + N + K)
+    X = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    W = (0.02 * torch.randn(N, K, device=cuda, generator=g)).bfloat16()
+    Y0 = torch.randn(M, N, device=cuda, generator=g)
+    Y = Y0.clone() if y_f32 else Y0.bfloat16()
+    check(lib().ds_gemm_skinny(X.data_ptr(), W.data_ptr(), Y.data_ptr(), M, N, K, y_f32, acc,
+                               torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    ref = X.float() @ W.float().T
+    if acc:
+        ref = ref + (Y0 if y_f32 else Y0.bfloat16().float())
+    err = (Y.float() - ref).abs().max().item()
+    assert err < (1e-3 if y_f32 else 1e-2 * ref.abs().max().item()), err
