@@ -183,7 +183,8 @@ int ds_attention(const void* qkv, const ds_entry* entries_host, const ds_entry* 
   if (n_entries <= 0 || n_kv_heads <= 0 || n_heads % n_kv_heads) return DS_EINVAL;
   int max_q = 0;
   for (int e = 0; e < n_entries; ++e) max_q = entries_host[e].q_len > max_q ? entries_host[e].q_len : max_q;
-  if (impl == 0) impl = 1;
+  // auto: decode / verify rows (R <= 32) -> K7; delta prefill -> tcgen05 K6
+  if (impl == 0) impl = max_q * (n_heads / n_kv_heads) > 32 ? 2 : 1;
   if (impl == 2)
     return launch_attn_prefill_sm100(qkv, entries_host, entries_dev, n_entries, k_pool_l, v_pool_l,
                                      kv_head_stride, pos2cell, pos_stride, n_heads, n_kv_heads,
@@ -218,7 +219,7 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
   int max_q = 0;
   for (int e = 0; e < a->n_entries; ++e)
     max_q = a->entries_host[e].q_len > max_q ? a->entries_host[e].q_len : max_q;
-  const int attn_impl = 1;
+  const int attn_impl = 0;  // auto
 
   DS_BLAS(cublasSetStream(rt.blas, stream));
   DS_BLAS(cublasSetWorkspace(rt.blas, b.blas_ws, kCublasWs));

@@ -88,6 +88,17 @@ def _entries(entries):
                                         (4500, 5), (777, 64), (0, 150), (2048, 300)])
 @pytest.mark.parametrize("contiguous", [False, True])
 def test_attention_paged_vs_fp32(cuda, past, q_len, contiguous):
+    _attention_case(cuda, past, q_len, contiguous, impl=1)
+
+
+@pytest.mark.parametrize("past,q_len", [(0, 32), (0, 150), (100, 33), (2048, 300), (3000, 881),
+                                        (127, 129), (5, 1)])
+@pytest.mark.parametrize("contiguous", [False, True])
+def test_attention_tcgen05_prefill_vs_fp32(cuda, past, q_len, contiguous):
+    _attention_case(cuda, past, q_len, contiguous, impl=2)
+
+
+def _attention_case(cuda, past, q_len, contiguous, impl):
     from paper_2605_26289_b200._lib import check, lib
 
     nh, nkv, d = 32, 8, 128
@@ -106,7 +117,7 @@ def test_attention_paged_vs_fp32(cuda, past, q_len, contiguous):
     check(lib().ds_attention(qkv_d.data_ptr(), ctypes.addressof(ent), ent_dev.data_ptr(), 1,
                              q_len, k_pool.data_ptr(), v_pool.data_ptr(), cap,
                              pos2cell.data_ptr(), pos2cell.shape[1], nh, nkv, d, 1.0 / d ** 0.5, out.data_ptr(),
-                             ws.data_ptr(), ws_bytes, 1, torch.cuda.current_stream().cuda_stream))
+                             ws.data_ptr(), ws_bytes, impl, torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     q = qkv[:, : nh * d].view(q_len, nh, d)
     ref = paged_attention(q, k_cpu[:, cells.long()].transpose(0, 1), v_cpu[:, cells.long()].transpose(0, 1),
