@@ -59,6 +59,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
   uint8_t* qs = smem + kStages * kStageBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(qs + kQRows * kD * 2);
   uint64_t* empty = full + kStages;
+  pdl_wait();
+  pdl_trigger();
 
   const int e = blockIdx.z / max_splits;
   const int split = blockIdx.z - e * max_splits;
@@ -342,11 +344,11 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
   const float sl2 = scale * 1.4426950408889634f;
   const int stride = (nh + 2 * nkv) * kD;
   auto kern = max_R <= 16 ? attn_decode_kernel<1> : attn_decode_kernel<2>;
-  kern<<<grid, kThreads, smem, stream>>>(
-      static_cast<const __nv_bfloat16*>(qkv), stride, entries_dev, n_entries, max_splits,
-      static_cast<const __nv_bfloat16*>(k_pool), static_cast<const __nv_bfloat16*>(v_pool),
-      pos2cell, pos_stride, nh, nkv, sl2, static_cast<__nv_bfloat16*>(out), part_o, part_lse,
-      head_stride, *tk, *tv);
+  launch_pdl(kern, grid, dim3(kThreads), smem, stream, static_cast<const __nv_bfloat16*>(qkv),
+             stride, entries_dev, n_entries, max_splits,
+             static_cast<const __nv_bfloat16*>(k_pool), static_cast<const __nv_bfloat16*>(v_pool),
+             pos2cell, pos_stride, nh, nkv, sl2, static_cast<__nv_bfloat16*>(out), part_o,
+             part_lse, head_stride, *tk, *tv);
   return (int)cudaGetLastError();
 }
 

@@ -63,6 +63,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_prefill_kernel(
   uint64_t* pv_done = bars + 8;    // [1] PV_j complete (P smem free, O stable)
   uint64_t* p_full = bars + 12;    // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  pdl_wait();
+  pdl_trigger();
 
   const ds_entry en = entries[blockIdx.z];
   const int G = nh / nkv;
@@ -313,11 +315,11 @@ int launch_attn_prefill_sm100(const void* qkv, const ds_entry* entries_host,
     max_qb = qb > max_qb ? qb : max_qb;
   }
   dim3 grid(max_qb, nkv, n_entries);
-  attn_prefill_kernel<<<grid, kThreads, kSmemBytes, stream>>>(
-      static_cast<const __nv_bfloat16*>(qkv), (nh + 2 * nkv) * kD, entries_dev,
-      static_cast<const __nv_bfloat16*>(k_pool), static_cast<const __nv_bfloat16*>(v_pool),
-      head_stride, pos2cell, pos_stride, nh, nkv, scale * 1.4426950408889634f,
-      static_cast<__nv_bfloat16*>(out), *tk, *tv);
+  launch_pdl(attn_prefill_kernel, grid, dim3(kThreads), kSmemBytes, stream,
+             static_cast<const __nv_bfloat16*>(qkv), (nh + 2 * nkv) * kD, entries_dev,
+             static_cast<const __nv_bfloat16*>(k_pool), static_cast<const __nv_bfloat16*>(v_pool),
+             head_stride, pos2cell, pos_stride, nh, nkv, scale * 1.4426950408889634f,
+             static_cast<__nv_bfloat16*>(out), *tk, *tv);
   return (int)cudaGetLastError();
 }
 

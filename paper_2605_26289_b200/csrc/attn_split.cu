@@ -257,6 +257,8 @@ __global__ void attn_combine_kernel(const ds_entry* __restrict__ entries, int n_
                                     const float* __restrict__ part_o,
                                     const float* __restrict__ part_lse,
                                     __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int e = blockIdx.z;
   const ds_entry en = entries[e];
   const int G = nh / nkv;
@@ -329,9 +331,8 @@ int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_en
                                       part_o, part_lse, stream);
     if (rc != 0 || !any_split) return rc;
     dim3 cgrid(max_R, nkv, n_entries);
-    attn_combine_kernel<<<cgrid, kD, 0, stream>>>(entries_dev, n_entries, nh, nkv, kSplitNW * 16,
-                                                  1, part_o, part_lse,
-                                                  static_cast<__nv_bfloat16*>(out));
+    launch_pdl(attn_combine_kernel, cgrid, dim3(kD), 0, stream, entries_dev, n_entries, nh, nkv,
+               kSplitNW * 16, 1, part_o, part_lse, static_cast<__nv_bfloat16*>(out));
     return (int)cudaGetLastError();
   }
   const int smem = 2 * 2 * kTileBytes;

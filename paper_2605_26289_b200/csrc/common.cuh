@@ -147,3 +147,31 @@ DS_DEVICE void named_bar_sync(int id, int threads) {
 }
 
 }  // namespace ds
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch: every forward kernel is launched with
+// programmatic stream serialization; it waits for its predecessor's memory
+// (griddepcontrol.wait) only where it first consumes it, and lets the next
+// kernel launch early (launch_dependents) so its prologue - e.g. the skinny
+// GEMM's first weight loads, which do not depend on activations - overlaps.
+// ---------------------------------------------------------------------------
+namespace ds {
+DS_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+DS_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+}  // namespace ds

@@ -48,12 +48,23 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemm_skinny_kernel(
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
 
+  uint4 a[U][2], b[U][MT];
+  // weights do not depend on the previous kernel: stream the first chunk
+  // before waiting on the activations (programmatic dependent launch)
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    a[u][0] = ldg_stream(w0 + 32 * u);
+    a[u][1] = ldg_stream(w1 + 32 * u);
+  }
+  pdl_wait();
+  pdl_trigger();
   for (int kc = 0; kc < kslice; kc += 32 * U) {
-    uint4 a[U][2], b[U][MT];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      a[u][0] = ldg_stream(w0 + kc + 32 * u);
-      a[u][1] = ldg_stream(w1 + kc + 32 * u);
+      if (kc) {
+        a[u][0] = ldg_stream(w0 + kc + 32 * u);
+        a[u][1] = ldg_stream(w1 + kc + 32 * u);
+      }
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
         b[u][mt] = xv[mt] ? __ldg(reinterpret_cast<const uint4*>(xr[mt] + kc + 32 * u))
@@ -99,9 +110,9 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemm_skinny_kernel(
 template <int MT, int U>
 static void launch(const void* X, const void* W, void* Y, int M, int N, int K, int y_f32, int acc,
                    cudaStream_t s) {
-  gemm_skinny_kernel<MT, U><<<N / 16, kGemvWarps * 32, 0, s>>>(
-      static_cast<const __nv_bfloat16*>(X), static_cast<const __nv_bfloat16*>(W), Y, M, N, K,
-      y_f32, acc);
+  launch_pdl(gemm_skinny_kernel<MT, U>, dim3(N / 16), dim3(kGemvWarps * 32), 0, s,
+             static_cast<const __nv_bfloat16*>(X), static_cast<const __nv_bfloat16*>(W), Y, M, N,
+             K, y_f32, acc);
 }
 
 }  // namespace ds

@@ -9,6 +9,8 @@ namespace ds {
 // out[r] = table[tok[r]] as bf16 (out_f32=0) or widened to fp32 (residual stream)
 __global__ void embed_kernel(const int32_t* __restrict__ tok, const uint4* __restrict__ table,
                              int chunks, void* __restrict__ out, int out_f32) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   const uint4* src = table + static_cast<int64_t>(tok[r]) * chunks;
   for (int j = threadIdx.x; j < chunks; j += blockDim.x) {
@@ -53,6 +55,8 @@ __global__ void __launch_bounds__(BLOCK) rmsnorm_kernel(const void* __restrict__
                                                         const uint4* __restrict__ w, float eps,
                                                         uint4* __restrict__ out) {
   __shared__ float s_part[BLOCK / 32];
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   const int64_t src = rows ? rows[r] : r;
   float v[MAXC][8];
@@ -97,6 +101,8 @@ __global__ void __launch_bounds__(BLOCK) rmsnorm_kernel(const void* __restrict__
 
 // out[r][j] = silu(gu[r][j]) * gu[r][F + j]
 __global__ void silu_mul_kernel(const uint4* __restrict__ gu, int chunks, uint4* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.y;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= chunks) return;
@@ -126,6 +132,8 @@ __global__ void rope_kv_store_kernel(__nv_bfloat16* __restrict__ qkv, const int3
                                      const float* __restrict__ rope_sin,
                                      __nv_bfloat16* __restrict__ k_pool,
                                      __nv_bfloat16* __restrict__ v_pool, int64_t head_stride) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   const int pos = row_pos[r];
   const int64_t cell = pos2cell[static_cast<int64_t>(row_seq[r]) * pos_stride + pos];
@@ -169,8 +177,8 @@ int ds_embed(const int32_t* tokens, int n_rows, const void* table, int hidden, v
              int out_f32, ds_stream_t stream) {
   if (n_rows < 0 || hidden % 8) return DS_EINVAL;
   if (n_rows == 0) return DS_OK;
-  ds::embed_kernel<<<n_rows, 128, 0, (cudaStream_t)stream>>>(
-      tokens, static_cast<const uint4*>(table), hidden / 8, out, out_f32);
+  ds::launch_pdl(ds::embed_kernel, dim3(n_rows), dim3(128), 0, (cudaStream_t)stream, tokens,
+                 static_cast<const uint4*>(table), hidden / 8, out, out_f32);
   return (int)cudaGetLastError();
 }
 
@@ -178,8 +186,9 @@ int ds_rmsnorm(const void* x, int x_f32, const int32_t* rows, int n_rows, int hi
                const void* w, float eps, void* out, ds_stream_t stream) {
   if (n_rows < 0 || hidden % 8 || hidden > 8 * 256 * 4) return DS_EINVAL;
   if (n_rows == 0) return DS_OK;
-  ds::rmsnorm_kernel<256, 4><<<n_rows, 256, 0, (cudaStream_t)stream>>>(
-      x, rows, hidden / 8, x_f32, static_cast<const uint4*>(w), eps, static_cast<uint4*>(out));
+  ds::launch_pdl(ds::rmsnorm_kernel<256, 4>, dim3(n_rows), dim3(256), 0, (cudaStream_t)stream, x,
+                 rows, hidden / 8, x_f32, static_cast<const uint4*>(w), eps,
+                 static_cast<uint4*>(out));
   return (int)cudaGetLastError();
 }
 
@@ -188,8 +197,8 @@ int ds_silu_mul(const void* gate_up, int n_rows, int ffn, void* out, ds_stream_t
   if (n_rows == 0) return DS_OK;
   const int chunks = ffn / 8;
   dim3 grid((chunks + 127) / 128, n_rows);
-  ds::silu_mul_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(static_cast<const uint4*>(gate_up),
-                                                              chunks, static_cast<uint4*>(out));
+  ds::launch_pdl(ds::silu_mul_kernel, grid, dim3(128), 0, (cudaStream_t)stream,
+                 static_cast<const uint4*>(gate_up), chunks, static_cast<uint4*>(out));
   return (int)cudaGetLastError();
 }
 
@@ -199,10 +208,10 @@ int ds_rope_kv_store(void* qkv, int n_rows, const int32_t* row_seq, const int32_
                      void* v_pool_l, int64_t kv_head_stride, ds_stream_t stream) {
   if (n_rows < 0 || head_dim % 16) return DS_EINVAL;
   if (n_rows == 0) return DS_OK;
-  ds::rope_kv_store_kernel<<<n_rows, 256, 0, (cudaStream_t)stream>>>(
-      static_cast<__nv_bfloat16*>(qkv), row_seq, row_pos, pos2cell, pos_stride, n_heads,
-      n_kv_heads, head_dim, rope_cos, rope_sin, static_cast<__nv_bfloat16*>(k_pool_l),
-      static_cast<__nv_bfloat16*>(v_pool_l), kv_head_stride);
+  ds::launch_pdl(ds::rope_kv_store_kernel, dim3(n_rows), dim3(256), 0, (cudaStream_t)stream,
+                 static_cast<__nv_bfloat16*>(qkv), row_seq, row_pos, pos2cell, pos_stride, n_heads,
+                 n_kv_heads, head_dim, rope_cos, rope_sin, static_cast<__nv_bfloat16*>(k_pool_l),
+                 static_cast<__nv_bfloat16*>(v_pool_l), kv_head_stride);
   return (int)cudaGetLastError();
 }
 

@@ -249,6 +249,8 @@ __global__ void __launch_bounds__(BLOCK) token_policy_kernel(
     const uint64_t* row_hash, const float* logits, int model_vocab, int policy, int mm,
     int policy_vocab, int32_t* out_tok, int32_t* out_src) {
   __shared__ int s_best;
+  pdl_wait();
+  pdl_trigger();
   const int o = blockIdx.x;
   int ei = 0;
   while (ei + 1 < n_entries && entries[ei + 1].out_start <= o) ++ei;
@@ -278,6 +280,8 @@ __global__ void __launch_bounds__(BLOCK) token_policy_kernel(
 
 __global__ void verify_accept_kernel(const ds_entry* entries, int n_entries, const int32_t* hist,
                                      int64_t stride, const int32_t* out_tok, int32_t* out_accept) {
+  pdl_wait();
+  pdl_trigger();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n_entries) return;
   const ds_entry en = entries[e];
@@ -295,11 +299,13 @@ void launch_token_policy(const ds_forward_args* a, const ds_kv_store* kv, uint64
                          cudaStream_t stream) {
   (void)hash_stream;
   constexpr int B = 256;
-  token_policy_kernel<B><<<a->n_out, B, 0, stream>>>(
-      a->entries, a->n_entries, kv->hist, kv->pos_stride, row_hash, a->logits, model_vocab,
-      a->policy, a->copy_min_match, a->policy_vocab, a->out_tok, a->out_src);
-  verify_accept_kernel<<<(a->n_entries + 63) / 64, 64, 0, stream>>>(
-      a->entries, a->n_entries, kv->hist, kv->pos_stride, a->out_tok, a->out_accept);
+  launch_pdl(token_policy_kernel<B>, dim3(a->n_out), dim3(B), 0, stream, a->entries,
+             a->n_entries, kv->hist, kv->pos_stride, (const uint64_t*)row_hash,
+             (const float*)a->logits, model_vocab, a->policy, a->copy_min_match, a->policy_vocab,
+             a->out_tok, a->out_src);
+  launch_pdl(verify_accept_kernel, dim3((a->n_entries + 63) / 64), dim3(64), 0, stream,
+             a->entries, a->n_entries, (const int32_t*)kv->hist, kv->pos_stride,
+             (const int32_t*)a->out_tok, a->out_accept);
 }
 
 void launch_row_hash(const ds_forward_args* a, const ds_kv_store* kv, uint64_t* row_hash,
