@@ -64,8 +64,11 @@ inline size_t attn_partial_bytes(const ds_entry* entries, int n, int nh, int nkv
 
 // upper bound of attn_partial_bytes for any batch (sum over
 // split entries of n_splits*qblocks*nkv <= 4*kNumSMs)
+size_t prefill_partial_bytes_bound();
 inline size_t attn_partial_bytes_bound() {
-  return static_cast<size_t>(4 * kNumSMs) * kSplitRows * (128 + 1) * sizeof(float);
+  const size_t dec = static_cast<size_t>(4 * kNumSMs) * kSplitRows * (128 + 1) * sizeof(float);
+  const size_t pre = prefill_partial_bytes_bound();
+  return dec > pre ? dec : pre;
 }
 
 }  // namespace ds

@@ -1,26 +1,29 @@
 // K6: delta-prefill attention on the 5th-generation tensor cores (tcgen05).
 //
 // Delta new query tokens attend causally over an m-token prefix that lives in
-// the paged (head-major) cell pool.  One CTA per (128 packed query rows, KV
-// head): GQA packing puts the G query heads of 128/G consecutive positions in
-// the M=128 rows, so every K/V tile is loaded once for all G heads.
-// Warp roles (6 warps, one CTA per SM, all 512 TMEM columns):
-//   warp 0  TMA producer: per 128-key tile, four 2D TMA boxes (K, V x two
+// the paged (head-major) cell pool.  Work unit = (128 packed query rows, KV
+// head, key split): GQA packing puts the G query heads of 128/G consecutive
+// positions in the M=128 rows, so every K/V tile is loaded once for all G
+// heads.  Two CTAs share an SM (256 TMEM columns and ~112 KB smem each), so
+// one CTA's softmax overlaps the other's tensor-core work.  Warp roles:
+//   warp 0  TMA producer: per 64-key tile, four 2D TMA boxes (K, V x two
 //           128-byte column halves, SWIZZLE_128B) when the tile's cells form
 //           one run, else a cell-by-cell cp.async gather into the same layout;
-//           2-stage smem ring with full/empty mbarriers.
-//   warp 1  MMA issuer (one elected thread): S_j = Q.K_j^T (M=N=K=128, 8 x
-//           tcgen05.mma kind::f16, A/B K-major SW128 descriptors) into a
-//           double-buffered TMEM S, then O += P_j.V_j (B = V MN-major) into a
-//           TMEM-resident O accumulator; completion via tcgen05.commit ->
-//           mbarrier.  S_{j+1} is issued before PV_j so the tensor core
-//           overlaps the softmax of tile j.
-//   warps 2-5 softmax (thread = TMEM lane = query row): one batched
-//           tcgen05.ld of the S row, online softmax in the log2 domain with
-//           causal masking only on diagonal tiles, P (bf16) to smem in the UMMA
-//           A layout.  The running max is only raised when it grows by more
-//           than 2^8 (P <= 256 stays exact in bf16/fp32), so the O rescale in
-//           TMEM (ld/scale/st) is rare; final O/l epilogue from TMEM.
+//           2-stage ring with full/empty mbarriers.
+//   warp 1  MMA issuer (one elected thread): S_j = Q.K_j^T (M=128, N=64, K=128;
+//           8 x tcgen05.mma kind::f16, K-major SW128 descriptors) into a
+//           double-buffered TMEM S; O += P_j.V_j with P read straight from
+//           TMEM (the "TS" form; B = V MN-major) into a TMEM-resident O;
+//           completion through tcgen05.commit.  S_{j+1} is issued before PV_j.
+//   warps 2-5 softmax (thread = TMEM lane = query row): batched tcgen05.ld of
+//           the S row, online softmax in the log2 domain (scale folded into one
+//           FFMA per element), causal masking only on diagonal tiles, P (bf16)
+//           written back over its own S columns with one tcgen05.st - no smem
+//           round trip and no wait on the previous PV.  The running max is
+//           raised only when it grows by more than 2^8, so the O rescale in
+//           TMEM is rare.
+// Long contexts are split over keys so the grid fills whole waves of
+// 2 x 148 CTAs; attn_prefill_combine merges the (O, lse) partials.
 #include "../../include/deltaserve_b200.h"
 #include "common.cuh"
 #include "tc.cuh"
@@ -30,53 +33,69 @@ namespace ds {
 
 namespace {
 constexpr int kD = 128;
-constexpr int kBM = 128;                  // packed query rows per CTA
-constexpr int kBN = 128;                  // keys per tile
-constexpr int kHalf = kBM * 128;          // one 64-column half of a 128-row tile (16 KB)
-constexpr int kTile = 2 * kHalf;          // 32 KB
+constexpr int kBM = 128;                    // packed query rows per CTA
+constexpr int kBN = 64;                     // keys per tile
+constexpr int kQHalf = kBM * 128;           // Q: 64-column half of [128 rows][128 d] (16 KB)
+constexpr int kKHalf = kBN * 128;           // K/V: 64-column half of [64 keys][128 d] (8 KB)
 constexpr int kStages = 2;
 constexpr int kThreads = 6 * 32;
-constexpr int kSmemQ = 0;
-constexpr int kSmemP = kTile;
-constexpr int kSmemKV = 2 * kTile;                        // stages x (K | V)
-constexpr int kSmemBar = kSmemKV + kStages * 2 * kTile;   // barriers after the ring
-constexpr int kSmemBytes = kSmemBar + 256 + 1024;         // + alignment slack
+constexpr int kSmemQ = 0;                             // 32 KB
+constexpr int kSmemKV = 2 * kQHalf;                   // stages x (K 16 KB | V 16 KB)
+constexpr int kSmemBar = kSmemKV + kStages * 4 * kKHalf;
+constexpr int kSmemBytes = kSmemBar + 128;
+constexpr int kTmemCols = 256;  // S0/P0 [0,64) S1/P1 [64,128) O [128,256)
+constexpr int kMaxSplits = 8;
+constexpr int kMaxPartialCtas = 8 * 148;  // bounds the split-partial workspace
 
-DS_DEVICE int sw128(int row, int chunk16) {
-  return (chunk16 >> 3) * kHalf + row * 128 + (((chunk16 & 7) ^ (row & 7)) << 4);
+// 16-byte chunk c (0..15 over d) of row r in a tile of `rows` rows, SW128
+DS_DEVICE int sw128(int rows, int row, int chunk16) {
+  return (chunk16 >> 3) * rows * 128 + row * 128 + (((chunk16 & 7) ^ (row & 7)) << 4);
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads, 1) attn_prefill_kernel(
+// partial output slot of (entry e, split s, q-block qb, kv head kh): 128 rows
+DS_DEVICE int64_t prefill_slot(int e, int s, int qb, int kh, int splits, int max_qb, int nkv) {
+  return ((static_cast<int64_t>(e) * splits + s) * max_qb + qb) * nkv + kh;
+}
+
+__global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
     const __nv_bfloat16* __restrict__ qkv, int qkv_stride, const ds_entry* __restrict__ entries,
     const __nv_bfloat16* __restrict__ kpool, const __nv_bfloat16* __restrict__ vpool,
     int64_t head_stride, const int32_t* __restrict__ pos2cell, int64_t pos_stride, int nh,
-    int nkv, float scale_log2, __nv_bfloat16* __restrict__ out,
+    int nkv, float scale_log2, __nv_bfloat16* __restrict__ out, int splits, int max_qb,
+    float* __restrict__ part_o, float* __restrict__ part_lse,
     const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
-  uint64_t* kv_full = bars;        // [2]
-  uint64_t* kv_empty = bars + 2;   // [2]
-  uint64_t* s_full = bars + 4;     // [2]
-  uint64_t* s_empty = bars + 6;    // [2]
-  uint64_t* pv_done = bars + 8;    // [1] PV_j complete (P smem free, O stable)
-  uint64_t* p_full = bars + 12;    // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* kv_full = bars;       // [2]
+  uint64_t* kv_empty = bars + 2;  // [2]
+  uint64_t* s_full = bars + 4;    // [2]
+  uint64_t* s_empty = bars + 6;   // [2]
+  uint64_t* pv_done = bars + 8;   // PV_j complete: P smem free, O stable
+  uint64_t* p_full = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  if (smem_u32(smem) & 1023) __trap();  // SW128 tiles need 1 KB alignment
   pdl_wait();
   pdl_trigger();
 
-  const ds_entry en = entries[blockIdx.z];
+  const int e = blockIdx.z / splits;
+  const int split = blockIdx.z - e * splits;
+  const ds_entry en = entries[e];
   const int G = nh / nkv;
-  const int pos_per_block = kBM / G;
-  const int t0 = blockIdx.x * pos_per_block;
+  const int ppb = kBM / G;  // positions per block
+  const int qb = blockIdx.x;
+  const int t0 = qb * ppb;
   if (t0 >= en.q_len) return;
   const int kh = blockIdx.y;
-  const int t_last = min(en.q_len, t0 + pos_per_block) - 1;
+  const int t_last = min(en.q_len, t0 + ppb) - 1;
   const int kv_len = en.past + en.q_len;
   const int kv_hi = en.past + t_last + 1;  // keys any row of this block can see
-  const int ntiles = (kv_hi + kBN - 1) / kBN;
+  const int ntiles_all = (kv_hi + kBN - 1) / kBN;
+  const int per = (ntiles_all + splits - 1) / splits;
+  const int j0 = split * per;
+  const int j1 = min(ntiles_all, j0 + per);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ntiles = j0 >= j1 ? 0 : j1 - j0;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -89,7 +108,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_prefill_kernel(
     mbar_init(p_full, 4);
     mbar_fence_init();
   }
-  if (warp == 1) tc::alloc(tmem_slot, 512);
+  if (warp == 1) tc::alloc(tmem_slot, kTmemCols);
   if (warp >= 2) {  // Q rows (packed r = t*G + g) -> smem, UMMA A layout
     const int r = tid - 64;
     const int t = t0 + r / G, g = r - (r / G) * G;
@@ -99,7 +118,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_prefill_kernel(
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
       const uint4 v = ok ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
-      *reinterpret_cast<uint4*>(smem + kSmemQ + sw128(r, c)) = v;
+      *reinterpret_cast<uint4*>(smem + kSmemQ + sw128(kBM, r, c)) = v;
     }
     tc::fence_proxy_async();
   }
@@ -116,38 +135,37 @@ __global__ void __launch_bounds__(kThreads, 1) attn_prefill_kernel(
       tma_prefetch_desc(&tmv);
     }
     const int64_t hrow = kh * head_stride;
-    for (int j = 0; j < ntiles; ++j) {
-      const int st = j % kStages;
-      if (j >= kStages) mbar_wait(&kv_empty[st], ((j / kStages) - 1) & 1);
-      uint8_t* ks = smem + kSmemKV + st * 2 * kTile;
-      uint8_t* vs = ks + kTile;
-      const int kt = j * kBN;
+    for (int jj = 0; jj < ntiles; ++jj) {
+      const int st = jj % kStages;
+      if (jj >= kStages) mbar_wait(&kv_empty[st], ((jj / kStages) - 1) & 1);
+      uint8_t* ks = smem + kSmemKV + st * 4 * kKHalf;
+      uint8_t* vs = ks + 2 * kKHalf;
+      const int kt = (j0 + jj) * kBN;
       const int nvalid = min(kBN, kv_hi - kt);
-      int c[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) c[i] = lane + 32 * i < nvalid ? __ldg(p2c + kt + lane + 32 * i) : -1;
-      const int c0 = __shfl_sync(0xffffffffu, c[0], 0);
-      bool ok = true;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) ok &= (c[i] < 0) || (c[i] == c0 + lane + 32 * i);
-      if (__all_sync(0xffffffffu, ok)) {
+      const int c_lo = lane < nvalid ? __ldg(p2c + kt + lane) : -1;
+      const int c_hi = lane + 32 < nvalid ? __ldg(p2c + kt + 32 + lane) : -1;
+      const int c0 = __shfl_sync(0xffffffffu, c_lo, 0);
+      const bool run = __all_sync(0xffffffffu, (c_lo < 0 || c_lo == c0 + lane) &&
+                                                    (c_hi < 0 || c_hi == c0 + 32 + lane));
+      if (run) {
         if (lane == 0) {
-          mbar_expect_tx(&kv_full[st], 2 * kTile);
+          mbar_expect_tx(&kv_full[st], 4 * kKHalf);
           const int row = static_cast<int>(hrow + c0);
           tma_load_2d(ks, &tmk, 0, row, &kv_full[st]);
-          tma_load_2d(ks + kHalf, &tmk, 64, row, &kv_full[st]);
+          tma_load_2d(ks + kKHalf, &tmk, 64, row, &kv_full[st]);
           tma_load_2d(vs, &tmv, 0, row, &kv_full[st]);
-          tma_load_2d(vs + kHalf, &tmv, 64, row, &kv_full[st]);
+          tma_load_2d(vs + kKHalf, &tmv, 64, row, &kv_full[st]);
         }
       } else {
 #pragma unroll 1
-        for (int i = 0; i < 4; ++i) {
-          const int r = lane + 32 * i;
-          const int64_t off = (hrow + (c[i] >= 0 ? c[i] : c0)) * kD;
+        for (int h = 0; h < 2; ++h) {
+          const int r = lane + 32 * h;
+          const int cv = h ? c_hi : c_lo;
+          const int64_t off = (hrow + (cv >= 0 ? cv : c0)) * kD;
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            cp_async16(ks + sw128(r, q), kpool + off + q * 8);
-            cp_async16(vs + sw128(r, q), vpool + off + q * 8);
+            cp_async16(ks + sw128(kBN, r, q), kpool + off + q * 8);
+            cp_async16(vs + sw128(kBN, r, q), vpool + off + q * 8);
           }
         }
         cp_async_commit();
@@ -159,82 +177,90 @@ __global__ void __launch_bounds__(kThreads, 1) attn_prefill_kernel(
     }
   } else if (warp == 1) {
     // ======================= MMA issuer =======================
-    if (lane == 0) {
+    if (lane == 0 && ntiles > 0) {
       constexpr uint32_t idesc_s = tc::idesc_bf16(kBM, kBN, false);
       constexpr uint32_t idesc_pv = tc::idesc_bf16(kBM, kD, true);
       const uint32_t q_base = smem_u32(smem + kSmemQ);
-      const uint32_t p_base = smem_u32(smem + kSmemP);
       const uint32_t kv_base = smem_u32(smem + kSmemKV);
-      auto issue_s = [&](int j) {
-        const int st = j % kStages, sb = j & 1;
-        mbar_wait(&kv_full[st], (j / kStages) & 1);
-        if (j >= 2) mbar_wait(&s_empty[sb], ((j >> 1) - 1) & 1);
+      auto issue_s = [&](int jj) {
+        const int st = jj % kStages, sb = jj & 1;
+        mbar_wait(&kv_full[st], (jj / kStages) & 1);
+        // S/P buffer sb was last read by PV_{jj-2}, issued (in order) before us
         tc::fence_after();
-        const uint32_t kb = kv_base + st * 2 * kTile;
+        const uint32_t kb = kv_base + st * 4 * kKHalf;
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-          tc::mma(tmem + sb * kBN, tc::smem_desc(q_base + off, 16, 1024),
-                  tc::smem_desc(kb + off, 16, 1024), idesc_s, kk > 0);
+          tc::mma(tmem + sb * kBN,
+                  tc::smem_desc(q_base + (kk >> 2) * kQHalf + (kk & 3) * 32, 16, 1024),
+                  tc::smem_desc(kb + (kk >> 2) * kKHalf + (kk & 3) * 32, 16, 1024), idesc_s,
+                  kk > 0);
         }
         tc::commit(&s_full[sb]);
       };
       issue_s(0);
-      for (int j = 0; j < ntiles; ++j) {
-        if (j + 1 < ntiles) issue_s(j + 1);
-        const int st = j % kStages;
-        mbar_wait(p_full, j & 1);
+      for (int jj = 0; jj < ntiles; ++jj) {
+        if (jj + 1 < ntiles) issue_s(jj + 1);
+        const int st = jj % kStages;
+        mbar_wait(p_full, jj & 1);
         tc::fence_after();
-        const uint32_t vb = kv_base + st * 2 * kTile + kTile;
+        const uint32_t vb = kv_base + st * 4 * kKHalf + 2 * kKHalf;
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk) {
-          tc::mma(tmem + 256, tc::smem_desc(p_base + (kk >> 2) * kHalf + (kk & 3) * 32, 16, 1024),
-                  tc::smem_desc(vb + kk * 2048, kHalf, 1024), idesc_pv, (j | kk) > 0);
+          tc::mma_ts(tmem + 2 * kBN, tmem + (jj & 1) * kBN + kk * 8,
+                     tc::smem_desc(vb + kk * 2048, kKHalf, 1024), idesc_pv, (jj | kk) > 0);
         }
         tc::commit(pv_done);
         tc::commit(&kv_empty[st]);
       }
     }
   } else {
-    // ================ softmax / correction / epilogue ================
+    // ================ softmax / epilogue ================
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int r = quad * 32 + lane;
     const int t = t0 + r / G, g = r - (r / G) * G;
-    const int pos = en.past + t;  // this row's absolute position (causal bound)
+    const int pos = en.past + t;  // absolute position of this row (causal bound)
     const uint32_t trow = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-    const uint32_t tO = trow + 256;
+    const uint32_t tO = trow + 2 * kBN;
     const int blk_pos_min = en.past + t0;
     float m_ref = -INFINITY, l_run = 0.f;
-    uint8_t* prow = smem + kSmemP;
-    uint32_t sv[kBN];
-    for (int j = 0; j < ntiles; ++j) {
-      const int sb = j & 1;
-      const int kt = j * kBN;
-      mbar_wait(&s_full[sb], (j >> 1) & 1);
+    uint32_t sv[kD];
+    for (int jj = 0; jj < ntiles; ++jj) {
+      const int sb = jj & 1;
+      const int kt = (j0 + jj) * kBN;
+      mbar_wait(&s_full[sb], (jj >> 1) & 1);
       tc::fence_after();
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) tc::ld32_issue(trow + sb * kBN + cc * 32, sv + cc * 32);
+      tc::ld32_issue(trow + sb * kBN, sv);
+      tc::ld32_issue(trow + sb * kBN + 32, sv + 32);
       tc::wait_ld();
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[sb]);  // S buffer is in registers now
       const bool need_mask = (kt + kBN - 1 > blk_pos_min) || (kt + kBN > kv_len);
-      float mx = -INFINITY;
+      if (need_mask) {
 #pragma unroll
-      for (int i = 0; i < kBN; ++i) {
-        float x = __uint_as_float(sv[i]) * scale_log2;
-        if (need_mask) x = (kt + i <= pos && kt + i < kv_len) ? x : -INFINITY;
-        sv[i] = __float_as_uint(x);
-        mx = fmaxf(mx, x);
+        for (int i = 0; i < kBN; ++i)
+          if (!(kt + i <= pos && kt + i < kv_len)) sv[i] = __float_as_uint(-INFINITY);
       }
-      // PV_{j-1} done: P smem is free and O in TMEM is stable
-      if (j > 0) {
-        mbar_wait(pv_done, (j - 1) & 1);
-        tc::fence_after();
-      }
+      float mraw = -INFINITY;  // max of raw scores (scale > 0 commutes with max)
+#pragma unroll
+      for (int i = 0; i < kBN; ++i) mraw = fmaxf(mraw, __uint_as_float(sv[i]));
+      const float mx = mraw * scale_log2;
       const float new_ref = (mx > m_ref + 8.f) ? mx : m_ref;
       const float scale_old = (m_ref == -INFINITY) ? 0.f : fast_exp2(m_ref - new_ref);
-      if (j > 0 && __any_sync(0xffffffffu, new_ref != m_ref)) {  // rare O correction
+      const float mref = new_ref == -INFINITY ? 0.f : new_ref;
+      float sum = 0.f;
+      uint32_t pk[kBN / 2];
+#pragma unroll
+      for (int i = 0; i < kBN; i += 2) {
+        const float p0 = fast_exp2(fmaf(__uint_as_float(sv[i]), scale_log2, -mref));
+        const float p1 = fast_exp2(fmaf(__uint_as_float(sv[i + 1]), scale_log2, -mref));
+        sum += p0 + p1;
+        pk[i / 2] = pack_bf16(p0, p1);
+      }
+      tc::st32(trow + sb * kBN, pk);  // P_j over its own S columns
+      // PV_{j-1} done (O stable) before an O correction and before PV_j is issued
+      if (jj > 0) {
+        mbar_wait(pv_done, (jj - 1) & 1);
+        tc::fence_after();
+      }
+      if (jj > 0 && __any_sync(0xffffffffu, new_ref != m_ref)) {  // rare O correction
         uint32_t ov[32];
 #pragma unroll 1
         for (int cc = 0; cc < 4; ++cc) {
@@ -244,60 +270,116 @@ __global__ void __launch_bounds__(kThreads, 1) attn_prefill_kernel(
           for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * scale_old);
           tc::st32(tO + cc * 32, ov);
         }
-        tc::wait_st();
       }
-      l_run *= scale_old;
+      tc::wait_st();
+      l_run = l_run * scale_old + sum;
       m_ref = new_ref;
-      const float mref = m_ref == -INFINITY ? 0.f : m_ref;
-      float sum = 0.f;
-#pragma unroll
-      for (int cc = 0; cc < 16; ++cc) {
-        uint32_t pk[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float p0 = fast_exp2(__uint_as_float(sv[cc * 8 + 2 * q]) - mref);
-          const float p1 = fast_exp2(__uint_as_float(sv[cc * 8 + 2 * q + 1]) - mref);
-          sum += p0 + p1;
-          pk[q] = pack_bf16(p0, p1);
-        }
-        *reinterpret_cast<uint4*>(prow + sw128(r, cc)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-      }
-      l_run += sum;
-      tc::fence_proxy_async();
       tc::fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
     }
-    mbar_wait(pv_done, (ntiles - 1) & 1);
-    tc::fence_after();
+    if (ntiles > 0) {
+      mbar_wait(pv_done, (ntiles - 1) & 1);
+      tc::fence_after();
 #pragma unroll
-    for (int cc = 0; cc < 4; ++cc) tc::ld32_issue(tO + cc * 32, sv + cc * 32);
-    tc::wait_ld();
-    if (t < en.q_len) {
-      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-      uint4* dst = reinterpret_cast<uint4*>(out + static_cast<int64_t>(en.q_start + t) * nh * kD +
-                                            (kh * G + g) * kD);
+      for (int cc = 0; cc < 4; ++cc) tc::ld32_issue(tO + cc * 32, sv + cc * 32);
+      tc::wait_ld();
+    }
+    const float* o = reinterpret_cast<const float*>(sv);
+    if (splits == 1) {
+      if (t < en.q_len) {
+        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+        uint4* dst = reinterpret_cast<uint4*>(
+            out + static_cast<int64_t>(en.q_start + t) * nh * kD + (kh * G + g) * kD);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const float* o = reinterpret_cast<const float*>(sv) + 8 * q;
-        dst[q] = make_uint4(pack_bf16(o[0] * inv, o[1] * inv), pack_bf16(o[2] * inv, o[3] * inv),
-                            pack_bf16(o[4] * inv, o[5] * inv), pack_bf16(o[6] * inv, o[7] * inv));
+        for (int q = 0; q < 16; ++q)
+          dst[q] = make_uint4(pack_bf16(o[8 * q] * inv, o[8 * q + 1] * inv),
+                              pack_bf16(o[8 * q + 2] * inv, o[8 * q + 3] * inv),
+                              pack_bf16(o[8 * q + 4] * inv, o[8 * q + 5] * inv),
+                              pack_bf16(o[8 * q + 6] * inv, o[8 * q + 7] * inv));
       }
+    } else {
+      const int64_t slot = prefill_slot(e, split, qb, kh, splits, max_qb, nkv) * kBM + r;
+      const bool any = ntiles > 0 && l_run > 0.f;
+      const float inv = any ? 1.f / l_run : 0.f;
+      float4* dst = reinterpret_cast<float4*>(part_o + slot * kD);
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        dst[q] = make_float4(any ? o[4 * q] * inv : 0.f, any ? o[4 * q + 1] * inv : 0.f,
+                             any ? o[4 * q + 2] * inv : 0.f, any ? o[4 * q + 3] * inv : 0.f);
+      part_lse[slot] = any ? m_ref + __log2f(l_run) : -INFINITY;
     }
   }
   tc::fence_before();
   __syncthreads();
   if (warp == 1) {
     tc::fence_after();
-    tc::dealloc(tmem, 512);
+    tc::dealloc(tmem, kTmemCols);
   }
+}
+
+// merge key-split partials: out = sum_s 2^(lse_s - max) O_s / sum_s 2^(lse_s - max)
+__global__ void attn_prefill_combine(const ds_entry* __restrict__ entries, int splits, int max_qb,
+                                     int nh, int nkv, const float* __restrict__ part_o,
+                                     const float* __restrict__ part_lse,
+                                     __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int e = blockIdx.z, kh = blockIdx.y, qb = blockIdx.x;
+  const ds_entry en = entries[e];
+  const int G = nh / nkv;
+  const int t0 = qb * (kBM / G);
+  if (t0 >= en.q_len) return;
+  for (int idx = threadIdx.x; idx < kBM * 16; idx += blockDim.x) {
+    const int r = idx >> 4, c8 = idx & 15;
+    const int t = t0 + r / G, g = r - (r / G) * G;
+    if (t >= en.q_len) continue;
+    float mx = -INFINITY;
+    for (int s = 0; s < splits; ++s)
+      mx = fmaxf(mx, part_lse[prefill_slot(e, s, qb, kh, splits, max_qb, nkv) * kBM + r]);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, wsum = 0.f;
+    for (int s = 0; s < splits; ++s) {
+      const int64_t slot = prefill_slot(e, s, qb, kh, splits, max_qb, nkv) * kBM + r;
+      const float lse = part_lse[slot];
+      if (lse == -INFINITY) continue;
+      const float w = exp2f(lse - mx);
+      wsum += w;
+      const float4* p = reinterpret_cast<const float4*>(part_o + slot * kD + c8 * 8);
+      const float4 a = p[0], b = p[1];
+      acc[0] += w * a.x; acc[1] += w * a.y; acc[2] += w * a.z; acc[3] += w * a.w;
+      acc[4] += w * b.x; acc[5] += w * b.y; acc[6] += w * b.z; acc[7] += w * b.w;
+    }
+    const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+    *reinterpret_cast<uint4*>(out + static_cast<int64_t>(en.q_start + t) * nh * kD +
+                              (kh * G + g) * kD + c8 * 8) =
+        make_uint4(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv),
+                   pack_bf16(acc[4] * inv, acc[5] * inv), pack_bf16(acc[6] * inv, acc[7] * inv));
+  }
+}
+
+// key splits that best fill whole waves of 2 CTAs per SM (>= 8 tiles each)
+static int prefill_splits(int ctas, int max_tiles) {
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= kMaxSplits; ++s) {
+    if (s > 1 && (max_tiles / s < 8 || ctas * s > kMaxPartialCtas)) break;
+    const long total = static_cast<long>(ctas) * s;
+    const long slots = 2L * 148;
+    const long waves = (total + slots - 1) / slots;
+    const double eff = static_cast<double>(total) / static_cast<double>(waves * slots);
+    if (eff > best_eff + 1e-3) {
+      best_eff = eff;
+      best = s;
+    }
+  }
+  return best;
 }
 
 int launch_attn_prefill_sm100(const void* qkv, const ds_entry* entries_host,
                               const ds_entry* entries_dev, int n_entries, const void* k_pool,
                               const void* v_pool, int64_t head_stride, const int32_t* pos2cell,
                               int64_t pos_stride, int nh, int nkv, int hd, float scale, void* out,
-                              cudaStream_t stream) {
+                              void* workspace, size_t ws_bytes, cudaStream_t stream) {
   if (hd != kD || nh % nkv || kBM % (nh / nkv)) return DS_EUNSUPPORTED;
   const CUtensorMap* tk = kv_tensor_map(k_pool, static_cast<int64_t>(nkv) * head_stride, kBN);
   const CUtensorMap* tv = kv_tensor_map(v_pool, static_cast<int64_t>(nkv) * head_stride, kBN);
@@ -309,18 +391,41 @@ int launch_attn_prefill_sm100(const void* qkv, const ds_entry* entries_host,
     attr = true;
   }
   const int ppb = kBM / (nh / nkv);
-  int max_qb = 0;
+  int max_qb = 0, qb_total = 0, max_tiles = 0;
   for (int e = 0; e < n_entries; ++e) {
-    const int qb = (entries_host[e].q_len + ppb - 1) / ppb;
+    const ds_entry& en = entries_host[e];
+    const int qb = (en.q_len + ppb - 1) / ppb;
     max_qb = qb > max_qb ? qb : max_qb;
+    qb_total += qb;
+    const int tiles = (en.past + en.q_len + kBN - 1) / kBN;
+    max_tiles = tiles > max_tiles ? tiles : max_tiles;
   }
-  dim3 grid(max_qb, nkv, n_entries);
-  launch_pdl(attn_prefill_kernel, grid, dim3(kThreads), kSmemBytes, stream,
-             static_cast<const __nv_bfloat16*>(qkv), (nh + 2 * nkv) * kD, entries_dev,
-             static_cast<const __nv_bfloat16*>(k_pool), static_cast<const __nv_bfloat16*>(v_pool),
-             head_stride, pos2cell, pos_stride, nh, nkv, scale * 1.4426950408889634f,
-             static_cast<__nv_bfloat16*>(out), *tk, *tv);
+  int splits = prefill_splits(qb_total * nkv, max_tiles);
+  const size_t need = static_cast<size_t>(n_entries) * splits * max_qb * nkv * kBM *
+                      (kD + 1) * sizeof(float);
+  if (splits > 1 && need > ws_bytes) splits = 1;
+  float* part_o = static_cast<float*>(workspace);
+  float* part_lse =
+      part_o + static_cast<size_t>(n_entries) * splits * max_qb * nkv * kBM * kD;
+  dim3 grid(max_qb, nkv, n_entries * splits);
+  cudaError_t err = launch_pdl(
+      attn_prefill_kernel, grid, dim3(kThreads), kSmemBytes, stream,
+      static_cast<const __nv_bfloat16*>(qkv), (nh + 2 * nkv) * kD, entries_dev,
+      static_cast<const __nv_bfloat16*>(k_pool), static_cast<const __nv_bfloat16*>(v_pool),
+      head_stride, pos2cell, pos_stride, nh, nkv, scale * 1.4426950408889634f,
+      static_cast<__nv_bfloat16*>(out), splits, max_qb, part_o, part_lse, *tk, *tv);
+  if (err != cudaSuccess) return static_cast<int>(err);
+  if (splits > 1) {
+    err = launch_pdl(attn_prefill_combine, dim3(max_qb, nkv, n_entries), dim3(256), 0, stream,
+                     entries_dev, splits, max_qb, nh, nkv, (const float*)part_o,
+                     (const float*)part_lse, static_cast<__nv_bfloat16*>(out));
+    if (err != cudaSuccess) return static_cast<int>(err);
+  }
   return (int)cudaGetLastError();
+}
+
+size_t prefill_partial_bytes_bound() {
+  return static_cast<size_t>(kMaxPartialCtas) * kBM * (kD + 1) * sizeof(float);
 }
 
 }  // namespace ds

@@ -25,7 +25,7 @@ int launch_attn_prefill_sm100(const void* qkv, const ds_entry* entries_host,
                               const ds_entry* entries_dev, int n_entries, const void* k_pool,
                               const void* v_pool, int64_t head_stride, const int32_t* pos2cell,
                               int64_t pos_stride, int nh, int nkv, int hd, float scale, void* out,
-                              cudaStream_t stream);
+                              void* workspace, size_t ws_bytes, cudaStream_t stream);
 
 namespace {
 
@@ -188,7 +188,8 @@ int ds_attention(const void* qkv, const ds_entry* entries_host, const ds_entry* 
   if (impl == 2)
     return launch_attn_prefill_sm100(qkv, entries_host, entries_dev, n_entries, k_pool_l, v_pool_l,
                                      kv_head_stride, pos2cell, pos_stride, n_heads, n_kv_heads,
-                                     head_dim, scale, out, (cudaStream_t)stream);
+                                     head_dim, scale, out, workspace, workspace_bytes,
+                                     (cudaStream_t)stream);
   return launch_attn_split(qkv, entries_host, entries_dev, n_entries, k_pool_l, v_pool_l,
                            kv_head_stride, pos2cell, pos_stride, n_heads, n_kv_heads, head_dim,
                            scale, out, workspace, workspace_bytes, (cudaStream_t)stream);

@@ -115,3 +115,20 @@ DS_DEVICE void st32(uint32_t taddr, const uint32_t* r) {
 DS_DEVICE void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 }  // namespace tc
 }  // namespace ds
+
+namespace ds {
+namespace tc {
+// D[tmem] (+)= A[tmem] * B[smem]  ("TS" form: A is read from tensor memory,
+// 16-bit elements packed two per 32-bit column, lane = row)
+DS_DEVICE void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                      uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+}  // namespace tc
+}  // namespace ds
