@@ -89,6 +89,8 @@ typedef struct {
 #define DS_KV_UNMAP 1
 #define DS_KV_TRIE_INC 2
 #define DS_KV_TRIE_DEC 3
+#define DS_KV_MAP_SCRATCH 4 /* pos2cell only (batched verify rows live in scratch cells
+                               until the host knows the accept count) */
 
 int ds_kv_apply(const ds_kv_op* ops_dev, int n_ops, int32_t* pos2cell, int64_t pos_stride,
                 int n_seqs, uint32_t* member, int mask_words, int32_t* trie_ref,
@@ -99,6 +101,12 @@ int ds_kv_apply(const ds_kv_op* ops_dev, int n_ops, int32_t* pos2cell, int64_t p
  * (prompt upload at admission; pending tokens before the n-gram matcher). */
 int ds_hist_write(const int32_t* src, const int32_t* segs, int n_segs, int32_t* hist,
                   int64_t pos_stride, ds_stream_t stream);
+
+/* Copy all layers' K and V rows of cell src[i] to cell dst[i] (pairs int32
+ * [n][2]) in a head-major pool; used to move accepted verify rows from scratch
+ * cells into the cells the reference allocator assigns. */
+int ds_kv_copy_cells(void* k_pool, void* v_pool, int layers, int n_kv_heads, int64_t head_stride,
+                     int head_dim, const int32_t* pairs, int n, ds_stream_t stream);
 
 /* Derived refcount (popcount(member) + trie_ref) and occupancy (cells with
  * refcount > 0) - the device view of kvcache.py:91-100, 185-187. */

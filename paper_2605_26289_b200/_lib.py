@@ -22,7 +22,7 @@ class KvOp(ctypes.Structure):
     _fields_ = [("kind", c_i32), ("seq", c_i32), ("pos", c_i32), ("cell", c_i32), ("len", c_i32)]
 
 
-KV_MAP, KV_UNMAP, KV_TRIE_INC, KV_TRIE_DEC = 0, 1, 2, 3
+KV_MAP, KV_UNMAP, KV_TRIE_INC, KV_TRIE_DEC, KV_MAP_SCRATCH = 0, 1, 2, 3, 4
 
 
 class Model(ctypes.Structure):
@@ -90,6 +90,7 @@ def lib() -> ctypes.CDLL:
         "ds_host_fnv1a32_tokens": (ctypes.c_uint32, [P, c_i64, ctypes.c_uint32]),
         "ds_kv_apply": (c_i32, [P, c_i32, P, c_i64, c_i32, P, c_i32, P, P]),
         "ds_hist_write": (c_i32, [P, P, c_i32, P, c_i64, P]),
+        "ds_kv_copy_cells": (c_i32, [P, P, c_i32, c_i32, c_i64, c_i32, P, c_i32, P]),
         "ds_kv_refcount": (c_i32, [P, c_i32, P, c_i64, P, P, P]),
         "ds_forward_workspace_bytes": (ctypes.c_size_t, [P, c_i32, c_i32, c_i32]),
         "ds_model_forward": (c_i32, [P, P, P, P]),

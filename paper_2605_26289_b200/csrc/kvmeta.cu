@@ -43,6 +43,13 @@ __global__ void __launch_bounds__(1024) kv_apply_kernel(const ds_kv_op* __restri
       case DS_KV_TRIE_DEC:
         for (int j = threadIdx.x; j < op.len; j += blockDim.x) trie_ref[op.cell + j] -= 1;
         break;
+      case DS_KV_MAP_SCRATCH: {
+        if (!mirrored) break;
+        int32_t* row = pos2cell + static_cast<int64_t>(op.seq) * pos_stride + op.pos;
+        for (int j = threadIdx.x; j < op.len; j += blockDim.x)
+          if (op.pos + j < pos_stride) row[j] = op.cell + j;
+        break;
+      }
       default:
         break;
     }
@@ -76,9 +83,37 @@ __global__ void hist_write_kernel(const int32_t* __restrict__ src, const int32_t
   for (int j = threadIdx.x; j < sg[2]; j += blockDim.x) dst[j] = s[j];
 }
 
+// one CTA per (pair, layer): K and V rows of every KV head (2 * nkv * hd bf16)
+__global__ void kv_copy_cells_kernel(__nv_bfloat16* k_pool, __nv_bfloat16* v_pool, int nkv,
+                                     int64_t head_stride, int hd, const int32_t* pairs) {
+  const int i = blockIdx.x, l = blockIdx.y;
+  const int64_t src = pairs[2 * i], dst = pairs[2 * i + 1];
+  const int per_head = hd / 8;
+  const int64_t layer = static_cast<int64_t>(l) * nkv * head_stride * hd;
+  for (int j = threadIdx.x; j < 2 * nkv * per_head; j += blockDim.x) {
+    const int kv = j / (nkv * per_head);
+    const int rem = j - kv * nkv * per_head;
+    const int h = rem / per_head, c = rem - h * per_head;
+    __nv_bfloat16* pool = kv ? v_pool : k_pool;
+    uint4* d = reinterpret_cast<uint4*>(pool + layer + (h * head_stride + dst) * hd) + c;
+    const uint4* s = reinterpret_cast<const uint4*>(pool + layer + (h * head_stride + src) * hd) + c;
+    *d = *s;
+  }
+}
+
 }  // namespace ds
 
 extern "C" {
+
+int ds_kv_copy_cells(void* k_pool, void* v_pool, int layers, int n_kv_heads, int64_t head_stride,
+                     int head_dim, const int32_t* pairs, int n, ds_stream_t stream) {
+  if (n < 0 || head_dim % 8) return DS_EINVAL;
+  if (n == 0) return DS_OK;
+  ds::kv_copy_cells_kernel<<<dim3(n, layers), 256, 0, (cudaStream_t)stream>>>(
+      static_cast<__nv_bfloat16*>(k_pool), static_cast<__nv_bfloat16*>(v_pool), n_kv_heads,
+      head_stride, head_dim, pairs);
+  return (int)cudaGetLastError();
+}
 
 int ds_kv_apply(const ds_kv_op* ops_dev, int n_ops, int32_t* pos2cell, int64_t pos_stride,
                 int n_seqs, uint32_t* member, int mask_words, int32_t* trie_ref,

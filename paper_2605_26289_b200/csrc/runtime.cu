@@ -221,6 +221,11 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
   for (int e = 0; e < a->n_entries; ++e)
     max_q = a->entries_host[e].q_len > max_q ? a->entries_host[e].q_len : max_q;
   const int attn_impl = 0;  // auto
+  // entries ordered long (q*G > 32: tcgen05 K6) first, then short (K7)
+  int n_long = 0;
+  while (n_long < a->n_entries && a->entries_host[n_long].q_len * (nh / nkv) > 32) ++n_long;
+  for (int e = n_long; e < a->n_entries; ++e)
+    if (a->entries_host[e].q_len * (nh / nkv) > 32) n_long = 0;  // unsorted: auto dispatch
 
   DS_BLAS(cublasSetStream(rt.blas, stream));
   DS_BLAS(cublasSetWorkspace(rt.blas, b.blas_ws, kCublasWs));
@@ -253,9 +258,20 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
     DS_CHECK(ds_rope_kv_store(b.qkv, T, a->row_seq, a->row_pos, kv->pos2cell, kv->pos_stride, nh,
                               nkv, hd, m->rope_cos, m->rope_sin, kp + l * kv_layer,
                               vp + l * kv_layer, kv->capacity, stream));
-    DS_CHECK(ds_attention(b.qkv, a->entries_host, a->entries, a->n_entries, T, kp + l * kv_layer,
-                          vp + l * kv_layer, kv->capacity, kv->pos2cell, kv->pos_stride, nh, nkv,
-                          hd, scale, b.attn, b.attn_ws, b.attn_ws_bytes, attn_impl, stream));
+    if (n_long > 0 && n_long < a->n_entries) {  // mixed plan: K6 for prefill chunks, K7 rest
+      DS_CHECK(ds_attention(b.qkv, a->entries_host, a->entries, n_long, T, kp + l * kv_layer,
+                            vp + l * kv_layer, kv->capacity, kv->pos2cell, kv->pos_stride, nh,
+                            nkv, hd, scale, b.attn, b.attn_ws, b.attn_ws_bytes, 2, stream));
+      DS_CHECK(ds_attention(b.qkv, a->entries_host + n_long, a->entries + n_long,
+                            a->n_entries - n_long, T, kp + l * kv_layer, vp + l * kv_layer,
+                            kv->capacity, kv->pos2cell, kv->pos_stride, nh, nkv, hd, scale,
+                            b.attn, b.attn_ws, b.attn_ws_bytes, 1, stream));
+    } else {
+      DS_CHECK(ds_attention(b.qkv, a->entries_host, a->entries, a->n_entries, T,
+                            kp + l * kv_layer, vp + l * kv_layer, kv->capacity, kv->pos2cell,
+                            kv->pos_stride, nh, nkv, hd, scale, b.attn, b.attn_ws,
+                            b.attn_ws_bytes, attn_impl, stream));
+    }
     DS_CHECK(project(rt.blas, b.attn, wo + static_cast<size_t>(l) * H * nh * hd, b.x, T, H,
                      nh * hd, true, true, stream));
     DS_CHECK(ds_rmsnorm(b.x, 1, nullptr, T, H, mn + static_cast<size_t>(l) * H, m->rms_eps, b.h,

@@ -73,12 +73,14 @@ class RowResult:
 
     argmax_id: int
     copy_source: int | None
+    scratch: list | None = None
 
 
 @dataclass
 class VerifyResult:
     accepted: int
     rows: list
+    scratch: list | None = None
 
 
 @dataclass
@@ -91,6 +93,7 @@ class EntryRequest:
     batch: list        # tokens forwarded
     tokens: list       # full committed token list of the slot (for the prefix hash)
     n_draft: int = 0
+    scratch: bool = False  # rows' K/V go to scratch cells (batched decode/verify)
 
 
 class _Staging:
@@ -150,6 +153,10 @@ class GpuEngine:
         self.n_seqs = n_seqs
         self.capacity = kv.capacity_cells
         self.pos_stride = self.capacity
+        # batched plans park decode/verify rows in scratch cells past the
+        # allocator's range until the accept count is known (cell-id parity)
+        self.n_scratch = ((cfg.spec_max_lookahead + 1) * n_seqs) if cfg.batched_forward else 0
+        self.head_stride = self.capacity + self.n_scratch
         dev = self.device
         L = lib()
 
@@ -166,7 +173,7 @@ class GpuEngine:
         # ---- paged KV store ----
         # head-major [L][kv_head][cell][hd]: a run of consecutive cells of one head
         # is one contiguous block -> TMA boxes for the attention kernels
-        self.k_pool = torch.zeros((s.layers, s.n_kv_heads, self.capacity, s.head_dim),
+        self.k_pool = torch.zeros((s.layers, s.n_kv_heads, self.head_stride, s.head_dim),
                                   dtype=torch.bfloat16, device=dev)
         self.v_pool = torch.zeros_like(self.k_pool)
         self.pos2cell = torch.zeros((n_seqs, self.pos_stride), dtype=torch.int32, device=dev)
@@ -194,7 +201,7 @@ class GpuEngine:
             self.w["w_down"].data_ptr(), self.w["final_norm"].data_ptr(),
             self.w["lm_head"].data_ptr(), self.rope_cos.data_ptr(), self.rope_sin.data_ptr(),
             self.pos_stride)
-        self.kv_c = _lib.KvStore(self.k_pool.data_ptr(), self.v_pool.data_ptr(), self.capacity,
+        self.kv_c = _lib.KvStore(self.k_pool.data_ptr(), self.v_pool.data_ptr(), self.head_stride,
                                  self.pos2cell.data_ptr(), self.hist.data_ptr(), self.pos_stride,
                                  n_seqs)
         ws = L.ds_forward_workspace_bytes(ctypes.byref(self.model_c), self.max_rows,
@@ -202,6 +209,7 @@ class GpuEngine:
         self.workspace = torch.empty(ws, dtype=torch.uint8, device=dev)
         self._hash: dict[int, tuple[int, int]] = {}   # seq -> (length, FNV64 of hist[:length])
         self._pending_hist: list[tuple[int, int, np.ndarray]] = []
+        self._copies: list[tuple[int, int]] = []
         self.gpu_launches = 0
         self._ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
         self.reset_counters()
@@ -263,10 +271,22 @@ class GpuEngine:
         self._hash[seq] = (past, st)
         return st
 
-    def _stage_metadata(self) -> tuple[int, int, int, int]:
-        """Queue pending hist writes and kv ops; returns offsets for the flush."""
-        segs_off = ops_off = -1
-        n_segs = n_ops = 0
+    def queue_copies(self, pairs) -> None:
+        """(src_cell, dst_cell) K/V row moves applied at the next flush."""
+        self._copies.extend(pairs)
+
+    def _stage_metadata(self, extra_ops=None) -> tuple:
+        """Queue pending hist writes, cell copies and kv ops; offsets for the flush."""
+        segs_off = ops_off = cp_off = -1
+        n_segs = n_ops = n_cp = 0
+        if self._copies:
+            last = {}
+            for src, dst in self._copies:  # a later owner of a cell wins
+                last[dst] = src
+            pairs = np.array([(src, dst) for dst, src in last.items()], dtype=np.int32)
+            cp_off = self.stage.add(pairs)
+            n_cp = len(pairs)
+            self._copies = []
         if self._pending_hist:
             segs = np.zeros((len(self._pending_hist), 4), dtype=np.int32)
             data = []
@@ -280,14 +300,20 @@ class GpuEngine:
             segs_off = self.stage.add(segs)
             n_segs = len(segs)
             self._pending_hist = []
-        ops = self.kv.take_ops()
+        ops = self.kv.take_ops() + (extra_ops or [])
         if ops:
             ops_off = self.stage.add(np.asarray(ops, dtype=np.int32))
             n_ops = len(ops)
-        return segs_off, n_segs, ops_off, n_ops
+        return segs_off, n_segs, ops_off, n_ops, cp_off, n_cp
 
-    def _apply_metadata(self, segs_off, n_segs, ops_off, n_ops, stream) -> None:
+    def _apply_metadata(self, segs_off, n_segs, ops_off, n_ops, cp_off, n_cp, stream) -> None:
         L = lib()
+        if n_cp:
+            s = self.shape
+            check(L.ds_kv_copy_cells(self.k_pool.data_ptr(), self.v_pool.data_ptr(), s.layers,
+                                     s.n_kv_heads, self.head_stride, s.head_dim,
+                                     self.stage.dptr(cp_off), n_cp, stream), "ds_kv_copy_cells")
+            self.gpu_launches += 1
         if n_segs:
             check(L.ds_hist_write(self.stage.dev.data_ptr(), self.stage.dptr(segs_off), n_segs,
                                   self.hist.data_ptr(), self.pos_stride, stream), "ds_hist_write")
@@ -308,17 +334,23 @@ class GpuEngine:
 
     # -- forward -------------------------------------------------------------------
 
-    def run(self, reqs: list[EntryRequest]) -> list:
-        """Execute entries in one native forward; returns RowResult / VerifyResult."""
+    def run(self, reqs: list[EntryRequest], count: bool = True) -> list:
+        """Execute entries in one native forward; returns RowResult / VerifyResult
+        per request (in request order).  Requests with ``scratch`` get their rows'
+        K/V in scratch cells; their cells are reported in ``result.scratch``."""
         n_e = len(reqs)
         if n_e == 0:
             return []
         if n_e > self.max_entries:
             raise ValueError(f"{n_e} entries > engine max {self.max_entries}")
+        G = self.shape.n_heads // self.shape.n_kv_heads
+        order = sorted(range(n_e), key=lambda i: 0 if len(reqs[i].batch) * G > 32 else 1)
         ents = np.zeros(n_e, dtype=_ENTRY_DT)
         toks, rseq, rpos, orow = [], [], [], []
         q_start = out_start = 0
-        for i, r in enumerate(reqs):
+        scratch_ops, scratch_of, s_off = [], {}, 0
+        for i, ri in enumerate(order):
+            r = reqs[ri]
             q = len(r.batch)
             if q == 0:
                 raise ValueError("batch must be non-empty")
@@ -329,14 +361,22 @@ class GpuEngine:
             rseq.append(np.full(q, r.seq, dtype=np.int32))
             rpos.append(np.arange(r.past, r.past + q, dtype=np.int32))
             orow.append(np.arange(q_start + q - n_out, q_start + q, dtype=np.int32))
+            if r.scratch:
+                if s_off + q > self.n_scratch:
+                    raise ValueError("scratch cells exhausted")
+                cell = self.capacity + s_off
+                scratch_ops.append((_lib.KV_MAP_SCRATCH, r.seq, r.past, cell, q))
+                scratch_of[ri] = list(range(cell, cell + q))
+                s_off += q
             q_start += q
             out_start += n_out
-            self.ledger.count_forward(q)
+            if count:
+                self.ledger.count_forward(q)
         if q_start > self.max_rows or out_start > self.max_out:
             raise ValueError("forward exceeds engine buffers")
         st = self.stage
         st.reset()
-        meta = self._stage_metadata()
+        meta = self._stage_metadata(scratch_ops)
         o_ent = st.add(ents.view(np.int32))
         o_tok = st.add(np.concatenate(toks))
         o_seq = st.add(np.concatenate(rseq))
@@ -370,12 +410,16 @@ class GpuEngine:
         f[3] += sum(r.past + len(r.batch) for r in reqs)
         h = self.res_host.numpy()
         tok, src, acc = h[: self.max_out], h[self.max_out: 2 * self.max_out], h[2 * self.max_out:]
-        out = []
-        for i, r in enumerate(reqs):
+        out = [None] * n_e
+        for i, ri in enumerate(order):
+            r = reqs[ri]
             o0, n_out = int(ents[i]["out_start"]), int(ents[i]["n_out"])
             rows = [RowResult(int(tok[o0 + j]), None if src[o0 + j] < 0 else int(src[o0 + j]))
                     for j in range(n_out)]
-            out.append(VerifyResult(int(acc[i]), rows) if r.kind == _lib.ENTRY_VERIFY else rows[0])
+            res = VerifyResult(int(acc[i]), rows) if r.kind == _lib.ENTRY_VERIFY else rows[0]
+            if r.scratch:
+                res.scratch = scratch_of[ri]
+            out[ri] = res
         return out
 
     def launches_per_forward(self, reqs) -> int:

@@ -62,3 +62,29 @@ class OracleEngine:
             ring = list(tokens[-window:])
             out.append(cpu.lookup_ngram(ring, ring, min_match, cap))
         return out
+
+    # batched plan execution (InferenceCore with batched_forward=True)
+    def run(self, reqs, count=True):
+        from paper_2605_26289_b200 import _lib
+
+        out = []
+        for r in reqs:
+            q = len(r.batch)
+            if count:
+                self.ledger.count_forward(q)
+            self._write(r.seq, r.past, list(r.batch))
+            if r.kind == _lib.ENTRY_VERIFY:
+                rows = [self._row(r.seq, r.past + i + 1) for i in range(q)]
+                acc = 0
+                while acc < q - 1 and rows[acc].argmax_id == r.batch[1 + acc]:
+                    acc += 1
+                res = VerifyResult(acc, rows)
+            else:
+                res = self._row(r.seq, r.past + q)
+            if r.scratch:
+                res.scratch = list(range(-q, 0))
+            out.append(res)
+        return out
+
+    def queue_copies(self, pairs):
+        self.copies = getattr(self, "copies", 0) + len(list(pairs))

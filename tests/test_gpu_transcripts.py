@@ -25,10 +25,12 @@ def _device_invariants(core):
             assert eng.device_cells(seq, n) == core.kv.cell_ids(seq, 0, n)
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c2_nospec", "c3", "c4_small", "c5_small"])
-def test_trace_parity_gpu(cuda, name):
+@pytest.mark.parametrize("name,batched", [("c1", False), ("c2", False), ("c2_nospec", False),
+                                          ("c3", False), ("c4_small", False), ("c5_small", False),
+                                          ("c2", True), ("c3", True), ("c5_small", True)])
+def test_trace_parity_gpu(cuda, name, batched):
     tr = load_trace(name)
-    core = InferenceCore(core_config_for(tr, model="tiny"))
+    core = InferenceCore(core_config_for(tr, model="tiny", batched_forward=batched))
     recs = replay(core, tr)
     assert mismatches(recs) == []
     final = tr["snapshots"][-1]

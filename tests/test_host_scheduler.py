@@ -14,10 +14,11 @@ from paper_2605_26289_b200.workload import core_config_for, load_trace, mismatch
 TRACES = ["c1", "c2", "c2_nospec", "c3", "c3_nogroup", "c4_small", "c5_small"]
 
 
+@pytest.mark.parametrize("batched", [False, True])
 @pytest.mark.parametrize("name", TRACES)
-def test_trace_parity_host(name):
+def test_trace_parity_host(name, batched):
     tr = load_trace(name)
-    cfg = core_config_for(tr, model="tiny")
+    cfg = core_config_for(tr, model="tiny", batched_forward=batched)
     core = InferenceCore(cfg, engine=OracleEngine(cfg.vocab, cfg.copy_min_match))
     recs = replay(core, tr)
     assert mismatches(recs) == []
