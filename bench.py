@@ -233,7 +233,7 @@ def kernel_micro(torch, dev, peaks) -> dict:
         ent = (_lib.Entry * 1)(_lib.Entry(0, past, q, 0, 0, 0, 0, 1, 0))
         ent_d = torch.frombuffer(bytearray(bytes(ent)), dtype=torch.uint8).to(dev)
         wsb = L.ds_attention_workspace_bytes(q, 1, nh, d)
-        ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
 
         def launch():
             _lib.check(L.ds_attention(qkv.data_ptr(), ctypes.addressof(ent), ent_d.data_ptr(), 1,

@@ -9,10 +9,13 @@
 //     stage's mbarrier; otherwise the warp gathers the tile cell by cell with
 //     16-byte cp.async into the same swizzled layout.  6-stage ring, up to 5
 //     tiles (~160 KB) in flight per SM;
-//   * 4 consumer warps: each owns 16 keys of every tile; QK^T and PV on
+//   * 8 consumer warps = 4 key groups x 2 head-dim halves: warp (kg, dh) owns
+//     16 keys of every tile and output columns [64*dh, 64*dh+64); QK^T (computed
+//     by both halves of a pair - cheap next to the latency it hides) and PV on
 //     mma.sync m16n8k16 (bf16 in, fp32 accumulate), online softmax with quad
 //     shuffles, lazy O rescale, masks only on boundary tiles; then release the
-//     stage through an "empty" mbarrier.
+//     stage through an "empty" mbarrier.  Two consumer warps per scheduler
+//     hide the HMMA/LDSM latency chains a single warp could not.
 // The 128-byte swizzle keeps ldmatrix bank-conflict free.  The 4 warp states
 // merge through smem; split partials (O, lse) go to attn_combine_kernel.
 #include "../../include/deltaserve_b200.h"
@@ -29,7 +32,8 @@ constexpr int kHalfBytes = kTile * kD * 2;  // one K (or V) tile: 2 x [64 rows][
 constexpr int kStageBytes = 2 * kHalfBytes;
 constexpr int kStages = 6;
 constexpr int kQRows = 32;
-constexpr int kConsumers = 4;
+constexpr int kConsumers = 8;  // 4 key groups x 2 d halves
+constexpr int kKeyGroups = 4;
 constexpr int kThreads = (kConsumers + 1) * 32;
 
 DS_DEVICE int qswz(int row, int chunk) {
@@ -53,7 +57,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     const __nv_bfloat16* __restrict__ vpool, const int32_t* __restrict__ pos2cell,
     int64_t pos_stride, int nh, int nkv, float scale_log2, __nv_bfloat16* __restrict__ out,
     float* __restrict__ part_o, float* __restrict__ part_lse, int64_t head_stride,
-    const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv) {
+    int* __restrict__ counters, const __grid_constant__ CUtensorMap tmk,
+    const __grid_constant__ CUtensorMap tmv) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // SW128 alignment
   uint8_t* qs = smem + kStages * kStageBytes;
@@ -163,8 +168,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
 
   // ================= consumers =================
   const int g8 = lane >> 2, t4 = lane & 3, mi = lane >> 3;
+  const int kg = warp & (kKeyGroups - 1), dh = warp / kKeyGroups;
   int qpos[MT][2];
-  float o[MT][16][4];
+  float o[MT][8][4];
   float m_run[MT][2], l_run[MT][2];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
@@ -176,18 +182,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
       l_run[mt][h] = 0.f;
     }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) o[mt][j][0] = o[mt][j][1] = o[mt][j][2] = o[mt][j][3] = 0.f;
+    for (int j = 0; j < 8; ++j) o[mt][j][0] = o[mt][j][1] = o[mt][j][2] = o[mt][j][3] = 0.f;
   }
   const uint32_t qs_u = smem_u32(qs);
-  // per-lane ldmatrix rows inside a tile (keys of this warp)
-  const int k_row = warp * 16 + (mi >> 1) * 8 + (lane & 7);
-  const int v_row = warp * 16 + (mi & 1) * 8 + (lane & 7);
+  // per-lane ldmatrix rows inside a tile (keys of this warp's group)
+  const int k_row = kg * 16 + (mi >> 1) * 8 + (lane & 7);
+  const int v_row = kg * 16 + (mi & 1) * 8 + (lane & 7);
 
   for (int it = 0; it < ntiles; ++it) {
     const int st = it % kStages;
     mbar_wait(&full[st], (it / kStages) & 1);
     const uint32_t ks_u = smem_u32(smem + st * kStageBytes), vs_u = ks_u + kHalfBytes;
-    const int kt = k_begin + it * kTile + warp * 16;
+    const int kt = k_begin + it * kTile + kg * 16;
     float s[MT][2][4];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
@@ -234,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
       }
       if (__any_sync(0xffffffffu, alpha[0] != 1.f || alpha[1] != 1.f)) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < 8; ++j) {
           o[mt][j][0] *= alpha[0];
           o[mt][j][1] *= alpha[0];
           o[mt][j][2] *= alpha[1];
@@ -259,9 +265,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
       pa[mt][3] = pack_bf16(s[mt][1][2], s[mt][1][3]);
     }
 #pragma unroll
-    for (int dn = 0; dn < 16; dn += 2) {
+    for (int dn = 0; dn < 8; dn += 2) {
       uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(b0, b1, b2, b3, vs_u + tswz(v_row, dn + (mi >> 1)));
+      ldsm_x4_t(b0, b1, b2, b3, vs_u + tswz(v_row, dh * 8 + dn + (mi >> 1)));
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         mma_bf16_16816(o[mt][dn], pa[mt], b0, b1);
@@ -273,10 +279,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
   }
   named_bar_sync(1, kConsumers * 32);  // all consumers done with the ring
 
-  // ---- merge the 4 warps' states (ring memory is free now) ----
+  // ---- merge the 4 key groups' states (ring memory is free now) ----
   float* osm = reinterpret_cast<float*>(smem);  // [4][32][128]
-  float* msm = osm + kConsumers * kQRows * kD;  // [4][32]
-  float* lsm = msm + kConsumers * kQRows;       // [4][32]
+  float* msm = osm + kKeyGroups * kQRows * kD;  // [4][32]
+  float* lsm = msm + kKeyGroups * kQRows;       // [4][32]
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
@@ -285,13 +291,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
       l += __shfl_xor_sync(0xffffffffu, l, 1);
       l += __shfl_xor_sync(0xffffffffu, l, 2);
       const int r = mt * 16 + g8 + 8 * h;
-      if (t4 == 0) {
-        msm[warp * kQRows + r] = m_run[mt][h];
-        lsm[warp * kQRows + r] = l;
+      if (t4 == 0 && dh == 0) {
+        msm[kg * kQRows + r] = m_run[mt][h];
+        lsm[kg * kQRows + r] = l;
       }
 #pragma unroll
-      for (int dn = 0; dn < 16; ++dn)
-        *reinterpret_cast<float2*>(osm + (warp * kQRows + r) * kD + dn * 8 + 2 * t4) =
+      for (int dn = 0; dn < 8; ++dn)
+        *reinterpret_cast<float2*>(osm + (kg * kQRows + r) * kD + dh * 64 + dn * 8 + 2 * t4) =
             make_float2(o[mt][dn][2 * h], o[mt][dn][2 * h + 1]);
     }
   }
@@ -302,11 +308,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     const int r = idx / kD, d = idx - r * kD;
     float mm = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kConsumers; ++w) mm = fmaxf(mm, msm[w * kQRows + r]);
+    for (int w = 0; w < kKeyGroups; ++w) mm = fmaxf(mm, msm[w * kQRows + r]);
     const float mref = mm == -INFINITY ? 0.f : mm;
     float L = 0.f, acc = 0.f;
 #pragma unroll
-    for (int w = 0; w < kConsumers; ++w) {
+    for (int w = 0; w < kKeyGroups; ++w) {
       const float sc = fast_exp2(msm[w * kQRows + r] - mref);
       L += lsm[w * kQRows + r] * sc;
       acc += osm[(w * kQRows + r) * kD + d] * sc;
@@ -328,7 +334,7 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
                        int n_entries, const void* k_pool, const void* v_pool, int64_t head_stride,
                        const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv, int max_R,
                        int max_splits, float scale, void* out, float* part_o, float* part_lse,
-                       cudaStream_t stream) {
+                       int* counters, cudaStream_t stream) {
   (void)entries_host;
   const int smem = decode_smem_bytes();
   static bool attr = false;
@@ -348,7 +354,7 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
              stride, entries_dev, n_entries, max_splits,
              static_cast<const __nv_bfloat16*>(k_pool), static_cast<const __nv_bfloat16*>(v_pool),
              pos2cell, pos_stride, nh, nkv, sl2, static_cast<__nv_bfloat16*>(out), part_o,
-             part_lse, head_stride, *tk, *tv);
+             part_lse, head_stride, counters, *tk, *tv);
   return (int)cudaGetLastError();
 }
 

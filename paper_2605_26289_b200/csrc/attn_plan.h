@@ -68,7 +68,7 @@ size_t prefill_partial_bytes_bound();
 inline size_t attn_partial_bytes_bound() {
   const size_t dec = static_cast<size_t>(4 * kNumSMs) * kSplitRows * (128 + 1) * sizeof(float);
   const size_t pre = prefill_partial_bytes_bound();
-  return dec > pre ? dec : pre;
+  return (dec > pre ? dec : pre) + (64 << 10);  // + split-merge counters
 }
 
 }  // namespace ds

@@ -44,7 +44,7 @@ constexpr int kSmemKV = 2 * kQHalf;                   // stages x (K 16 KB | V 1
 constexpr int kSmemBar = kSmemKV + kStages * 4 * kKHalf;
 constexpr int kSmemBytes = kSmemBar + 128;
 constexpr int kTmemCols = 256;  // S0/P0 [0,64) S1/P1 [64,128) O [128,256)
-constexpr int kMaxSplits = 8;
+constexpr int kMaxSplits = 64;
 constexpr int kMaxPartialCtas = 8 * 148;  // bounds the split-partial workspace
 
 // 16-byte chunk c (0..15 over d) of row r in a tile of `rows` rows, SW128
@@ -318,43 +318,43 @@ __global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
   }
 }
 
-// merge key-split partials: out = sum_s 2^(lse_s - max) O_s / sum_s 2^(lse_s - max)
-__global__ void attn_prefill_combine(const ds_entry* __restrict__ entries, int splits, int max_qb,
-                                     int nh, int nkv, const float* __restrict__ part_o,
-                                     const float* __restrict__ part_lse,
-                                     __nv_bfloat16* __restrict__ out) {
+// merge key-split partials: out = sum_s 2^(lse_s - max) O_s / sum_s 2^(lse_s - max).
+// One warp per packed row (lane = 4 head-dim columns); split loops unrolled so
+// the L2 loads of different splits overlap.
+__global__ void __launch_bounds__(256) attn_prefill_combine(
+    const ds_entry* __restrict__ entries, int splits, int max_qb, int nh, int nkv,
+    const float* __restrict__ part_o, const float* __restrict__ part_lse,
+    __nv_bfloat16* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
-  const int e = blockIdx.z, kh = blockIdx.y, qb = blockIdx.x;
+  const int e = blockIdx.z, kh = blockIdx.y;
+  const int qb = blockIdx.x >> 4;                          // 16 blocks x 8 rows per q-block
+  const int r = ((blockIdx.x & 15) << 3) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   const ds_entry en = entries[e];
   const int G = nh / nkv;
-  const int t0 = qb * (kBM / G);
-  if (t0 >= en.q_len) return;
-  for (int idx = threadIdx.x; idx < kBM * 16; idx += blockDim.x) {
-    const int r = idx >> 4, c8 = idx & 15;
-    const int t = t0 + r / G, g = r - (r / G) * G;
-    if (t >= en.q_len) continue;
-    float mx = -INFINITY;
-    for (int s = 0; s < splits; ++s)
-      mx = fmaxf(mx, part_lse[prefill_slot(e, s, qb, kh, splits, max_qb, nkv) * kBM + r]);
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, wsum = 0.f;
-    for (int s = 0; s < splits; ++s) {
-      const int64_t slot = prefill_slot(e, s, qb, kh, splits, max_qb, nkv) * kBM + r;
-      const float lse = part_lse[slot];
-      if (lse == -INFINITY) continue;
-      const float w = exp2f(lse - mx);
-      wsum += w;
-      const float4* p = reinterpret_cast<const float4*>(part_o + slot * kD + c8 * 8);
-      const float4 a = p[0], b = p[1];
-      acc[0] += w * a.x; acc[1] += w * a.y; acc[2] += w * a.z; acc[3] += w * a.w;
-      acc[4] += w * b.x; acc[5] += w * b.y; acc[6] += w * b.z; acc[7] += w * b.w;
-    }
-    const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
-    *reinterpret_cast<uint4*>(out + static_cast<int64_t>(en.q_start + t) * nh * kD +
-                              (kh * G + g) * kD + c8 * 8) =
-        make_uint4(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv),
-                   pack_bf16(acc[4] * inv, acc[5] * inv), pack_bf16(acc[6] * inv, acc[7] * inv));
+  const int t = qb * (kBM / G) + r / G, g = r - (r / G) * G;
+  if (t >= en.q_len) return;
+  const int64_t s0 = prefill_slot(e, 0, qb, kh, splits, max_qb, nkv) * kBM + r;
+  const int64_t ss = static_cast<int64_t>(max_qb) * nkv * kBM;  // slot stride between splits
+  float mx = -INFINITY;
+#pragma unroll 8
+  for (int s = 0; s < splits; ++s) mx = fmaxf(mx, __ldcg(part_lse + s0 + s * ss));
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float wsum = 0.f;
+#pragma unroll 8
+  for (int s = 0; s < splits; ++s) {
+    const int64_t slot = s0 + s * ss;
+    const float lse = __ldcg(part_lse + slot);
+    const float w = lse == -INFINITY ? 0.f : exp2f(lse - mx);
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(part_o + slot * kD) + lane);
+    wsum += w;
+    acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
   }
+  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+  uint2* dst = reinterpret_cast<uint2*>(out + static_cast<int64_t>(en.q_start + t) * nh * kD +
+                                        (kh * G + g) * kD) + lane;
+  *dst = make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
 }
 
 // key splits that best fill whole waves of 2 CTAs per SM (>= 8 tiles each)
@@ -400,6 +400,9 @@ int launch_attn_prefill_sm100(const void* qkv, const ds_entry* entries_host,
     const int tiles = (en.past + en.q_len + kBN - 1) / kBN;
     max_tiles = tiles > max_tiles ? tiles : max_tiles;
   }
+  constexpr size_t kCounterBytes = 64 << 10;  // reserved for the decode split counters
+  workspace = static_cast<uint8_t*>(workspace) + kCounterBytes;
+  ws_bytes = ws_bytes > kCounterBytes ? ws_bytes - kCounterBytes : 0;
   int splits = prefill_splits(qb_total * nkv, max_tiles);
   const size_t need = static_cast<size_t>(n_entries) * splits * max_qb * nkv * kBM *
                       (kD + 1) * sizeof(float);
@@ -416,7 +419,7 @@ int launch_attn_prefill_sm100(const void* qkv, const ds_entry* entries_host,
       static_cast<__nv_bfloat16*>(out), splits, max_qb, part_o, part_lse, *tk, *tv);
   if (err != cudaSuccess) return static_cast<int>(err);
   if (splits > 1) {
-    err = launch_pdl(attn_prefill_combine, dim3(max_qb, nkv, n_entries), dim3(256), 0, stream,
+    err = launch_pdl(attn_prefill_combine, dim3(max_qb * 16, nkv, n_entries), dim3(256), 0, stream,
                      entries_dev, splits, max_qb, nh, nkv, (const float*)part_o,
                      (const float*)part_lse, static_cast<__nv_bfloat16*>(out));
     if (err != cudaSuccess) return static_cast<int>(err);

@@ -270,18 +270,20 @@ __global__ void attn_combine_kernel(const ds_entry* __restrict__ entries, int n_
   const AttnSplitPlan plan = attn_split_plan(qblocks, en.past + en.q_len, nkv, n_entries, mode);
   if (plan.n_splits <= 1) return;
   const int64_t base = attn_partial_base(entries, e, n_entries, nh, nkv, mode);
+  // splits are independent loads: unrolled so their L2 latencies overlap
+  const int64_t s0 = (base + r) * nkv + kh, sstride = static_cast<int64_t>(R) * nkv;
   float lmax = -INFINITY;
-  for (int s = 0; s < plan.n_splits; ++s)
-    lmax = fmaxf(lmax, part_lse[(base + static_cast<int64_t>(s) * R + r) * nkv + kh]);
+#pragma unroll 8
+  for (int s = 0; s < plan.n_splits; ++s) lmax = fmaxf(lmax, __ldcg(part_lse + s0 + s * sstride));
   float acc = 0.f, wsum = 0.f;
   const int d = threadIdx.x;
+#pragma unroll 8
   for (int s = 0; s < plan.n_splits; ++s) {
-    const int64_t slot = (base + static_cast<int64_t>(s) * R + r) * nkv + kh;
-    const float lse = part_lse[slot];
-    if (lse == -INFINITY) continue;
-    const float w = exp2f(lse - lmax);
+    const int64_t slot = s0 + s * sstride;
+    const float lse = __ldcg(part_lse + slot);
+    const float w = lse == -INFINITY ? 0.f : exp2f(lse - lmax);
     wsum += w;
-    acc += w * part_o[slot * kD + d];
+    acc += w * __ldcg(part_o + slot * kD + d);
   }
   const int ti = r / G, gi = r - (r / G) * G;
   out[static_cast<int64_t>(en.q_start + ti) * nh * kD + (kh * G + gi) * kD + d] =
@@ -294,7 +296,7 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
                        int n_entries, const void* k_pool, const void* v_pool, int64_t head_stride,
                        const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv, int max_R,
                        int max_splits, float scale, void* out, float* part_o, float* part_lse,
-                       cudaStream_t stream);
+                       int* counters, cudaStream_t stream);
 
 int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_entry* entries_dev,
                       int n_entries, const void* k_pool, const void* v_pool, int64_t head_stride,
@@ -319,6 +321,12 @@ int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_en
     max_splits = p.n_splits > max_splits ? p.n_splits : max_splits;
     any_split |= p.n_splits > 1;
   }
+  // workspace: [split-merge counters (zero-initialised once, self-resetting)][partials]
+  constexpr size_t kCounterBytes = 64 << 10;
+  if (n_entries * nkv * 4 > static_cast<int>(kCounterBytes)) return DS_EUNSUPPORTED;
+  int* counters = static_cast<int*>(workspace);
+  workspace = static_cast<uint8_t*>(workspace) + kCounterBytes;
+  ws_bytes = ws_bytes > kCounterBytes ? ws_bytes - kCounterBytes : 0;
   const size_t need = attn_partial_bytes(entries_host, n_entries, nh, nkv, mode);
   if (need > ws_bytes) return DS_EWORKSPACE;
   float* part_o = static_cast<float*>(workspace);
@@ -327,12 +335,12 @@ int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_en
   if (mode == 1) {
     const int rc = launch_attn_decode(qkv, entries_host, entries_dev, n_entries, k_pool, v_pool,
                                       head_stride, pos2cell, pos_stride, nh, nkv, max_R,
-                                      max_splits, scale, out,
-                                      part_o, part_lse, stream);
+                                      max_splits, scale, out, part_o, part_lse, counters, stream);
     if (rc != 0 || !any_split) return rc;
     dim3 cgrid(max_R, nkv, n_entries);
     launch_pdl(attn_combine_kernel, cgrid, dim3(kD), 0, stream, entries_dev, n_entries, nh, nkv,
-               kSplitNW * 16, 1, part_o, part_lse, static_cast<__nv_bfloat16*>(out));
+               kSplitNW * 16, 1, (const float*)part_o, (const float*)part_lse,
+               static_cast<__nv_bfloat16*>(out));
     return (int)cudaGetLastError();
   }
   const int smem = 2 * 2 * kTileBytes;

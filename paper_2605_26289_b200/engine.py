@@ -206,7 +206,8 @@ class GpuEngine:
                                  n_seqs)
         ws = L.ds_forward_workspace_bytes(ctypes.byref(self.model_c), self.max_rows,
                                           self.max_out, self.max_entries)
-        self.workspace = torch.empty(ws, dtype=torch.uint8, device=dev)
+        # zero once: the attention split-merge counters live here and self-reset
+        self.workspace = torch.zeros(ws, dtype=torch.uint8, device=dev)
         self._hash: dict[int, tuple[int, int]] = {}   # seq -> (length, FNV64 of hist[:length])
         self._pending_hist: list[tuple[int, int, np.ndarray]] = []
         self._copies: list[tuple[int, int]] = []

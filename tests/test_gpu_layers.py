@@ -112,7 +112,7 @@ def _attention_case(cuda, past, q_len, contiguous, impl):
     ent_dev = torch.frombuffer(bytearray(bytes(ent)), dtype=torch.uint8).to(cuda)
     out = torch.zeros(q_len, nh * d, dtype=torch.bfloat16, device=cuda)
     ws_bytes = lib().ds_attention_workspace_bytes(q_len, 1, nh, d)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=cuda)
+    ws = torch.zeros(ws_bytes, dtype=torch.uint8, device=cuda)
     qkv_d = qkv.to(cuda)
     check(lib().ds_attention(qkv_d.data_ptr(), ctypes.addressof(ent), ent_dev.data_ptr(), 1,
                              q_len, k_pool.data_ptr(), v_pool.data_ptr(), cap,
