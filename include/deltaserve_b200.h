@@ -128,7 +128,8 @@ typedef struct {
   const void* wqkv;       /* bf16 [L][(nh+2nkv)*hd][hidden] */
   const void* wo;         /* bf16 [L][hidden][nh*hd] */
   const void* mlp_norm;   /* bf16 [L][hidden] */
-  const void* w_gate_up;  /* bf16 [L][2*ffn][hidden]  (gate rows first) */
+  const void* w_gate_up;  /* bf16 [L][2*ffn][hidden]: 8-row blocks, gate units 8b..8b+7
+                           * then up units 8b..8b+7 (row 16b+j: j<8 gate, else up) */
   const void* w_down;     /* bf16 [L][hidden][ffn] */
   const void* final_norm; /* bf16 [hidden] */
   const void* lm_head;    /* bf16 [vocab][hidden] */
@@ -179,7 +180,7 @@ typedef struct {
   int32_t* out_src;             /* device [n_out] copy source or -1 */
   int32_t* out_accept;          /* device [n_entries] accepted drafts (VERIFY) */
   float* logits;                /* device [n_out][vocab] fp32 */
-  void* workspace;
+  void* workspace;               /* zero-initialised once, then reused across calls */
   size_t workspace_bytes;
 } ds_forward_args;
 
@@ -216,6 +217,8 @@ int ds_attention(const void* qkv, const ds_entry* entries_host, const ds_entry* 
  * stream -> bf16: out = x * rsqrt(mean(x^2) + eps) * w, fp32 math. */
 int ds_rmsnorm(const void* x, int x_f32, const int32_t* rows, int n_rows, int hidden,
                const void* w, float eps, void* out, ds_stream_t stream);
+/* act[r][f] = silu(gate f) * up f from a gate|up row in the interleaved
+ * w_gate_up layout (ds_model). */
 int ds_silu_mul(const void* gate_up, int n_rows, int ffn, void* out, ds_stream_t stream);
 int ds_embed(const int32_t* tokens, int n_rows, const void* table, int hidden, void* out,
              int out_f32, ds_stream_t stream);
@@ -225,6 +228,33 @@ int ds_embed(const int32_t* tokens, int n_rows, const void* table, int hidden, v
  * HBM-bound; replaces cuBLAS for the engine's decode/verify projections. */
 int ds_gemm_skinny(const void* X, const void* W, void* Y, int M, int N, int K, int y_f32,
                    int accumulate, ds_stream_t stream);
+
+/* Epilogue fusions of the skinny GEMM (the decode forward's elementwise
+ * kernels folded into the projections; see gemm_skinny.cu).  An "ss buffer"
+ * is uint64 [32]: per-row sums of squares in 2^-24 fixed point (integer
+ * atomics, so the sum is independent of CTA order).
+ *  ss_out/h_out/h_w: residual producer (y_f32 = 1) - adds the rows' sums of
+ *      y^2 into ss_out (which must start at zero); h_out[m][n] =
+ *      bf16(y[m][n] * h_w[n]) (optional).
+ *  ss_zero: an ss buffer to clear (after the kernel's dependency wait) - the
+ *      forward alternates two buffers, each producer clearing the other.
+ *  row_ss/eps: norm consumer - row m of the product is scaled by
+ *      rsqrt(row_ss[m] * 2^-24 / K + eps) (X holds bf16(x * norm_w)).
+ *  swiglu: W rows are gate/up interleaved in 8-row blocks (see ds_model);
+ *      Y = bf16 silu(gate) * up [M][N/2]. */
+#define DS_SKINNY_SS_WORDS 32
+typedef struct {
+  const uint64_t* row_ss;
+  float eps;
+  uint64_t* ss_out;
+  uint64_t* ss_zero;
+  void* h_out;
+  const void* h_w;
+  int32_t swiglu;
+} ds_skinny_epi;
+
+int ds_gemm_skinny_ex(const void* X, const void* W, void* Y, int M, int N, int K, int y_f32,
+                      int accumulate, const ds_skinny_epi* epi, ds_stream_t stream);
 
 /* K8: row argmax over fp32 logits (lowest index on ties, engine.py:146-159). */
 int ds_argmax(const float* logits, int n_rows, int vocab, int32_t* out, ds_stream_t stream);

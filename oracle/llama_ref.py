@@ -15,6 +15,14 @@ from __future__ import annotations
 import torch
 
 
+
+def split_gate_up(gu, ffn: int):
+    """gate, up from a gate|up projection whose weight rows are interleaved in
+    8-unit blocks (row 16b+j: j<8 gate unit 8b+j, else up unit 8b+j-8) - the
+    ds_model.w_gate_up layout (include/deltaserve_b200.h)."""
+    v = gu.reshape(*gu.shape[:-1], ffn // 8, 2, 8)
+    return v[..., 0, :].reshape(*gu.shape[:-1], ffn), v[..., 1, :].reshape(*gu.shape[:-1], ffn)
+
 def _bf(x: torch.Tensor) -> torch.Tensor:
     return x.to(torch.bfloat16).float()
 
@@ -69,7 +77,7 @@ def forward(w: dict, shape, tokens: list[int], out_rows: list[int] | None = None
         x = x + o @ w["wo"][l].T  # fp32 residual stream
         h = rmsnorm(x, w["mlp_norm"][l], shape.rms_eps)
         gu = _bf(h @ w["w_gate_up"][l].T)
-        g, u = gu[:, : shape.ffn], gu[:, shape.ffn:]
+        g, u = split_gate_up(gu, shape.ffn)
         a = _bf(torch.nn.functional.silu(g) * u)
         x = x + a @ w["w_down"][l].T
     rows = list(range(T)) if out_rows is None else out_rows

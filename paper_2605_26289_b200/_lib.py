@@ -49,6 +49,14 @@ ENTRY_PREFILL, ENTRY_DECODE, ENTRY_VERIFY = 0, 1, 2
 POLICY_COPY, POLICY_ARGMAX = 0, 1
 
 
+
+
+class SkinnyEpi(ctypes.Structure):
+    """ds_skinny_epi: epilogue fusions of ds_gemm_skinny_ex."""
+    _fields_ = [("row_ss", c_vp), ("eps", c_f32), ("ss_out", c_vp), ("ss_zero", c_vp),
+                ("h_out", c_vp), ("h_w", c_vp), ("swiglu", c_i32)]
+
+
 class ForwardArgs(ctypes.Structure):
     _fields_ = [("n_entries", c_i32), ("n_rows", c_i32), ("n_out", c_i32), ("policy", c_i32),
                 ("copy_min_match", c_i32), ("policy_vocab", c_i32), ("entries_host", c_vp),
@@ -104,6 +112,7 @@ def lib() -> ctypes.CDLL:
         "ds_embed": (c_i32, [P, c_i32, P, c_i32, P, c_i32, P]),
         "ds_argmax": (c_i32, [P, c_i32, c_i32, P, P]),
         "ds_gemm_skinny": (c_i32, [P, P, P, c_i32, c_i32, c_i32, c_i32, c_i32, P]),
+        "ds_gemm_skinny_ex": (c_i32, [P, P, P, c_i32, c_i32, c_i32, c_i32, c_i32, P, P]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

@@ -9,12 +9,31 @@
 // k order inside each 32-wide chunk is permuted identically for A and B (a dot
 // product is order free), so one 16-byte X load supplies both k16 steps.
 // A CTA owns 16 output features; its 8 warps split K and reduce through smem.
+// The activation operand (L2-resident) is software-pipelined one chunk ahead
+// in registers so its latency never serialises the MMAs; rows >= M are
+// predicated off (no load).
+//
+// The epilogue absorbs the layer's elementwise kernels (ds_skinny_epi):
+//  * residual producer (wo, down; Y fp32 accumulate): also writes
+//    h = bf16(y * h_w) - the next RMSNorm's weight multiply - and this CTA's
+//    per-row partial sum of y^2 over its 16 features, added into the row sums
+//    in 2^-24 fixed point (integer atomics: bit-identical whatever the CTA
+//    order); it also clears the other ss buffer (consumed upstream);
+//  * norm consumer (wqkv, gate_up): scales row m of the product by
+//    rsqrt(row sum / K + eps) - RMSNorm is a per-row scalar, so it commutes
+//    with the projection.  The row sum is loaded before the main loop and
+//    only consumed in the epilogue (no exposed latency);
+//  * SwiGLU (gate_up with 8-row interleaved weights): feature rows g / g+8 of
+//    the CTA are gate / up of the same FFN unit, so the thread holding both
+//    writes act = bf16(silu(g) * u) directly (half the output bytes, no
+//    separate kernel).
 #include "../../include/deltaserve_b200.h"
 #include "common.cuh"
 
 namespace ds {
 
 constexpr int kGemvWarps = 8;
+constexpr float kSsScale = 16777216.f;  // 2^24 fixed point for the row sums of squares
 
 DS_DEVICE uint4 ldg_stream(const void* p) {
   uint4 r;
@@ -24,11 +43,25 @@ DS_DEVICE uint4 ldg_stream(const void* p) {
   return r;
 }
 
+// predicated 16-byte activation load (zeros when off), no branch
+DS_DEVICE uint4 ldg_pred(const void* p, bool on) {
+  uint4 r = make_uint4(0, 0, 0, 0);
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n"
+      " @q ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];\n}\n"
+      : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
+      : "l"(p), "r"(static_cast<int>(on)));
+  return r;
+}
+
+DS_DEVICE float bf16r(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+
 template <int MT, int U>
 __global__ void __launch_bounds__(kGemvWarps * 32) gemm_skinny_kernel(
     const __nv_bfloat16* __restrict__ X, const __nv_bfloat16* __restrict__ W, void* __restrict__ Y,
-    int M, int N, int K, int y_f32, int accumulate) {
+    int M, int N, int K, int y_f32, int accumulate, ds_skinny_epi epi) {
   __shared__ float red[kGemvWarps][MT][4][32];
+  __shared__ float s_inv[32];
+  __shared__ float s_sq[32][17];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int n0 = blockIdx.x * 16;
@@ -48,7 +81,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemm_skinny_kernel(
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
 
-  uint4 a[U][2], b[U][MT];
+  uint4 a[U][2], bn[U][MT];
   // weights do not depend on the previous kernel: stream the first chunk
   // before waiting on the activations (programmatic dependent launch)
 #pragma unroll
@@ -58,18 +91,34 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemm_skinny_kernel(
   }
   pdl_wait();
   pdl_trigger();
-  for (int kc = 0; kc < kslice; kc += 32 * U) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (kc) {
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) bn[u][mt] = ldg_pred(xr[mt] + 32 * u, xv[mt]);
+  if (epi.ss_zero && blockIdx.x == 0 && threadIdx.x < 32) epi.ss_zero[threadIdx.x] = 0;
+  // norm consumer: the producer's row sum of squares, needed only in the epilogue
+  const unsigned long long row_sum =
+      epi.row_ss && threadIdx.x < M ? __ldcg(reinterpret_cast<const unsigned long long*>(epi.row_ss) + threadIdx.x) : 0ull;
+
+  for (int kc = 0; kc < kslice; kc += 32 * U) {
+    if (kc) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
         a[u][0] = ldg_stream(w0 + kc + 32 * u);
         a[u][1] = ldg_stream(w1 + kc + 32 * u);
       }
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-        b[u][mt] = xv[mt] ? __ldg(reinterpret_cast<const uint4*>(xr[mt] + kc + 32 * u))
-                          : make_uint4(0, 0, 0, 0);
     }
+    uint4 b[U][MT];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) b[u][mt] = bn[u][mt];
+    // next chunk (the last iteration re-reads its own chunk: harmless, branch-free)
+    const int kn = kc + 32 * U < kslice ? kc + 32 * U : kc;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) bn[u][mt] = ldg_pred(xr[mt] + kn + 32 * u, xv[mt]);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint32_t s0[4] = {a[u][0].x, a[u][1].x, a[u][0].y, a[u][1].y};
@@ -85,34 +134,96 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemm_skinny_kernel(
   for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
     for (int q = 0; q < 4; ++q) red[warp][mt][q][lane] = acc[mt][q];
+  if (epi.row_ss && threadIdx.x < M)
+    s_inv[threadIdx.x] =
+        rsqrtf(__ull2float_rn(row_sum) / (kSsScale * static_cast<float>(K)) + epi.eps);
   __syncthreads();
-  // thread -> (mt, q, lane) output element; sum the 8 warps' partials
+  // accumulator element (mt, q, ln): c0,c1 = (feature g, tokens 2t, 2t+1);
+  // c2,c3 = (feature g+8, same tokens)
+  if (epi.swiglu) {
+    // (q, q+2) hold gate / up of FFN unit n0/2 + g for the same token
+    for (int idx = threadIdx.x; idx < MT * 2 * 32; idx += kGemvWarps * 32) {
+      const int mt = idx / 64, q = (idx / 32) & 1, ln = idx & 31;
+      const int m = mt * 8 + 2 * (ln & 3) + q;
+      if (m >= M) continue;
+      float sg = 0.f, su = 0.f;
+#pragma unroll
+      for (int w = 0; w < kGemvWarps; ++w) {
+        sg += red[w][mt][q][ln];
+        su += red[w][mt][q + 2][ln];
+      }
+      if (epi.row_ss) {
+        sg *= s_inv[m];
+        su *= s_inv[m];
+      }
+      const float gg = bf16r(sg), uu = bf16r(su);  // the unfused path stores gate|up in bf16
+      static_cast<__nv_bfloat16*>(Y)[static_cast<int64_t>(m) * (N / 2) + n0 / 2 + (ln >> 2)] =
+          __float2bfloat16_rn(gg / (1.f + expf(-gg)) * uu);
+    }
+    return;
+  }
   for (int idx = threadIdx.x; idx < MT * 4 * 32; idx += kGemvWarps * 32) {
     const int mt = idx / 128, q = (idx / 32) & 3, ln = idx & 31;
+    const int fl = (ln >> 2) + ((q & 2) ? 8 : 0);  // feature within the CTA
+    const int feat = n0 + fl;
+    const int m = mt * 8 + 2 * (ln & 3) + (q & 1);
+    if (m >= M) continue;
     float s = 0.f;
 #pragma unroll
     for (int w = 0; w < kGemvWarps; ++w) s += red[w][mt][q][ln];
-    // c0,c1: (feature g, tokens 2t, 2t+1); c2,c3: (feature g+8, same tokens)
-    const int feat = n0 + (ln >> 2) + ((q & 2) ? 8 : 0);
-    const int m = mt * 8 + 2 * (ln & 3) + (q & 1);
-    if (m >= M) continue;
+    if (epi.row_ss) s *= s_inv[m];
     const int64_t o = static_cast<int64_t>(m) * N + feat;
+    float y;
     if (y_f32) {
-      float* y = static_cast<float*>(Y) + o;
-      *y = accumulate ? *y + s : s;
+      float* yp = static_cast<float*>(Y) + o;
+      y = accumulate ? *yp + s : s;
+      *yp = y;
     } else {
-      __nv_bfloat16* y = static_cast<__nv_bfloat16*>(Y) + o;
-      *y = __float2bfloat16_rn(accumulate ? __bfloat162float(*y) + s : s);
+      __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(Y) + o;
+      const __nv_bfloat16 yb = __float2bfloat16_rn(accumulate ? __bfloat162float(*yp) + s : s);
+      *yp = yb;
+      y = __bfloat162float(yb);
+    }
+    if (epi.ss_out) {  // residual producer: the next RMSNorm's weight multiply + partial sums
+      if (epi.h_out)
+        static_cast<__nv_bfloat16*>(epi.h_out)[o] =
+            __float2bfloat16_rn(y * __bfloat162float(static_cast<const __nv_bfloat16*>(epi.h_w)[feat]));
+      s_sq[m][fl] = y * y;
+    }
+  }
+  if (epi.ss_out) {
+    __syncthreads();
+    if (threadIdx.x < M) {
+      float v = 0.f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v += s_sq[threadIdx.x][j];
+      atomicAdd(reinterpret_cast<unsigned long long*>(epi.ss_out) + threadIdx.x,
+                static_cast<unsigned long long>(__float2ll_rn(v * kSsScale)));
     }
   }
 }
 
 template <int MT, int U>
 static void launch(const void* X, const void* W, void* Y, int M, int N, int K, int y_f32, int acc,
-                   cudaStream_t s) {
+                   const ds_skinny_epi& epi, cudaStream_t s) {
+  const int kslice = K / kGemvWarps;
+  if constexpr (U > 1) {
+    if (kslice % (32 * U)) {
+      launch<MT, U / 2>(X, W, Y, M, N, K, y_f32, acc, epi, s);
+      return;
+    }
+  }
   launch_pdl(gemm_skinny_kernel<MT, U>, dim3(N / 16), dim3(kGemvWarps * 32), 0, s,
              static_cast<const __nv_bfloat16*>(X), static_cast<const __nv_bfloat16*>(W), Y, M, N,
-             K, y_f32, acc);
+             K, y_f32, acc, epi);
+}
+
+static int run(const void* X, const void* W, void* Y, int M, int N, int K, int y_f32, int acc,
+               const ds_skinny_epi& epi, cudaStream_t s) {
+  if (M <= 8) launch<1, 8>(X, W, Y, M, N, K, y_f32, acc, epi, s);
+  else if (M <= 16) launch<2, 4>(X, W, Y, M, N, K, y_f32, acc, epi, s);
+  else launch<4, 2>(X, W, Y, M, N, K, y_f32, acc, epi, s);
+  return (int)cudaGetLastError();
 }
 
 }  // namespace ds
@@ -120,18 +231,16 @@ static void launch(const void* X, const void* W, void* Y, int M, int N, int K, i
 extern "C" int ds_gemm_skinny(const void* X, const void* W, void* Y, int M, int N, int K,
                               int y_f32, int accumulate, ds_stream_t stream) {
   if (M <= 0 || M > 32 || N % 16 || K % (32 * ds::kGemvWarps)) return DS_EINVAL;
-  cudaStream_t s = (cudaStream_t)stream;
-  const int kslice = K / ds::kGemvWarps;
-  if (M <= 8) {
-    if (kslice % (32 * 8) == 0) ds::launch<1, 8>(X, W, Y, M, N, K, y_f32, accumulate, s);
-    else if (kslice % (32 * 4) == 0) ds::launch<1, 4>(X, W, Y, M, N, K, y_f32, accumulate, s);
-    else ds::launch<1, 1>(X, W, Y, M, N, K, y_f32, accumulate, s);
-  } else if (M <= 16) {
-    if (kslice % (32 * 4) == 0) ds::launch<2, 4>(X, W, Y, M, N, K, y_f32, accumulate, s);
-    else ds::launch<2, 1>(X, W, Y, M, N, K, y_f32, accumulate, s);
-  } else {
-    if (kslice % (32 * 2) == 0) ds::launch<4, 2>(X, W, Y, M, N, K, y_f32, accumulate, s);
-    else ds::launch<4, 1>(X, W, Y, M, N, K, y_f32, accumulate, s);
-  }
-  return (int)cudaGetLastError();
+  const ds_skinny_epi none{};
+  return ds::run(X, W, Y, M, N, K, y_f32, accumulate, none, (cudaStream_t)stream);
+}
+
+extern "C" int ds_gemm_skinny_ex(const void* X, const void* W, void* Y, int M, int N, int K,
+                                 int y_f32, int accumulate, const ds_skinny_epi* epi,
+                                 ds_stream_t stream) {
+  if (M <= 0 || M > 32 || N % 16 || K % (32 * ds::kGemvWarps) || !epi) return DS_EINVAL;
+  if (epi->swiglu && (y_f32 || accumulate || epi->ss_out)) return DS_EINVAL;
+  if (epi->ss_out && !y_f32) return DS_EINVAL;
+  if (epi->h_out && (!epi->ss_out || !epi->h_w)) return DS_EINVAL;
+  return ds::run(X, W, Y, M, N, K, y_f32, accumulate, *epi, (cudaStream_t)stream);
 }

@@ -99,15 +99,16 @@ __global__ void __launch_bounds__(BLOCK) rmsnorm_kernel(const void* __restrict__
   }
 }
 
-// out[r][j] = silu(gu[r][j]) * gu[r][F + j]
+// out[r][f] = silu(gate f) * up f; gate|up rows interleaved in 8-unit blocks
+// (ds_model.w_gate_up): 16-byte chunk j of the output reads chunks 2j, 2j+1
 __global__ void silu_mul_kernel(const uint4* __restrict__ gu, int chunks, uint4* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.y;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= chunks) return;
-  const uint4 g = __ldg(gu + static_cast<int64_t>(r) * 2 * chunks + j);
-  const uint4 u = __ldg(gu + static_cast<int64_t>(r) * 2 * chunks + chunks + j);
+  const uint4 g = __ldg(gu + static_cast<int64_t>(r) * 2 * chunks + 2 * j);
+  const uint4 u = __ldg(gu + static_cast<int64_t>(r) * 2 * chunks + 2 * j + 1);
   const __nv_bfloat162* pg = reinterpret_cast<const __nv_bfloat162*>(&g);
   const __nv_bfloat162* pu = reinterpret_cast<const __nv_bfloat162*>(&u);
   uint4 o;

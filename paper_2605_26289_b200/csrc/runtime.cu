@@ -71,6 +71,7 @@ struct Carve {
 struct Buffers {
   float* x;  // fp32 residual stream
   __nv_bfloat16 *h, *qkv, *attn, *gu, *act, *hf;
+  uint64_t* ss;  // 2 x 32: fixed-point row sums of squares (skinny GEMM epilogues)
   uint64_t* row_hash;
   void* attn_ws;
   size_t attn_ws_bytes;
@@ -83,6 +84,9 @@ size_t layout(const ds_model* m, int rows, int outs, Buffers* b, uint8_t* base) 
   const size_t QKV = static_cast<size_t>(m->n_heads + 2 * m->n_kv_heads) * m->head_dim;
   const size_t A = static_cast<size_t>(m->n_heads) * m->head_dim;
   Buffers t{};
+  // first, at a row-count-independent offset: the ss buffers' zero state
+  // carries over between calls with different batch sizes
+  t.ss = c.take<uint64_t>(2 * DS_SKINNY_SS_WORDS * 8);
   t.x = c.take<float>(rows * H * 4);
   t.h = c.take<__nv_bfloat16>(rows * H * 2);
   t.qkv = c.take<__nv_bfloat16>(rows * QKV * 2);
@@ -110,6 +114,9 @@ cublasStatus_t gemm(cublasHandle_t h, const void* X, const void* W, void* Y, int
 }  // namespace ds
 extern "C" int ds_gemm_skinny(const void* X, const void* W, void* Y, int M, int N, int K,
                               int y_f32, int accumulate, ds_stream_t stream);
+extern "C" int ds_gemm_skinny_ex(const void* X, const void* W, void* Y, int M, int N, int K,
+                                 int y_f32, int accumulate, const ds_skinny_epi* epi,
+                                 ds_stream_t stream);
 namespace ds {
 namespace {
 
@@ -250,11 +257,28 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
   const __nv_bfloat16* mn = static_cast<const __nv_bfloat16*>(m->mlp_norm);
   __nv_bfloat16* kp = static_cast<__nv_bfloat16*>(kv->k_pool);
   __nv_bfloat16* vp = static_cast<__nv_bfloat16*>(kv->v_pool);
+  // decode / verify row counts (T <= 32): the RMSNorms and the SwiGLU ride in
+  // the skinny GEMM epilogues - wo / down (residual producers) emit
+  // h = bf16(x * next norm weight) and per-CTA row sums of x^2, wqkv / gate_up
+  // scale their rows by the inverse RMS; gate_up emits silu(g)*u directly.
+  const bool fused = T <= 32 && H % 256 == 0 && F % 256 == 0 && (nh * hd) % 256 == 0 &&
+                     QKV % 16 == 0;
+  // two ss buffers, each producer clearing the one its consumer already read
+  // (wo clears ss_attn, read by this layer's wqkv; down clears ss_mlp)
+  uint64_t* ss_attn = b.ss;                       // down -> next wqkv
+  uint64_t* ss_mlp = b.ss + DS_SKINNY_SS_WORDS;  // wo -> gate_up
   for (int l = 0; l < L; ++l) {
-    DS_CHECK(ds_rmsnorm(b.x, 1, nullptr, T, H, an + static_cast<size_t>(l) * H, m->rms_eps, b.h,
-                        stream));
-    DS_CHECK(project(rt.blas, b.h, wqkv + static_cast<size_t>(l) * QKV * H, b.qkv, T, QKV, H,
-                     false, false, stream));
+    const __nv_bfloat16* wqkv_l = wqkv + static_cast<size_t>(l) * QKV * H;
+    if (fused && l > 0) {
+      ds_skinny_epi e{};
+      e.row_ss = ss_attn;
+      e.eps = m->rms_eps;
+      DS_CHECK(ds_gemm_skinny_ex(b.h, wqkv_l, b.qkv, T, QKV, H, 0, 0, &e, stream));
+    } else {
+      DS_CHECK(ds_rmsnorm(b.x, 1, nullptr, T, H, an + static_cast<size_t>(l) * H, m->rms_eps, b.h,
+                          stream));
+      DS_CHECK(project(rt.blas, b.h, wqkv_l, b.qkv, T, QKV, H, false, false, stream));
+    }
     DS_CHECK(ds_rope_kv_store(b.qkv, T, a->row_seq, a->row_pos, kv->pos2cell, kv->pos_stride, nh,
                               nkv, hd, m->rope_cos, m->rope_sin, kp + l * kv_layer,
                               vp + l * kv_layer, kv->capacity, stream));
@@ -272,15 +296,37 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
                             kv->pos_stride, nh, nkv, hd, scale, b.attn, b.attn_ws,
                             b.attn_ws_bytes, attn_impl, stream));
     }
-    DS_CHECK(project(rt.blas, b.attn, wo + static_cast<size_t>(l) * H * nh * hd, b.x, T, H,
-                     nh * hd, true, true, stream));
-    DS_CHECK(ds_rmsnorm(b.x, 1, nullptr, T, H, mn + static_cast<size_t>(l) * H, m->rms_eps, b.h,
-                        stream));
-    DS_CHECK(project(rt.blas, b.h, wgu + static_cast<size_t>(l) * 2 * F * H, b.gu, T, 2 * F, H,
-                     false, false, stream));
-    DS_CHECK(ds_silu_mul(b.gu, T, F, b.act, stream));
-    DS_CHECK(project(rt.blas, b.act, wd + static_cast<size_t>(l) * H * F, b.x, T, H, F, true,
-                     true, stream));
+    const __nv_bfloat16* wo_l = wo + static_cast<size_t>(l) * H * nh * hd;
+    const __nv_bfloat16* wgu_l = wgu + static_cast<size_t>(l) * 2 * F * H;
+    const __nv_bfloat16* wd_l = wd + static_cast<size_t>(l) * H * F;
+    if (fused) {
+      ds_skinny_epi eo{};
+      eo.ss_out = ss_mlp;
+      eo.ss_zero = ss_attn;
+      eo.h_out = b.h;
+      eo.h_w = mn + static_cast<size_t>(l) * H;
+      DS_CHECK(ds_gemm_skinny_ex(b.attn, wo_l, b.x, T, H, nh * hd, 1, 1, &eo, stream));
+      ds_skinny_epi eg{};
+      eg.row_ss = ss_mlp;
+      eg.eps = m->rms_eps;
+      eg.swiglu = 1;
+      DS_CHECK(ds_gemm_skinny_ex(b.h, wgu_l, b.act, T, 2 * F, H, 0, 0, &eg, stream));
+      ds_skinny_epi ed{};
+      ed.ss_out = ss_attn;  // (last layer: unused, keeps the clear/fill cycle uniform)
+      ed.ss_zero = ss_mlp;
+      if (l + 1 < L) {
+        ed.h_out = b.h;
+        ed.h_w = an + static_cast<size_t>(l + 1) * H;
+      }
+      DS_CHECK(ds_gemm_skinny_ex(b.act, wd_l, b.x, T, H, F, 1, 1, &ed, stream));
+    } else {
+      DS_CHECK(project(rt.blas, b.attn, wo_l, b.x, T, H, nh * hd, true, true, stream));
+      DS_CHECK(ds_rmsnorm(b.x, 1, nullptr, T, H, mn + static_cast<size_t>(l) * H, m->rms_eps,
+                          b.h, stream));
+      DS_CHECK(project(rt.blas, b.h, wgu_l, b.gu, T, 2 * F, H, false, false, stream));
+      DS_CHECK(ds_silu_mul(b.gu, T, F, b.act, stream));
+      DS_CHECK(project(rt.blas, b.act, wd_l, b.x, T, H, F, true, true, stream));
+    }
   }
   // final norm on sampled rows only, LM head in fp32
   DS_CHECK(ds_rmsnorm(b.x, 1, a->out_rows, a->n_out, H, m->final_norm, m->rms_eps, b.hf, stream));

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 import torch
 
-from oracle.llama_ref import paged_attention, rope_tables
+from oracle.llama_ref import paged_attention, rope_tables, split_gate_up
 
 pytestmark = pytest.mark.gpu
 
@@ -41,7 +41,8 @@ def test_rmsnorm_silu_embed_argmax(cuda):
     act = torch.empty(5, 2816, device=cuda, dtype=torch.bfloat16)
     check(L.ds_silu_mul(gu.data_ptr(), 5, 2816, act.data_ptr(), s))
     gf = gu.float()
-    ref = torch.nn.functional.silu(gf[:, :2816]) * gf[:, 2816:]
+    gt, up = split_gate_up(gf, 2816)
+    ref = torch.nn.functional.silu(gt) * up
     assert torch.allclose(act.float(), _bf(ref).float(), atol=1e-2, rtol=1e-2)
     table = torch.randn(100, 1024, device=cuda, generator=g).bfloat16()
     tok = torch.tensor([5, 99, 0], dtype=torch.int32, device=cuda)
@@ -179,3 +180,54 @@ def test_gemm_skinny_vs_fp32(cuda, M, N, K, y_f32, acc):
         ref = ref + (Y0 if y_f32 else Y0.bfloat16().float())
     err = (Y.float() - ref).abs().max().item()
     assert err < (1e-3 if y_f32 else 1e-2 * ref.abs().max().item()), err
+
+
+@pytest.mark.parametrize("M", [1, 5, 13, 20, 32])
+def test_gemm_skinny_epilogue_fusions(cuda, M):
+    """ds_gemm_skinny_ex: residual producer (y += X.W^T, h = bf16(y*w_norm),
+    per-CTA partial sums of y^2) feeding a norm consumer (row scale
+    rsqrt(mean(y^2)+eps)) and a SwiGLU consumer (8-row interleaved gate|up) -
+    against the unfused RMSNorm -> GEMM -> SiLU*up chain in fp32 with the
+    unfused path's bf16 storage points."""
+    from paper_2605_26289_b200._lib import SkinnyEpi, check, lib
+
+    L = lib()
+    s = torch.cuda.current_stream().cuda_stream
+    H, F, Kin = 2048, 1024, 1024
+    g = torch.Generator(device=cuda).manual_seed(M)
+    Xin = torch.randn(M, Kin, device=cuda, generator=g).bfloat16()
+    Wo = (0.05 * torch.randn(H, Kin, device=cuda, generator=g)).bfloat16()
+    x0 = torch.randn(M, H, device=cuda, generator=g)
+    nw = (1 + 0.1 * torch.randn(H, device=cuda, generator=g)).bfloat16()
+    Wgu = (0.02 * torch.randn(2 * F, H, device=cuda, generator=g)).bfloat16()
+    x = x0.clone()
+    h = torch.empty(M, H, device=cuda, dtype=torch.bfloat16)
+    ss = torch.zeros(32, device=cuda, dtype=torch.int64)
+    other = torch.full((32,), 7, device=cuda, dtype=torch.int64)
+    prod = SkinnyEpi(ss_out=ss.data_ptr(), ss_zero=other.data_ptr(), h_out=h.data_ptr(),
+                     h_w=nw.data_ptr())
+    check(L.ds_gemm_skinny_ex(Xin.data_ptr(), Wo.data_ptr(), x.data_ptr(), M, H, Kin, 1, 1,
+                              ctypes.byref(prod), s))
+    act = torch.empty(M, F, device=cuda, dtype=torch.bfloat16)
+    cons = SkinnyEpi(row_ss=ss.data_ptr(), eps=1e-5, swiglu=1)
+    check(L.ds_gemm_skinny_ex(h.data_ptr(), Wgu.data_ptr(), act.data_ptr(), M, 2 * F, H, 0, 0,
+                              ctypes.byref(cons), s))
+    q = torch.empty(M, 512, device=cuda, dtype=torch.bfloat16)
+    cons2 = SkinnyEpi(row_ss=ss.data_ptr(), eps=1e-5)
+    check(L.ds_gemm_skinny_ex(h.data_ptr(), Wgu[:512].contiguous().data_ptr(), q.data_ptr(), M,
+                              512, H, 0, 0, ctypes.byref(cons2), s))
+    torch.cuda.synchronize()
+    x_ref = x0 + Xin.float() @ Wo.float().T
+    assert (x - x_ref).abs().max().item() < 1e-3
+    assert torch.allclose(h.float(), _bf(x * nw.float()).float(), atol=0, rtol=0)
+    assert torch.allclose(ss[:M].double() / 2**24, (x * x).sum(-1).double(), rtol=1e-5)
+    assert other.eq(0).all()
+    hn = _bf(x_ref * torch.rsqrt((x_ref * x_ref).mean(-1, keepdim=True) + 1e-5) * nw.float())
+    gu = _bf(hn.float() @ Wgu.float().T).float()
+    gt, up = split_gate_up(gu, F)
+    a_ref = torch.nn.functional.silu(gt) * up
+    err = (act.float() - a_ref).abs().max().item()
+    assert err < 2e-2 * a_ref.abs().max().item(), err
+    q_ref = hn.float() @ Wgu[:512].float().T
+    err = (q.float() - q_ref).abs().max().item()
+    assert err < 2e-2 * q_ref.abs().max().item(), err
