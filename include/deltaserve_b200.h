@@ -125,7 +125,10 @@ typedef struct {
   float rms_eps;
   const void* embed;      /* bf16 [vocab][hidden] */
   const void* attn_norm;  /* bf16 [L][hidden] */
-  const void* wqkv;       /* bf16 [L][(nh+2nkv)*hd][hidden] */
+  const void* wqkv;       /* bf16 [L][(nh+2nkv)*hd][hidden]; inside each q and k head
+                           * the rows are RoPE-pair interleaved (hd = 128): row
+                           * 16t+j is dim 8t+j (j<8) or 64+8t+j-8 (j>=8), so a
+                           * 16-row tile holds 8 rotation pairs; v rows in order */
   const void* wo;         /* bf16 [L][hidden][nh*hd] */
   const void* mlp_norm;   /* bf16 [L][hidden] */
   const void* w_gate_up;  /* bf16 [L][2*ffn][hidden]: 8-row blocks, gate units 8b..8b+7
@@ -193,9 +196,11 @@ int ds_model_forward(const ds_model* model, const ds_kv_store* kv, const ds_forw
  * Individual layer kernels (exported for parity tests and microbenchmarks).
  * ---------------------------------------------------------------------- */
 
-/* K5: RoPE (rotate-half, cos/sin table) on q (in place in qkv) and k; store k,v
- * rows into the layer's head-major cell pool ([kv_head][cell][head_dim],
- * kv_head_stride = cells per head) at pos2cell[row_seq][row_pos]. */
+/* K5: RoPE (rotate-half, cos/sin table) on q (in place in qkv, written back in
+ * plain dim order) and k; store k,v rows into the layer's head-major cell pool
+ * ([kv_head][cell][head_dim], kv_head_stride = cells per head) at
+ * pos2cell[row_seq][row_pos].  q/k head columns of qkv arrive in the wqkv
+ * RoPE-pair interleaved order (ds_model); head_dim 128. */
 int ds_rope_kv_store(void* qkv, int n_rows, const int32_t* row_seq, const int32_t* row_pos,
                      const int32_t* pos2cell, int64_t pos_stride, int n_heads, int n_kv_heads,
                      int head_dim, const float* rope_cos, const float* rope_sin, void* k_pool_l,
@@ -241,7 +246,12 @@ int ds_gemm_skinny(const void* X, const void* W, void* Y, int M, int N, int K, i
  *  row_ss/eps: norm consumer - row m of the product is scaled by
  *      rsqrt(row_ss[m] * 2^-24 / K + eps) (X holds bf16(x * norm_w)).
  *  swiglu: W rows are gate/up interleaved in 8-row blocks (see ds_model);
- *      Y = bf16 silu(gate) * up [M][N/2]. */
+ *      Y = bf16 silu(gate) * up [M][N/2].
+ *  rope: W = wqkv (pair-interleaved q/k rows, see ds_model; head_dim 128):
+ *      q heads are rotated into Y [M][N] (plain dim order, k/v columns of Y
+ *      untouched), k heads rotated and v copied into the layer's head-major
+ *      pools at cell pos2cell[row_seq[m]][row_pos[m]] - the K5 kernel folded
+ *      into the projection. */
 #define DS_SKINNY_SS_WORDS 32
 typedef struct {
   const uint64_t* row_ss;
@@ -251,6 +261,17 @@ typedef struct {
   void* h_out;
   const void* h_w;
   int32_t swiglu;
+  int32_t rope;
+  int32_t n_heads, n_kv_heads;
+  const int32_t* row_seq;
+  const int32_t* row_pos;
+  const int32_t* pos2cell;
+  int64_t pos_stride;
+  const float* rope_cos; /* f32 [max_pos][64] */
+  const float* rope_sin;
+  void* k_pool_l;
+  void* v_pool_l;
+  int64_t kv_head_stride;
 } ds_skinny_epi;
 
 int ds_gemm_skinny_ex(const void* X, const void* W, void* Y, int M, int N, int K, int y_f32,

@@ -16,6 +16,22 @@ import torch
 
 
 
+
+def qk_perm(d: int = 128) -> torch.Tensor:
+    """perm[c] = head dim stored at column c of a q/k head in the wqkv layout
+    (RoPE-pair interleaved, include/deltaserve_b200.h ds_model.wqkv)."""
+    c = torch.arange(d)
+    t, j = c // 16, c % 16
+    return torch.where(j < 8, 8 * t + j, d // 2 + 8 * t + j - 8)
+
+
+def unpermute_qk(qkv: torch.Tensor, nh: int, nkv: int, d: int) -> torch.Tensor:
+    """qkv columns in wqkv order -> plain dim order for the q and k heads."""
+    inv = torch.argsort(qk_perm(d))
+    T = qkv.shape[0]
+    qk = qkv[:, : (nh + nkv) * d].reshape(T, nh + nkv, d)[:, :, inv].reshape(T, -1)
+    return torch.cat([qk, qkv[:, (nh + nkv) * d:]], dim=1)
+
 def split_gate_up(gu, ffn: int):
     """gate, up from a gate|up projection whose weight rows are interleaved in
     8-unit blocks (row 16b+j: j<8 gate unit 8b+j, else up unit 8b+j-8) - the
@@ -64,7 +80,7 @@ def forward(w: dict, shape, tokens: list[int], out_rows: list[int] | None = None
     scale = 1.0 / (d ** 0.5)
     for l in range(shape.layers):
         h = rmsnorm(x, w["attn_norm"][l], shape.rms_eps)
-        qkv = _bf(h @ w["wqkv"][l].T)
+        qkv = unpermute_qk(_bf(h @ w["wqkv"][l].T), nh, nkv, d)
         q = qkv[:, : nh * d].view(T, nh, d)
         k = qkv[:, nh * d: (nh + nkv) * d].view(T, nkv, d)
         v = qkv[:, (nh + nkv) * d:].view(T, nkv, d)

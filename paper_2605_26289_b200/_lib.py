@@ -54,7 +54,11 @@ POLICY_COPY, POLICY_ARGMAX = 0, 1
 class SkinnyEpi(ctypes.Structure):
     """ds_skinny_epi: epilogue fusions of ds_gemm_skinny_ex."""
     _fields_ = [("row_ss", c_vp), ("eps", c_f32), ("ss_out", c_vp), ("ss_zero", c_vp),
-                ("h_out", c_vp), ("h_w", c_vp), ("swiglu", c_i32)]
+                ("h_out", c_vp), ("h_w", c_vp), ("swiglu", c_i32), ("rope", c_i32),
+                ("n_heads", c_i32), ("n_kv_heads", c_i32), ("row_seq", c_vp), ("row_pos", c_vp),
+                ("pos2cell", c_vp), ("pos_stride", c_i64), ("rope_cos", c_vp),
+                ("rope_sin", c_vp), ("k_pool_l", c_vp), ("v_pool_l", c_vp),
+                ("kv_head_stride", c_i64)]
 
 
 class ForwardArgs(ctypes.Structure):

@@ -26,7 +26,10 @@
 //  * SwiGLU (gate_up with 8-row interleaved weights): feature rows g / g+8 of
 //    the CTA are gate / up of the same FFN unit, so the thread holding both
 //    writes act = bf16(silu(g) * u) directly (half the output bytes, no
-//    separate kernel).
+//    separate kernel);
+//  * RoPE + KV store (wqkv with RoPE-pair interleaved q/k rows): rows g / g+8
+//    are dims i / i+64 of one head, so the thread holding both rotates them;
+//    q goes to Y, k and v straight into the paged pools (the K5 kernel).
 #include "../../include/deltaserve_b200.h"
 #include "common.cuh"
 
@@ -55,6 +58,60 @@ DS_DEVICE uint4 ldg_pred(const void* p, bool on) {
 
 DS_DEVICE float bf16r(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
 
+// RoPE + KV store epilogue (head_dim 128; see the header comment)
+template <int MT>
+DS_DEVICE void rope_epilogue(const float (*red)[MT][4][32], const float* s_inv, const int* s_pos,
+                             const int64_t* s_cell, const ds_skinny_epi& epi, void* Y, int M,
+                             int N, int n0) {
+  constexpr int kHd = 128, kHalf = 64;
+  const int qk_width = (epi.n_heads + epi.n_kv_heads) * kHd;
+  __nv_bfloat16* kp = static_cast<__nv_bfloat16*>(epi.k_pool_l);
+  __nv_bfloat16* vp = static_cast<__nv_bfloat16*>(epi.v_pool_l);
+  if (n0 < qk_width) {
+    const int head = n0 / kHd, t = (n0 % kHd) / 16;
+    for (int idx = threadIdx.x; idx < MT * 2 * 32; idx += kGemvWarps * 32) {
+      const int mt = idx / 64, q = (idx / 32) & 1, ln = idx & 31;
+      const int m = mt * 8 + 2 * (ln & 3) + q;
+      if (m >= M) continue;
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int w = 0; w < kGemvWarps; ++w) {
+        s1 += red[w][mt][q][ln];
+        s2 += red[w][mt][q + 2][ln];
+      }
+      if (epi.row_ss) {
+        s1 *= s_inv[m];
+        s2 *= s_inv[m];
+      }
+      const float x1 = bf16r(s1), x2 = bf16r(s2);  // the unfused path stores qkv in bf16
+      const int i = 8 * t + (ln >> 2);
+      const int64_t tp = static_cast<int64_t>(s_pos[m]) * kHalf + i;
+      const float c = __ldg(epi.rope_cos + tp), sn = __ldg(epi.rope_sin + tp);
+      const __nv_bfloat16 y1 = __float2bfloat16_rn(x1 * c - x2 * sn);
+      const __nv_bfloat16 y2 = __float2bfloat16_rn(x2 * c + x1 * sn);
+      __nv_bfloat16* dst;
+      if (head < epi.n_heads)
+        dst = static_cast<__nv_bfloat16*>(Y) + static_cast<int64_t>(m) * N + head * kHd;
+      else
+        dst = kp + ((head - epi.n_heads) * epi.kv_head_stride + s_cell[m]) * kHd;
+      dst[i] = y1;
+      dst[i + kHalf] = y2;
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < MT * 4 * 32; idx += kGemvWarps * 32) {
+      const int mt = idx / 128, q = (idx / 32) & 3, ln = idx & 31;
+      const int m = mt * 8 + 2 * (ln & 3) + (q & 1);
+      if (m >= M) continue;
+      const int f = n0 - qk_width + (ln >> 2) + ((q & 2) ? 8 : 0);
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < kGemvWarps; ++w) s += red[w][mt][q][ln];
+      if (epi.row_ss) s *= s_inv[m];
+      vp[((f / kHd) * epi.kv_head_stride + s_cell[m]) * kHd + f % kHd] = __float2bfloat16_rn(s);
+    }
+  }
+}
+
 template <int MT, int U>
 __global__ void __launch_bounds__(kGemvWarps * 32) gemm_skinny_kernel(
     const __nv_bfloat16* __restrict__ X, const __nv_bfloat16* __restrict__ W, void* __restrict__ Y,
@@ -62,6 +119,8 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemm_skinny_kernel(
   __shared__ float red[kGemvWarps][MT][4][32];
   __shared__ float s_inv[32];
   __shared__ float s_sq[32][17];
+  __shared__ int s_pos[32];
+  __shared__ int64_t s_cell[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int n0 = blockIdx.x * 16;
@@ -99,6 +158,12 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemm_skinny_kernel(
   // norm consumer: the producer's row sum of squares, needed only in the epilogue
   const unsigned long long row_sum =
       epi.row_ss && threadIdx.x < M ? __ldcg(reinterpret_cast<const unsigned long long*>(epi.row_ss) + threadIdx.x) : 0ull;
+  // RoPE/KV store: row positions and sequences (the cell lookup waits for the epilogue)
+  int r_pos = 0, r_seq = 0;
+  if (epi.rope && threadIdx.x < M) {
+    r_pos = __ldg(epi.row_pos + threadIdx.x);
+    r_seq = __ldg(epi.row_seq + threadIdx.x);
+  }
 
   for (int kc = 0; kc < kslice; kc += 32 * U) {
     if (kc) {
@@ -137,7 +202,15 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemm_skinny_kernel(
   if (epi.row_ss && threadIdx.x < M)
     s_inv[threadIdx.x] =
         rsqrtf(__ull2float_rn(row_sum) / (kSsScale * static_cast<float>(K)) + epi.eps);
+  if (epi.rope && threadIdx.x < M) {
+    s_pos[threadIdx.x] = r_pos;
+    s_cell[threadIdx.x] = __ldg(epi.pos2cell + static_cast<int64_t>(r_seq) * epi.pos_stride + r_pos);
+  }
   __syncthreads();
+  if (epi.rope) {
+    rope_epilogue<MT>(red, s_inv, s_pos, s_cell, epi, Y, M, N, n0);
+    return;
+  }
   // accumulator element (mt, q, ln): c0,c1 = (feature g, tokens 2t, 2t+1);
   // c2,c3 = (feature g+8, same tokens)
   if (epi.swiglu) {
@@ -240,6 +313,11 @@ extern "C" int ds_gemm_skinny_ex(const void* X, const void* W, void* Y, int M, i
                                  ds_stream_t stream) {
   if (M <= 0 || M > 32 || N % 16 || K % (32 * ds::kGemvWarps) || !epi) return DS_EINVAL;
   if (epi->swiglu && (y_f32 || accumulate || epi->ss_out)) return DS_EINVAL;
+  if (epi->rope && (y_f32 || accumulate || epi->ss_out || epi->swiglu || epi->n_kv_heads <= 0 ||
+                    N != (epi->n_heads + 2 * epi->n_kv_heads) * 128 || !epi->row_seq ||
+                    !epi->row_pos || !epi->pos2cell || !epi->rope_cos || !epi->rope_sin ||
+                    !epi->k_pool_l || !epi->v_pool_l))
+    return DS_EINVAL;
   if (epi->ss_out && !y_f32) return DS_EINVAL;
   if (epi->h_out && (!epi->ss_out || !epi->h_w)) return DS_EINVAL;
   return ds::run(X, W, Y, M, N, K, y_f32, accumulate, *epi, (cudaStream_t)stream);

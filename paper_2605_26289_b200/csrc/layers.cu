@@ -124,8 +124,16 @@ __global__ void silu_mul_kernel(const uint4* __restrict__ gu, int chunks, uint4*
   out[static_cast<int64_t>(r) * chunks + j] = o;
 }
 
-// K5: rotate-half RoPE on q (in place) and k, store k and v rows into the
-// cell pool (layout [cell][kv_head][head_dim]).  One CTA per batch row.
+// K5: rotate-half RoPE on q (in place, written back in plain dim order) and k,
+// store k and v rows into the head-major cell pool.  q/k head columns arrive
+// RoPE-pair interleaved (ds_model.wqkv: column 16t+j = dim 8t+j or 64+8t+j-8),
+// so the row's q/k part is staged in smem before the in-place rewrite.  One
+// CTA per batch row.  (The decode forward folds this into the wqkv epilogue.)
+DS_DEVICE int qk_col(int dim) {  // column of head dim `dim` (hd = 128)
+  const int hi = dim >= 64, i = dim - 64 * hi;
+  return 16 * (i >> 3) + 8 * hi + (i & 7);
+}
+
 __global__ void rope_kv_store_kernel(__nv_bfloat16* __restrict__ qkv, const int32_t* row_seq,
                                      const int32_t* row_pos, const int32_t* __restrict__ pos2cell,
                                      int64_t pos_stride, int nh, int nkv, int hd,
@@ -133,6 +141,7 @@ __global__ void rope_kv_store_kernel(__nv_bfloat16* __restrict__ qkv, const int3
                                      const float* __restrict__ rope_sin,
                                      __nv_bfloat16* __restrict__ k_pool,
                                      __nv_bfloat16* __restrict__ v_pool, int64_t head_stride) {
+  extern __shared__ __align__(16) __nv_bfloat16 stage[];  // [(nh + nkv) * hd]
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.x;
@@ -141,18 +150,23 @@ __global__ void rope_kv_store_kernel(__nv_bfloat16* __restrict__ qkv, const int3
   const int half = hd / 2;
   const int width = (nh + 2 * nkv) * hd;
   __nv_bfloat16* row = qkv + static_cast<int64_t>(r) * width;
+  const int qk_chunks = (nh + nkv) * hd / 8;
+  for (int j = threadIdx.x; j < qk_chunks; j += blockDim.x)
+    reinterpret_cast<uint4*>(stage)[j] = reinterpret_cast<const uint4*>(row)[j];
+  __syncthreads();
   const float* cs = rope_cos + static_cast<int64_t>(pos) * half;
   const float* sn = rope_sin + static_cast<int64_t>(pos) * half;
   const int n_pairs = (nh + nkv) * half;
   for (int idx = threadIdx.x; idx < n_pairs; idx += blockDim.x) {
     const int head = idx / half;
     const int i = idx - head * half;
-    __nv_bfloat16* x = row + head * hd;
-    const float x1 = __bfloat162float(x[i]);
-    const float x2 = __bfloat162float(x[i + half]);
+    const __nv_bfloat16* xs = stage + head * hd;
+    const float x1 = __bfloat162float(xs[qk_col(i)]);
+    const float x2 = __bfloat162float(xs[qk_col(i + half)]);
     const float c = __ldg(cs + i), s = __ldg(sn + i);
     const __nv_bfloat16 y1 = __float2bfloat16_rn(x1 * c - x2 * s);
     const __nv_bfloat16 y2 = __float2bfloat16_rn(x2 * c + x1 * s);
+    __nv_bfloat16* x = row + head * hd;
     x[i] = y1;
     x[i + half] = y2;
     if (head >= nh) {
@@ -207,9 +221,11 @@ int ds_rope_kv_store(void* qkv, int n_rows, const int32_t* row_seq, const int32_
                      const int32_t* pos2cell, int64_t pos_stride, int n_heads, int n_kv_heads,
                      int head_dim, const float* rope_cos, const float* rope_sin, void* k_pool_l,
                      void* v_pool_l, int64_t kv_head_stride, ds_stream_t stream) {
-  if (n_rows < 0 || head_dim % 16) return DS_EINVAL;
+  if (n_rows < 0 || head_dim != 128) return DS_EINVAL;
   if (n_rows == 0) return DS_OK;
-  ds::launch_pdl(ds::rope_kv_store_kernel, dim3(n_rows), dim3(256), 0, (cudaStream_t)stream,
+  const int smem = (n_heads + n_kv_heads) * head_dim * 2;
+  if (smem > 48 * 1024) return DS_EUNSUPPORTED;
+  ds::launch_pdl(ds::rope_kv_store_kernel, dim3(n_rows), dim3(256), smem, (cudaStream_t)stream,
                  static_cast<__nv_bfloat16*>(qkv), row_seq, row_pos, pos2cell, pos_stride, n_heads,
                  n_kv_heads, head_dim, rope_cos, rope_sin, static_cast<__nv_bfloat16*>(k_pool_l),
                  static_cast<__nv_bfloat16*>(v_pool_l), kv_head_stride);

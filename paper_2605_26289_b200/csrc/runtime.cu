@@ -262,26 +262,42 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
   // h = bf16(x * next norm weight) and per-CTA row sums of x^2, wqkv / gate_up
   // scale their rows by the inverse RMS; gate_up emits silu(g)*u directly.
   const bool fused = T <= 32 && H % 256 == 0 && F % 256 == 0 && (nh * hd) % 256 == 0 &&
-                     QKV % 16 == 0;
+                     QKV % 16 == 0 && hd == 128;
   // two ss buffers, each producer clearing the one its consumer already read
   // (wo clears ss_attn, read by this layer's wqkv; down clears ss_mlp)
   uint64_t* ss_attn = b.ss;                       // down -> next wqkv
   uint64_t* ss_mlp = b.ss + DS_SKINNY_SS_WORDS;  // wo -> gate_up
   for (int l = 0; l < L; ++l) {
     const __nv_bfloat16* wqkv_l = wqkv + static_cast<size_t>(l) * QKV * H;
-    if (fused && l > 0) {
+    if (fused) {  // norm (row scale) + projection + RoPE + KV store in one launch
       ds_skinny_epi e{};
-      e.row_ss = ss_attn;
-      e.eps = m->rms_eps;
+      if (l > 0) {
+        e.row_ss = ss_attn;
+        e.eps = m->rms_eps;
+      } else {
+        DS_CHECK(ds_rmsnorm(b.x, 1, nullptr, T, H, an, m->rms_eps, b.h, stream));
+      }
+      e.rope = 1;
+      e.n_heads = nh;
+      e.n_kv_heads = nkv;
+      e.row_seq = a->row_seq;
+      e.row_pos = a->row_pos;
+      e.pos2cell = kv->pos2cell;
+      e.pos_stride = kv->pos_stride;
+      e.rope_cos = m->rope_cos;
+      e.rope_sin = m->rope_sin;
+      e.k_pool_l = kp + l * kv_layer;
+      e.v_pool_l = vp + l * kv_layer;
+      e.kv_head_stride = kv->capacity;
       DS_CHECK(ds_gemm_skinny_ex(b.h, wqkv_l, b.qkv, T, QKV, H, 0, 0, &e, stream));
     } else {
       DS_CHECK(ds_rmsnorm(b.x, 1, nullptr, T, H, an + static_cast<size_t>(l) * H, m->rms_eps, b.h,
                           stream));
       DS_CHECK(project(rt.blas, b.h, wqkv_l, b.qkv, T, QKV, H, false, false, stream));
+      DS_CHECK(ds_rope_kv_store(b.qkv, T, a->row_seq, a->row_pos, kv->pos2cell, kv->pos_stride,
+                                nh, nkv, hd, m->rope_cos, m->rope_sin, kp + l * kv_layer,
+                                vp + l * kv_layer, kv->capacity, stream));
     }
-    DS_CHECK(ds_rope_kv_store(b.qkv, T, a->row_seq, a->row_pos, kv->pos2cell, kv->pos_stride, nh,
-                              nkv, hd, m->rope_cos, m->rope_sin, kp + l * kv_layer,
-                              vp + l * kv_layer, kv->capacity, stream));
     if (n_long > 0 && n_long < a->n_entries) {  // mixed plan: K6 for prefill chunks, K7 rest
       DS_CHECK(ds_attention(b.qkv, a->entries_host, a->entries, n_long, T, kp + l * kv_layer,
                             vp + l * kv_layer, kv->capacity, kv->pos2cell, kv->pos_stride, nh,

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 import torch
 
-from oracle.llama_ref import paged_attention, rope_tables, split_gate_up
+from oracle.llama_ref import paged_attention, qk_perm, rope_tables, split_gate_up, unpermute_qk
 
 pytestmark = pytest.mark.gpu
 
@@ -135,13 +135,18 @@ def test_rope_kv_store(cuda):
     cos, sin = rope_tables(64, d, 500000.0)
     g = torch.Generator(device="cpu").manual_seed(2)
     qkv = torch.randn(T, (nh + 2 * nkv) * d, generator=g).bfloat16()
+    # the kernel takes q/k heads in the wqkv (RoPE-pair interleaved) column order
+    perm = qk_perm(d)
+    qkv_in = qkv.clone()
+    qk = qkv_in[:, : (nh + nkv) * d].view(T, nh + nkv, d)
+    qk[:] = qkv[:, : (nh + nkv) * d].view(T, nh + nkv, d)[:, :, perm]
     row_seq = torch.full((T,), 1, dtype=torch.int32)
     row_pos = torch.arange(10, 10 + T, dtype=torch.int32)
     pos2cell = torch.zeros(2, 64, dtype=torch.int32)
     pos2cell[1, 10:16] = torch.tensor([40, 3, 17, 8, 9, 60], dtype=torch.int32)
     kp = torch.zeros(nkv, 64, d, dtype=torch.bfloat16, device=cuda)
     vp = torch.zeros_like(kp)
-    qd = qkv.to(cuda)
+    qd = qkv_in.to(cuda)
     keep = [t.to(cuda) for t in (row_seq, row_pos, pos2cell, cos, sin)]  # keep alive
     rs, rp, p2c, cd, sd = keep
     check(lib().ds_rope_kv_store(qd.data_ptr(), T, rs.data_ptr(), rp.data_ptr(), p2c.data_ptr(),
@@ -231,3 +236,59 @@ def test_gemm_skinny_epilogue_fusions(cuda, M):
     q_ref = hn.float() @ Wgu[:512].float().T
     err = (q.float() - q_ref).abs().max().item()
     assert err < 2e-2 * q_ref.abs().max().item(), err
+
+
+@pytest.mark.parametrize("M", [1, 5, 17, 32])
+@pytest.mark.parametrize("norm", [False, True])
+def test_gemm_skinny_rope_kv_epilogue(cuda, M, norm):
+    """ds_gemm_skinny_ex rope mode (wqkv projection + RoPE + KV store, the
+    decode forward's K5 fusion) vs torch: qkv = bf16(X.W^T) in the wqkv
+    RoPE-pair interleaved layout, un-permuted, rotated, q to Y, k/v into the
+    head-major pools at pos2cell cells."""
+    from paper_2605_26289_b200._lib import SkinnyEpi, check, lib
+
+    nh, nkv, d, H = 8, 2, 128, 1024
+    QKV = (nh + 2 * nkv) * d
+    g = torch.Generator(device="cpu").manual_seed(M + 100 * norm)
+    X = torch.randn(M, H, generator=g).bfloat16()
+    W = (0.05 * torch.randn(QKV, H, generator=g)).bfloat16()
+    cos, sin = rope_tables(4096, d, 500000.0)
+    row_seq = torch.randint(0, 3, (M,), generator=g, dtype=torch.int32)
+    row_pos = torch.randint(0, 4096, (M,), generator=g, dtype=torch.int32)
+    cells = torch.randperm(256, generator=g)[:M].to(torch.int32)
+    pos2cell = torch.zeros(3, 4096, dtype=torch.int32)
+    pos2cell[row_seq.long(), row_pos.long()] = cells
+    head_stride = 256
+    kp = torch.zeros(nkv, head_stride, d, dtype=torch.bfloat16, device=cuda)
+    vp = torch.zeros_like(kp)
+    Y = torch.zeros(M, QKV, dtype=torch.bfloat16, device=cuda)
+    dev = [t.to(cuda) for t in (X, W, cos, sin, row_seq, row_pos, pos2cell)]
+    Xd, Wd, cd, sd, rsd, rpd, p2cd = dev
+    ss = torch.zeros(32, dtype=torch.int64, device=cuda)
+    scale = torch.ones(M)
+    if norm:  # consumer row scale: X holds bf16(x * w); row sums of x^2 given
+        x = torch.randn(M, H, generator=g) * 2
+        fixed = ((x * x).double().sum(-1) * 2**24).round().long()
+        ss.copy_(torch.nn.functional.pad(fixed, (0, 32 - M)).to(cuda))
+        scale = torch.rsqrt((x * x).sum(-1) / H + 1e-5)
+    epi = SkinnyEpi(row_ss=ss.data_ptr() if norm else None, eps=1e-5, rope=1, n_heads=nh,
+                    n_kv_heads=nkv, row_seq=rsd.data_ptr(), row_pos=rpd.data_ptr(),
+                    pos2cell=p2cd.data_ptr(), pos_stride=4096, rope_cos=cd.data_ptr(),
+                    rope_sin=sd.data_ptr(), k_pool_l=kp.data_ptr(), v_pool_l=vp.data_ptr(),
+                    kv_head_stride=head_stride)
+    check(lib().ds_gemm_skinny_ex(Xd.data_ptr(), Wd.data_ptr(), Y.data_ptr(), M, QKV, H, 0, 0,
+                                  ctypes.byref(epi), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    qkv = unpermute_qk(_bf((X.float() @ W.float().T) * scale[:, None]), nh, nkv, d).float()
+    from oracle.llama_ref import rope
+
+    c, s_ = cos[row_pos.long()], sin[row_pos.long()]
+    q = rope(qkv[:, : nh * d].view(M, nh, d), c, s_)
+    k = rope(qkv[:, nh * d:(nh + nkv) * d].view(M, nkv, d), c, s_)
+    v = qkv[:, (nh + nkv) * d:].view(M, nkv, d)
+    # fp32 accumulation order + FMA contraction: a bf16 ulp or two
+    tol = dict(atol=2e-2, rtol=2e-2)
+    assert torch.allclose(Y.cpu().float()[:, : nh * d].view(M, nh, d), q, **tol)
+    cl = cells.long()
+    assert torch.allclose(kp.cpu().float()[:, cl].transpose(0, 1), k, **tol)
+    assert torch.allclose(vp.cpu().float()[:, cl].transpose(0, 1), v, **tol)

@@ -33,3 +33,27 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
 print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25, max_name_column_width=70))
 st = eng.forward_stats()
 print(st)
+
+# critical-path attribution: with PDL a kernel launches early and waits, so its
+# duration overstates its cost; the gap between consecutive kernel END times on
+# the main stream is what each kernel adds to the forward.
+import json, tempfile
+from collections import defaultdict
+tr = os.path.join(tempfile.mkdtemp(), "t.json")
+prof.export_chrome_trace(tr)
+ev = [e for e in json.load(open(tr))["traceEvents"] if e.get("cat") == "kernel"]
+streams = defaultdict(list)
+for e in ev:
+    streams[e["args"].get("stream")].append(e)
+main = max(streams.values(), key=len)
+main.sort(key=lambda e: e["ts"] + e["dur"])
+inc = defaultdict(float)
+cnt = defaultdict(int)
+for a, b in zip(main, main[1:]):
+    name = b["name"].split("(")[0].split("<")[0][:60]
+    inc[name] += (b["ts"] + b["dur"]) - (a["ts"] + a["dur"])
+    cnt[name] += 1
+tot = sum(inc.values())
+print(f"\ncritical-path increments over {len(main)} kernels ({tot / 5:.1f} us per forward):")
+for k, v in sorted(inc.items(), key=lambda kv: -kv[1]):
+    print(f"  {k:60s} {cnt[k] // 5:5d}/fwd {v / 5:9.1f} us/fwd {v / cnt[k]:7.2f} us each {v / tot * 100:5.1f}%")
