@@ -17,7 +17,13 @@
 //     stage through an "empty" mbarrier.  Two consumer warps per scheduler
 //     hide the HMMA/LDSM latency chains a single warp could not.
 // The 128-byte swizzle keeps ldmatrix bank-conflict free.  The 4 warp states
-// merge through smem; split partials (O, lse) go to attn_combine_kernel.
+// merge through smem; split partials (O, lse) go to attn_combine_kernel (an
+// in-kernel last-CTA merge was measured slower: its serial L2 round trips
+// outlast the combine launch, which PDL already overlaps).
+// Programmatic dependent launch: only q and the K/V rows of this batch's own
+// positions (>= past) come from the preceding wqkv projection, so the
+// producer streams every tile of older keys before the dependency wait - the
+// KV read overlaps the projection's tail; consumers wait before loading q.
 #include "../../include/deltaserve_b200.h"
 #include "attn_plan.h"
 #include "common.cuh"
@@ -64,8 +70,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
   uint8_t* qs = smem + kStages * kStageBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(qs + kQRows * kD * 2);
   uint64_t* empty = full + kStages;
-  pdl_wait();
-  pdl_trigger();
 
   const int e = blockIdx.z / max_splits;
   const int split = blockIdx.z - e * max_splits;
@@ -88,20 +92,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     }
     mbar_fence_init();
   }
-  if (warp < kConsumers) {  // Q rows -> smem (swizzled, zero padded to 32 rows)
-    for (int c = tid; c < kQRows * 16; c += kConsumers * 32) {
-      const int r = c >> 4, chunk = c & 15;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (r < R) {
-        const int ti = r / G, gi = r - ti * G;
-        v = *reinterpret_cast<const uint4*>(qkv +
-                                            static_cast<int64_t>(en.q_start + ti) * qkv_stride +
-                                            (kh * G + gi) * kD + chunk * 8);
-      }
-      *reinterpret_cast<uint4*>(qs + qswz(r, chunk)) = v;
-    }
-  }
-  __syncthreads();
+  __syncthreads();  // barriers initialised
 
   const int32_t* p2c = pos2cell + static_cast<int64_t>(en.seq) * pos_stride;
   if (warp == kConsumers) {
@@ -122,6 +113,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     int c_lo, c_hi, n1_lo, n1_hi, n2_lo, n2_hi;
     cells(0, c_lo, c_hi);
     cells(1, n1_lo, n1_hi);
+    bool waited = false;
     for (int it = 0; it < ntiles; ++it) {
       cells(it + 2, n2_lo, n2_hi);
       const int st = it % kStages;
@@ -130,6 +122,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
       uint8_t* vs = ks + kHalfBytes;
       const int kt = k_begin + it * kTile;
       const int nvalid = min(kTile, k_end - kt);
+      if (!waited && kt + nvalid > en.past) {  // first tile holding this batch's own K/V
+        pdl_wait();
+        waited = true;
+      }
       const int c0 = __shfl_sync(0xffffffffu, c_lo, 0);
       const bool run = __all_sync(0xffffffffu, (lane >= nvalid || c_lo == c0 + lane) &&
                                                     (lane + 32 >= nvalid || c_hi == c0 + 32 + lane));
@@ -163,10 +159,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
       c_lo = n1_lo; c_hi = n1_hi;
       n1_lo = n2_lo; n1_hi = n2_hi;
     }
+    if (!waited) pdl_wait();
+    pdl_trigger();
     return;
   }
 
   // ================= consumers =================
+  pdl_wait();  // q comes from the preceding projection
+  pdl_trigger();
+  {  // Q rows -> smem (swizzled, zero padded to 32 rows)
+    for (int c = tid; c < kQRows * 16; c += kConsumers * 32) {
+      const int r = c >> 4, chunk = c & 15;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (r < R) {
+        const int ti = r / G, gi = r - ti * G;
+        v = *reinterpret_cast<const uint4*>(qkv +
+                                            static_cast<int64_t>(en.q_start + ti) * qkv_stride +
+                                            (kh * G + gi) * kD + chunk * 8);
+      }
+      *reinterpret_cast<uint4*>(qs + qswz(r, chunk)) = v;
+    }
+  }
+  named_bar_sync(1, kConsumers * 32);  // q staged
   const int g8 = lane >> 2, t4 = lane & 3, mi = lane >> 3;
   const int kg = warp & (kKeyGroups - 1), dh = warp / kKeyGroups;
   int qpos[MT][2];

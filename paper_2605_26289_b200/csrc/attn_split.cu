@@ -313,10 +313,11 @@ int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_en
   }
   const int mode = max_R <= 32 ? 1 : 0;  // warp-specialised decode kernel vs split kernel
   int max_splits = 1;
-  bool any_split = false;
+  bool any_split = false;  // some entry needs the combine kernel
   for (int e = 0; e < n_entries; ++e) {
     const ds_entry& en = entries_host[e];
-    const int qb = (en.q_len * (nh / nkv) + kSplitNW * 16 - 1) / (kSplitNW * 16);
+    const int R = en.q_len * (nh / nkv);
+    const int qb = (R + kSplitNW * 16 - 1) / (kSplitNW * 16);
     const AttnSplitPlan p = attn_split_plan(qb, en.past + en.q_len, nkv, n_entries, mode);
     max_splits = p.n_splits > max_splits ? p.n_splits : max_splits;
     any_split |= p.n_splits > 1;

@@ -84,9 +84,12 @@ size_t layout(const ds_model* m, int rows, int outs, Buffers* b, uint8_t* base) 
   const size_t QKV = static_cast<size_t>(m->n_heads + 2 * m->n_kv_heads) * m->head_dim;
   const size_t A = static_cast<size_t>(m->n_heads) * m->head_dim;
   Buffers t{};
-  // first, at a row-count-independent offset: the ss buffers' zero state
-  // carries over between calls with different batch sizes
+  // first, at row-count-independent offsets: the ss buffers and the attention
+  // split-merge counters are zero between calls (self re-arming), which must
+  // hold whatever the previous call's batch size was
   t.ss = c.take<uint64_t>(2 * DS_SKINNY_SS_WORDS * 8);
+  t.attn_ws_bytes = attn_partial_bytes_bound();
+  t.attn_ws = c.take<uint8_t>(t.attn_ws_bytes);
   t.x = c.take<float>(rows * H * 4);
   t.h = c.take<__nv_bfloat16>(rows * H * 2);
   t.qkv = c.take<__nv_bfloat16>(rows * QKV * 2);
@@ -95,8 +98,6 @@ size_t layout(const ds_model* m, int rows, int outs, Buffers* b, uint8_t* base) 
   t.act = c.take<__nv_bfloat16>(rows * F * 2);
   t.hf = c.take<__nv_bfloat16>(static_cast<size_t>(outs) * H * 2);
   t.row_hash = c.take<uint64_t>(static_cast<size_t>(outs) * 8);
-  t.attn_ws_bytes = attn_partial_bytes_bound();
-  t.attn_ws = c.take<uint8_t>(t.attn_ws_bytes);
   t.blas_ws = c.take<uint8_t>(kCublasWs);
   if (b) *b = t;
   return c.off;

@@ -92,6 +92,14 @@ def test_attention_paged_vs_fp32(cuda, past, q_len, contiguous):
     _attention_case(cuda, past, q_len, contiguous, impl=1)
 
 
+@pytest.mark.parametrize("past,q_len", [(300, 1), (301, 1), (302, 5), (64, 1), (127, 1)])
+@pytest.mark.parametrize("contiguous", [False, True])
+def test_attention_small_gqa(cuda, past, q_len, contiguous):
+    """The tiny model's head shape (8 q / 2 kv heads): few CTAs, so short
+    contexts still split and merge inline."""
+    _attention_case(cuda, past, q_len, contiguous, impl=1, nh=8, nkv=2)
+
+
 @pytest.mark.parametrize("past,q_len", [(0, 32), (0, 150), (100, 33), (2048, 300), (3000, 881),
                                         (127, 129), (5, 1)])
 @pytest.mark.parametrize("contiguous", [False, True])
@@ -99,12 +107,12 @@ def test_attention_tcgen05_prefill_vs_fp32(cuda, past, q_len, contiguous):
     _attention_case(cuda, past, q_len, contiguous, impl=2)
 
 
-def _attention_case(cuda, past, q_len, contiguous, impl):
+def _attention_case(cuda, past, q_len, contiguous, impl, nh=32, nkv=8):
     from paper_2605_26289_b200._lib import check, lib
 
-    nh, nkv, d = 32, 8, 128
+    d = 128
     kv_len = past + q_len
-    k_pool, v_pool, pos2cell, cells, k_cpu, v_cpu, cap = _setup_paged(cuda, kv_len,
+    k_pool, v_pool, pos2cell, cells, k_cpu, v_cpu, cap = _setup_paged(cuda, kv_len, nkv=nkv,
                                                                      seed=past + q_len,
                                                                      contiguous=contiguous)
     g = torch.Generator(device="cpu").manual_seed(1)
@@ -115,17 +123,20 @@ def _attention_case(cuda, past, q_len, contiguous, impl):
     ws_bytes = lib().ds_attention_workspace_bytes(q_len, 1, nh, d)
     ws = torch.zeros(ws_bytes, dtype=torch.uint8, device=cuda)
     qkv_d = qkv.to(cuda)
-    check(lib().ds_attention(qkv_d.data_ptr(), ctypes.addressof(ent), ent_dev.data_ptr(), 1,
-                             q_len, k_pool.data_ptr(), v_pool.data_ptr(), cap,
-                             pos2cell.data_ptr(), pos2cell.shape[1], nh, nkv, d, 1.0 / d ** 0.5, out.data_ptr(),
-                             ws.data_ptr(), ws_bytes, impl, torch.cuda.current_stream().cuda_stream))
-    torch.cuda.synchronize()
     q = qkv[:, : nh * d].view(q_len, nh, d)
     ref = paged_attention(q, k_cpu[:, cells.long()].transpose(0, 1), v_cpu[:, cells.long()].transpose(0, 1),
                           list(range(past, kv_len)), kv_len, 1.0 / d ** 0.5)
-    got = out.cpu().float().view(q_len, nh, d)
-    err = (got - ref).abs().max().item()
-    assert err < 2e-2, err
+    for _ in range(3):  # repeated launches: split-merge arrival counters must re-arm
+        out.zero_()
+        check(lib().ds_attention(qkv_d.data_ptr(), ctypes.addressof(ent), ent_dev.data_ptr(), 1,
+                                 q_len, k_pool.data_ptr(), v_pool.data_ptr(), cap,
+                                 pos2cell.data_ptr(), pos2cell.shape[1], nh, nkv, d, 1.0 / d ** 0.5,
+                                 out.data_ptr(), ws.data_ptr(), ws_bytes, impl,
+                                 torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        got = out.cpu().float().view(q_len, nh, d)
+        err = (got - ref).abs().max().item()
+        assert err < 2e-2, err
 
 
 def test_rope_kv_store(cuda):
