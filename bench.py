@@ -208,7 +208,10 @@ WORKLOAD_DESC = {
 
 def kernel_micro(torch, dev, peaks) -> dict:
     """K7 / K6 at the BASELINE reference points (8B shape, one layer), timed
-    with CUDA events on the launching stream; roofline vs measured peaks."""
+    with CUDA events on the launching stream over 20 back-to-back launches
+    (each including its split merge), alternating between two copies of the
+    K/V pool so no launch finds the previous one's K/V in L2 (2 x 134 MB >
+    126 MB L2); roofline vs measured peaks."""
     import ctypes
 
     from paper_2605_26289_b200 import _lib
@@ -218,15 +221,15 @@ def kernel_micro(torch, dev, peaks) -> dict:
     L = _lib.lib()
     out = {}
     stream = torch.cuda.current_stream()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for name, past, q, impl in (("K7_verify_m32k_q5", 32768, 5, 1),
                                 ("K7_decode_m32k_q1", 32768, 1, 1),
                                 ("K6_prefill_d881_m31489", 31489, 881, 0)):
         kv_len = past + q
         cap = kv_len + 64
         g = torch.Generator(device=dev).manual_seed(7)
-        kp = torch.randn(nkv, cap, d, device=dev, dtype=torch.bfloat16, generator=g)
-        vp = torch.randn(nkv, cap, d, device=dev, dtype=torch.bfloat16, generator=g)
+        pools = [(torch.randn(nkv, cap, d, device=dev, dtype=torch.bfloat16, generator=g),
+                  torch.randn(nkv, cap, d, device=dev, dtype=torch.bfloat16, generator=g))
+                 for _ in range(2)]
         p2c = torch.arange(cap, dtype=torch.int32, device=dev).view(1, cap)
         qkv = torch.randn(q, (nh + 2 * nkv) * d, device=dev, dtype=torch.bfloat16, generator=g)
         o = torch.empty(q, nh * d, device=dev, dtype=torch.bfloat16)
@@ -235,29 +238,24 @@ def kernel_micro(torch, dev, peaks) -> dict:
         wsb = L.ds_attention_workspace_bytes(q, 1, nh, d)
         ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
 
-        def launch():
+        def launch(i):
+            kp, vp = pools[i & 1]
             _lib.check(L.ds_attention(qkv.data_ptr(), ctypes.addressof(ent), ent_d.data_ptr(), 1,
                                       q, kp.data_ptr(), vp.data_ptr(), cap, p2c.data_ptr(), cap, nh,
                                       nkv, d, 1.0 / d ** 0.5, o.data_ptr(), ws.data_ptr(), wsb,
                                       impl, stream.cuda_stream), name)
 
-        for _ in range(3):
-            launch()
+        for i in range(4):
+            launch(i)
         torch.cuda.synchronize()
-        # [L2 flush, event, launch, event] x 10 enqueued without host syncs: the
-        # events bracket only the attention launch on its stream, the flush keeps
-        # every launch cold (HBM), and the host stays ahead of the GPU
-        evs = []
-        for _ in range(10):
-            flush.zero_()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            launch()
-            b.record(stream)
-            evs.append((a, b))
-        torch.cuda.synchronize()
-        times = [a.elapsed_time(b) / 1000.0 for a, b in evs]
-        t = statistics.median(times)
+        reps = 20
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(reps):
+            launch(i)
+        b.record(stream)
+        b.synchronize()
+        t = a.elapsed_time(b) / 1000.0 / reps
         bytes_ = nkv * 2 * d * 2 * kv_len + 2 * q * nh * d * 2  # K+V once + q in + o out
         flops = 4.0 * nh * d * q * (past + (q + 1) / 2)
         if name.startswith("K7"):
@@ -269,7 +267,7 @@ def kernel_micro(torch, dev, peaks) -> dict:
                          "achieved": round(flops / t / 1e12, 1), "peak": tf_burst,
                          "unit": "TFLOP/s", "frac": round(flops / t / 1e12 / tf_burst, 3),
                          "algo_flops": flops}
-        del kp, vp, qkv, o, ws
+        del pools, qkv, o, ws
     return out
 
 

@@ -1,29 +1,38 @@
-// K7 (decode / speculative verify, R = q_len * G <= 32 packed query rows).
+// K7 (decode / speculative verify, R = q_len * G <= 24 packed query rows).
 //
 // HBM-bound: every K/V byte of a split is read once and feeds all R rows (GQA
 // packing: row r = t*G + g, so the G query heads sharing a KV head share its
-// tiles).  Warp-specialised, one CTA per SM:
-//   * producer warp: per 64-key tile, when the tile's cells form one run
+// tiles).  With so few query rows the MMAs run "swapped": keys are the M side
+// of m16n8k16 and the packed query rows the N side (n-tiles of 8 rows), so no
+// MMA lane is spent on padding rows beyond 8*ceil(R/8):
+//   S^T[key][row]  = K[key][:] . Q^T           (A = K tile via ldmatrix,
+//                                               B = q rows, held in registers
+//                                               for R <= 16, else ldmatrix'd
+//                                               from a swizzled smem copy)
+//   O^T[d][row]   += V^T[d][key] . P^T[key][row] (A = V tile via ldmatrix.trans,
+//                                               B = P^T: the S^T accumulators
+//                                               packed to bf16 and transposed
+//                                               in registers with movmatrix)
+// Warp-specialised, one CTA per SM (9 warps: at most 168 registers per
+// thread, since a sub-partition holds three of them):
+//   * producer warp: per 128-key tile, when the tile's cells form one run
 //     (the common case - first-fit allocation, head-major pool) four 2D TMA
 //     boxes (K and V, two 128-byte column halves, SWIZZLE_128B) complete on the
 //     stage's mbarrier; otherwise the warp gathers the tile cell by cell with
-//     16-byte cp.async into the same swizzled layout.  6-stage ring, up to 5
-//     tiles (~160 KB) in flight per SM;
-//   * 8 consumer warps = 4 key groups x 2 head-dim halves: warp (kg, dh) owns
-//     16 keys of every tile and output columns [64*dh, 64*dh+64); QK^T (computed
-//     by both halves of a pair - cheap next to the latency it hides) and PV on
-//     mma.sync m16n8k16 (bf16 in, fp32 accumulate), online softmax with quad
-//     shuffles, lazy O rescale, masks only on boundary tiles; then release the
-//     stage through an "empty" mbarrier.  Two consumer warps per scheduler
-//     hide the HMMA/LDSM latency chains a single warp could not.
-// The 128-byte swizzle keeps ldmatrix bank-conflict free.  The 4 warp states
-// merge through smem; split partials (O, lse) go to attn_combine_kernel (an
-// in-kernel last-CTA merge was measured slower: its serial L2 round trips
-// outlast the combine launch, which PDL already overlaps).
+//     16-byte cp.async into the same swizzled layout.  3 stages x 64 KB;
+//   * 8 consumer warps: warp w owns keys [16w, 16w+16) of every tile and keeps
+//     its own online-softmax state (running max per row, lazily rescaled O^T);
+//     the 8 states merge through smem at the end.
 // Programmatic dependent launch: only q and the K/V rows of this batch's own
 // positions (>= past) come from the preceding wqkv projection, so the
 // producer streams every tile of older keys before the dependency wait - the
 // KV read overlaps the projection's tail; consumers wait before loading q.
+// Key splits: when a launch has at most kDecodeMaxCluster splits per (entry,
+// kv head), those CTAs form a thread-block cluster; each leaves its normalised
+// rows + log-sum-exp in shared memory and the cluster merges them through
+// distributed shared memory (no global partials, no combine launch - the
+// short-context case, where that fixed cost dominates).  Longer contexts write
+// split partials (O, lse) for attn_combine_kernel.
 #include "../../include/deltaserve_b200.h"
 #include "attn_plan.h"
 #include "common.cuh"
@@ -33,30 +42,55 @@ namespace ds {
 
 namespace {
 constexpr int kD = 128;
-constexpr int kTile = 64;
-constexpr int kHalfBytes = kTile * kD * 2;  // one K (or V) tile: 2 x [64 rows][128 B]
-constexpr int kStageBytes = 2 * kHalfBytes;
-constexpr int kStages = 6;
-constexpr int kQRows = 32;
-constexpr int kConsumers = 8;  // 4 key groups x 2 d halves
-constexpr int kKeyGroups = 4;
+constexpr int kTile = 128;                   // keys per stage
+constexpr int kBoxBytes = kTile * 128;       // [128 keys][64 d] bf16 = one TMA box
+constexpr int kHalfBytes = 2 * kBoxBytes;    // a K (or V) tile
+constexpr int kStageBytes = 2 * kHalfBytes;  // K + V = 64 KB
+constexpr int kStages = 3;
+constexpr int kConsumers = 8;
+constexpr int kKeysPerWarp = kTile / kConsumers;  // 16 = the MMA M side
 constexpr int kThreads = (kConsumers + 1) * 32;
+constexpr int kMaxRows = kDecodeMaxRows;  // NT <= 3; more rows go to K6
+constexpr int kQBytes = 32 * kD * 2;
 
+// TMA SWIZZLE_128B layout of a [128 keys][128 d] tile: two 64-column halves of
+// 128-byte rows; 16-byte chunk c of a row sits at c ^ (row & 7).
+DS_DEVICE int tswz(int row, int chunk16) {
+  return (chunk16 >> 3) * kBoxBytes + row * 128 + (((chunk16 & 7) ^ (row & 7)) << 4);
+}
+
+// swizzled [row][128 d] bf16 q copy: 16-byte chunk c of row r at c ^ (r & 7)
 DS_DEVICE int qswz(int row, int chunk) {
   return row * (kD * 2) + (((chunk & 8) | ((chunk & 7) ^ (row & 7))) << 4);
 }
-// TMA SWIZZLE_128B layout of a [64 rows][128 d] tile: two 64-column halves of
-// 128-byte rows; 16-byte chunk c of a row sits at c ^ (row & 7).
-DS_DEVICE int tswz(int row, int chunk16) {
-  return (chunk16 >> 3) * (kTile * 128) + row * 128 + (((chunk16 & 7) ^ (row & 7)) << 4);
+
+// transpose an 8x8 bf16 matrix held as one packed pair per lane
+DS_DEVICE uint32_t movm_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(y) : "r"(x));
+  return y;
+}
+// merge the 8 consumer warps' online-softmax states for (row r, column d):
+// returns the row max; L = sum of exp, acc = weighted O
+DS_DEVICE float merged_row(const float* msm, const float* lsm, const float* osm, int r, int d,
+                           float& L, float& acc) {
+  float mm = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < kConsumers; ++w) mm = fmaxf(mm, msm[w * kMaxRows + r]);
+  const float mref = mm == -INFINITY ? 0.f : mm;
+#pragma unroll
+  for (int w = 0; w < kConsumers; ++w) {
+    const float sc = fast_exp2(msm[w * kMaxRows + r] - mref);
+    L += lsm[w * kMaxRows + r] * sc;
+    acc += osm[(w * kMaxRows + r) * kD + d] * sc;
+  }
+  return mm;
 }
 }  // namespace
 
-int decode_smem_bytes() {
-  return 1024 + kStages * kStageBytes + kQRows * kD * 2 + 2 * kStages * 8;
-}
+int decode_smem_bytes() { return 1024 + kStages * kStageBytes + kQBytes + 2 * kStages * 8; }
 
-template <int MT>
+template <int NT>  // n-tiles of 8 packed query rows
 __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     const __nv_bfloat16* __restrict__ qkv, int qkv_stride, const ds_entry* __restrict__ entries,
     int n_entries, int max_splits, const __nv_bfloat16* __restrict__ kpool,
@@ -65,10 +99,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     float* __restrict__ part_o, float* __restrict__ part_lse, int64_t head_stride,
     int* __restrict__ counters, const __grid_constant__ CUtensorMap tmk,
     const __grid_constant__ CUtensorMap tmv) {
+  (void)counters;
+  const bool cluster_merge = max_splits <= kDecodeMaxCluster;  // launched with clusters
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // SW128 alignment
   uint8_t* qs = smem + kStages * kStageBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(qs + kQRows * kD * 2);
+  // split-merge buffers inside the ring, past the warp-merge area (used after both)
+  float* cval = reinterpret_cast<float*>(smem + 128 * 1024);  // [R][128] this split's rows
+  float* clse = cval + kMaxRows * kD;                          // [R]
+  float* cw = clse + kMaxRows;                                 // [R][16] split weights
+  uint64_t* full = reinterpret_cast<uint64_t*>(qs + kQBytes);
   uint64_t* empty = full + kStages;
 
   const int e = blockIdx.z / max_splits;
@@ -78,7 +118,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
   const int R = en.q_len * G;
   const int kv_len = en.past + en.q_len;
   const AttnSplitPlan plan = attn_split_plan(1, kv_len, nkv, n_entries, 1);
-  if (split >= plan.n_splits) return;
+  const bool active = split < plan.n_splits;  // idle CTAs still join the cluster merge
   const int kh = blockIdx.y;
   const int k_begin = split * plan.split_len;
   const int k_end = min(k_begin + plan.split_len, kv_len);
@@ -95,27 +135,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
   __syncthreads();  // barriers initialised
 
   const int32_t* p2c = pos2cell + static_cast<int64_t>(en.seq) * pos_stride;
-  if (warp == kConsumers) {
+  if (!active) {
+  } else if (warp == kConsumers) {
     // ================= producer =================
     if (lane == 0) {
       tma_prefetch_desc(&tmk);
       tma_prefetch_desc(&tmv);
     }
     const int64_t hrow = kh * head_stride;
-    // cell ids are prefetched two tiles ahead so their latency never stalls
-    // the TMA issue loop
-    auto cells = [&](int t, int& lo, int& hi) {
+    // cell ids (4 per lane per tile) are prefetched two tiles ahead so their
+    // latency never stalls the TMA issue loop
+    auto cells = [&](int t, int (&c)[4]) {
       const int kt = k_begin + t * kTile;
       const int nv = t < ntiles ? min(kTile, k_end - kt) : 0;
-      lo = lane < nv ? __ldg(p2c + kt + lane) : -1;
-      hi = lane + 32 < nv ? __ldg(p2c + kt + 32 + lane) : -1;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c[i] = lane + 32 * i < nv ? __ldg(p2c + kt + lane + 32 * i) : -1;
     };
-    int c_lo, c_hi, n1_lo, n1_hi, n2_lo, n2_hi;
-    cells(0, c_lo, c_hi);
-    cells(1, n1_lo, n1_hi);
+    int cur[4], nx1[4], nx2[4];
+    cells(0, cur);
+    cells(1, nx1);
     bool waited = false;
     for (int it = 0; it < ntiles; ++it) {
-      cells(it + 2, n2_lo, n2_hi);
+      cells(it + 2, nx2);
       const int st = it % kStages;
       if (it >= kStages) mbar_wait(&empty[st], ((it / kStages) - 1) & 1);
       uint8_t* ks = smem + st * kStageBytes;
@@ -126,24 +167,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
         pdl_wait();
         waited = true;
       }
-      const int c0 = __shfl_sync(0xffffffffu, c_lo, 0);
-      const bool run = __all_sync(0xffffffffu, (lane >= nvalid || c_lo == c0 + lane) &&
-                                                    (lane + 32 >= nvalid || c_hi == c0 + 32 + lane));
-      if (run) {  // one contiguous run of cells: 4 TMA boxes
+      const int c0 = __shfl_sync(0xffffffffu, cur[0], 0);
+      bool mine = true;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        mine &= lane + 32 * i >= nvalid || cur[i] == c0 + lane + 32 * i;
+      if (__all_sync(0xffffffffu, mine)) {  // one contiguous run of cells: 4 TMA boxes
         if (lane == 0) {
           mbar_expect_tx(&full[st], kStageBytes);
           const int row = static_cast<int>(hrow + c0);
           tma_load_2d(ks, &tmk, 0, row, &full[st]);
-          tma_load_2d(ks + kTile * 128, &tmk, 64, row, &full[st]);
+          tma_load_2d(ks + kBoxBytes, &tmk, 64, row, &full[st]);
           tma_load_2d(vs, &tmv, 0, row, &full[st]);
-          tma_load_2d(vs + kTile * 128, &tmv, 64, row, &full[st]);
+          tma_load_2d(vs + kBoxBytes, &tmv, 64, row, &full[st]);
         }
       } else {  // fragmented: cell-by-cell 16-byte gathers into the same layout
 #pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-          const int r = lane + 32 * h;
-          const int cv = h ? c_hi : c_lo;
-          const int cl = cv >= 0 ? cv : c0;  // tail rows duplicate a valid cell (masked)
+        for (int i = 0; i < 4; ++i) {
+          const int r = lane + 32 * i;
+          const int cl = cur[i] >= 0 ? cur[i] : c0;  // tail rows duplicate a valid cell (masked)
           const int64_t off = (hrow + cl) * kD;
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
@@ -156,192 +198,250 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[st]);
       }
-      c_lo = n1_lo; c_hi = n1_hi;
-      n1_lo = n2_lo; n1_hi = n2_hi;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        cur[i] = nx1[i];
+        nx1[i] = nx2[i];
+      }
     }
     if (!waited) pdl_wait();
-    pdl_trigger();
-    return;
-  }
-
-  // ================= consumers =================
-  pdl_wait();  // q comes from the preceding projection
-  pdl_trigger();
-  {  // Q rows -> smem (swizzled, zero padded to 32 rows)
-    for (int c = tid; c < kQRows * 16; c += kConsumers * 32) {
-      const int r = c >> 4, chunk = c & 15;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (r < R) {
-        const int ti = r / G, gi = r - ti * G;
-        v = *reinterpret_cast<const uint4*>(qkv +
-                                            static_cast<int64_t>(en.q_start + ti) * qkv_stride +
-                                            (kh * G + gi) * kD + chunk * 8);
+  } else {
+    // ================= consumers =================
+    pdl_wait();  // q comes from the preceding projection
+    const int g = lane >> 2, t = lane & 3;
+    // Q^T as the B operand: qb[j][kk] covers rows 8j + g, d [16kk + 2t, +1] and
+    // [16kk + 8 + 2t, +1] - registers for NT <= 2, else a swizzled smem copy
+    constexpr bool kQSmem = NT >= 3;
+    uint32_t qb[kQSmem ? 1 : NT][8][2];
+    int qpos[NT][2];  // absolute position of rows 8j + 2t + h (-1: padding row)
+    if constexpr (kQSmem) {
+      for (int c = tid; c < 8 * NT * 16; c += kConsumers * 32) {
+        const int r = c >> 4, chunk = c & 15;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (r < R)
+          v = *reinterpret_cast<const uint4*>(qkv +
+                                              static_cast<int64_t>(en.q_start + r / G) * qkv_stride +
+                                              (kh * G + r % G) * kD + chunk * 8);
+        *reinterpret_cast<uint4*>(qs + qswz(r, chunk)) = v;
       }
-      *reinterpret_cast<uint4*>(qs + qswz(r, chunk)) = v;
+      named_bar_sync(1, kConsumers * 32);
     }
-  }
-  named_bar_sync(1, kConsumers * 32);  // q staged
-  const int g8 = lane >> 2, t4 = lane & 3, mi = lane >> 3;
-  const int kg = warp & (kKeyGroups - 1), dh = warp / kKeyGroups;
-  int qpos[MT][2];
-  float o[MT][8][4];
-  float m_run[MT][2], l_run[MT][2];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = mt * 16 + g8 + 8 * h;
-      qpos[mt][h] = r < R ? en.past + r / G : -1;
-      m_run[mt][h] = -INFINITY;
-      l_run[mt][h] = 0.f;
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) o[mt][j][0] = o[mt][j][1] = o[mt][j][2] = o[mt][j][3] = 0.f;
-  }
-  const uint32_t qs_u = smem_u32(qs);
-  // per-lane ldmatrix rows inside a tile (keys of this warp's group)
-  const int k_row = kg * 16 + (mi >> 1) * 8 + (lane & 7);
-  const int v_row = kg * 16 + (mi & 1) * 8 + (lane & 7);
-
-  for (int it = 0; it < ntiles; ++it) {
-    const int st = it % kStages;
-    mbar_wait(&full[st], (it / kStages) & 1);
-    const uint32_t ks_u = smem_u32(smem + st * kStageBytes), vs_u = ks_u + kHalfBytes;
-    const int kt = k_begin + it * kTile + kg * 16;
-    float s[MT][2][4];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) s[mt][j][0] = s[mt][j][1] = s[mt][j][2] = s[mt][j][3] = 0.f;
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4(b0, b1, b2, b3, ks_u + tswz(k_row, 2 * kk + (mi & 1)));
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        uint32_t a[4];
-        ldsm_x4(a[0], a[1], a[2], a[3],
-                qs_u + qswz(mt * 16 + (lane & 7) + ((mi & 1) ? 8 : 0), 2 * kk + (mi >> 1)));
-        mma_bf16_16816(s[mt][0], a, b0, b1);
-        mma_bf16_16816(s[mt][1], a, b2, b3);
-      }
-    }
-    const bool need_mask = (kt + 16 > k_end) || (kt + 15 > en.past);
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      float mx[2] = {m_run[mt][0], m_run[mt][1]};
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float v = s[mt][j][q] * scale_log2;
-          if (need_mask) {
-            const int key = kt + j * 8 + 2 * t4 + (q & 1);
-            v = (key < k_end && key <= qpos[mt][q >> 1]) ? v : -INFINITY;
-          }
-          s[mt][j][q] = v;
-          mx[q >> 1] = fmaxf(mx[q >> 1], v);
+  #pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      if constexpr (!kQSmem) {
+        const int r = 8 * j + g;
+        const bool valid = r < R;
+        const int rr = valid ? r : 0;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(
+            qkv + static_cast<int64_t>(en.q_start + rr / G) * qkv_stride + (kh * G + rr % G) * kD);
+  #pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          qb[j][kk][0] = valid ? src[8 * kk + t] : 0u;
+          qb[j][kk][1] = valid ? src[8 * kk + 4 + t] : 0u;
         }
-      float alpha[2], mref[2];
-#pragma unroll
+      }
+  #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 1));
-        mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 2));
-        mref[h] = mx[h] == -INFINITY ? 0.f : mx[h];
-        alpha[h] = fast_exp2(m_run[mt][h] - mref[h]);
-        m_run[mt][h] = mx[h];
-        l_run[mt][h] *= alpha[h];
-      }
-      if (__any_sync(0xffffffffu, alpha[0] != 1.f || alpha[1] != 1.f)) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          o[mt][j][0] *= alpha[0];
-          o[mt][j][1] *= alpha[0];
-          o[mt][j][2] *= alpha[1];
-          o[mt][j][3] *= alpha[1];
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float p = fast_exp2(s[mt][j][q] - mref[q >> 1]);
-          s[mt][j][q] = p;
-          l_run[mt][q >> 1] += p;
-        }
-    }
-    uint32_t pa[MT][4];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      pa[mt][0] = pack_bf16(s[mt][0][0], s[mt][0][1]);
-      pa[mt][1] = pack_bf16(s[mt][0][2], s[mt][0][3]);
-      pa[mt][2] = pack_bf16(s[mt][1][0], s[mt][1][1]);
-      pa[mt][3] = pack_bf16(s[mt][1][2], s[mt][1][3]);
-    }
-#pragma unroll
-    for (int dn = 0; dn < 8; dn += 2) {
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(b0, b1, b2, b3, vs_u + tswz(v_row, dh * 8 + dn + (mi >> 1)));
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        mma_bf16_16816(o[mt][dn], pa[mt], b0, b1);
-        mma_bf16_16816(o[mt][dn + 1], pa[mt], b2, b3);
+        const int rh = 8 * j + 2 * t + h;
+        qpos[j][h] = rh < R ? en.past + rh / G : -1;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
-  }
-  named_bar_sync(1, kConsumers * 32);  // all consumers done with the ring
+    float o[8][NT][4];
+    float m_run[NT][2], l_run[NT][2];  // l_run: this lane's keys only (reduced at the end)
+  #pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      m_run[j][0] = m_run[j][1] = -INFINITY;
+      l_run[j][0] = l_run[j][1] = 0.f;
+  #pragma unroll
+      for (int i = 0; i < 8; ++i) o[i][j][0] = o[i][j][1] = o[i][j][2] = o[i][j][3] = 0.f;
+    }
+    const int kw = warp * kKeysPerWarp;
+    // per-lane ldmatrix rows: K (A, row-major) and V (A = V^T via .trans)
+    const int k_row = kw + (lane & 7) + ((lane >> 3) & 1) * 8, k_chunk = lane >> 4;
+    const int v_row = kw + (lane & 7) + ((lane >> 4) << 3), v_chunk = (lane >> 3) & 1;
 
-  // ---- merge the 4 key groups' states (ring memory is free now) ----
-  float* osm = reinterpret_cast<float*>(smem);  // [4][32][128]
-  float* msm = osm + kKeyGroups * kQRows * kD;  // [4][32]
-  float* lsm = msm + kKeyGroups * kQRows;       // [4][32]
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float l = l_run[mt][h];
-      l += __shfl_xor_sync(0xffffffffu, l, 1);
-      l += __shfl_xor_sync(0xffffffffu, l, 2);
-      const int r = mt * 16 + g8 + 8 * h;
-      if (t4 == 0 && dh == 0) {
-        msm[kg * kQRows + r] = m_run[mt][h];
-        lsm[kg * kQRows + r] = l;
+    for (int it = 0; it < ntiles; ++it) {
+      const int st = it % kStages;
+      mbar_wait(&full[st], (it / kStages) & 1);
+      const uint32_t ks_u = smem_u32(smem + st * kStageBytes), vs_u = ks_u + kHalfBytes;
+      float s[NT][4];
+  #pragma unroll
+      for (int j = 0; j < NT; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+  #pragma unroll
+      for (int kk = 0; kk < 8; kk += 2) {
+        uint32_t a0[4], a1[4];
+        ldsm_x4(a0[0], a0[1], a0[2], a0[3], ks_u + tswz(k_row, 2 * kk + k_chunk));
+        ldsm_x4(a1[0], a1[1], a1[2], a1[3], ks_u + tswz(k_row, 2 * kk + 2 + k_chunk));
+  #pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          uint32_t b[4];
+          if constexpr (kQSmem) {
+            ldsm_x4(b[0], b[1], b[2], b[3], smem_u32(qs) + qswz(8 * j + (lane & 7), 2 * kk + (lane >> 3)));
+          } else {
+            b[0] = qb[j][kk][0];
+            b[1] = qb[j][kk][1];
+            b[2] = qb[j][kk + 1][0];
+            b[3] = qb[j][kk + 1][1];
+          }
+          mma_bf16_16816(s[j], a0, b[0], b[1]);
+          mma_bf16_16816(s[j], a1, b[2], b[3]);
+        }
       }
-#pragma unroll
-      for (int dn = 0; dn < 8; ++dn)
-        *reinterpret_cast<float2*>(osm + (kg * kQRows + r) * kD + dh * 64 + dn * 8 + 2 * t4) =
-            make_float2(o[mt][dn][2 * h], o[mt][dn][2 * h + 1]);
+      // s[j][q]: key kt + g (+8 for q >= 2), row 8j + 2t + (q & 1)
+      const int kt = k_begin + it * kTile + kw;
+      const bool need_mask = (kt + kKeysPerWarp > k_end) || (kt + kKeysPerWarp - 1 > en.past);
+      uint32_t pb[NT][2];
+  #pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        float mx[2] = {m_run[j][0], m_run[j][1]};
+  #pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float v = s[j][q] * scale_log2;
+          if (need_mask) {
+            const int key = kt + g + ((q >> 1) << 3);
+            v = (key < k_end && key <= qpos[j][q & 1]) ? v : -INFINITY;
+          }
+          s[j][q] = v;
+          mx[q & 1] = fmaxf(mx[q & 1], v);
+        }
+        float alpha[2], mref[2];
+  #pragma unroll
+        for (int h = 0; h < 2; ++h) {  // row max over the warp's 16 keys (lanes sharing t)
+          mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 4));
+          mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 8));
+          mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 16));
+          mref[h] = mx[h] == -INFINITY ? 0.f : mx[h];
+          alpha[h] = fast_exp2(m_run[j][h] - mref[h]);
+          m_run[j][h] = mx[h];
+          l_run[j][h] *= alpha[h];
+        }
+        if (__any_sync(0xffffffffu, alpha[0] != 1.f || alpha[1] != 1.f)) {
+  #pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            o[i][j][0] *= alpha[0];
+            o[i][j][1] *= alpha[1];
+            o[i][j][2] *= alpha[0];
+            o[i][j][3] *= alpha[1];
+          }
+        }
+        float p[4];
+  #pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          p[q] = fast_exp2(s[j][q] - mref[q & 1]);
+          l_run[j][q & 1] += p[q];
+        }
+        // (keys g | g+8, rows 2t, 2t+1) -> transposed: (keys 2t, 2t+1 | +8, row g)
+        pb[j][0] = movm_t(pack_bf16(p[0], p[1]));
+        pb[j][1] = movm_t(pack_bf16(p[2], p[3]));
+      }
+  #pragma unroll
+      for (int i = 0; i < 8; ++i) {  // d rows [16i, 16i+16)
+        uint32_t a[4];
+        ldsm_x4_t(a[0], a[1], a[2], a[3], vs_u + tswz(v_row, 2 * i + v_chunk));
+  #pragma unroll
+        for (int j = 0; j < NT; ++j) mma_bf16_16816(o[i][j], a, pb[j][0], pb[j][1]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    named_bar_sync(1, kConsumers * 32);  // all consumers done with the ring
+
+    // ---- merge the 8 warps' states (ring memory is free now) ----
+    float* osm = reinterpret_cast<float*>(smem);     // [8][24][128]
+    float* msm = osm + kConsumers * kMaxRows * kD;   // [8][24]
+    float* lsm = msm + kConsumers * kMaxRows;        // [8][24]
+  #pragma unroll
+    for (int j = 0; j < NT; ++j) {
+  #pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float l = l_run[j][h];
+        l += __shfl_xor_sync(0xffffffffu, l, 4);
+        l += __shfl_xor_sync(0xffffffffu, l, 8);
+        l += __shfl_xor_sync(0xffffffffu, l, 16);
+        const int r = 8 * j + 2 * t + h;
+        if (g == 0) {
+          msm[warp * kMaxRows + r] = m_run[j][h];
+          lsm[warp * kMaxRows + r] = l;
+        }
+      }
+  #pragma unroll
+      for (int i = 0; i < 8; ++i)
+  #pragma unroll
+        for (int q = 0; q < 4; ++q)
+          osm[(warp * kMaxRows + 8 * j + 2 * t + (q & 1)) * kD + 16 * i + g + ((q >> 1) << 3)] =
+              o[i][j][q];
+    }
+    named_bar_sync(1, kConsumers * 32);
+    if (plan.n_splits == 1) {  // no split: write the rows directly
+      for (int idx = tid; idx < R * kD; idx += kConsumers * 32) {
+        const int r = idx / kD, d = idx - r * kD;
+        float L = 0.f, acc = 0.f;
+        merged_row(msm, lsm, osm, r, d, L, acc);
+        const int ti = r / G, gi = r - ti * G;
+        out[static_cast<int64_t>(en.q_start + ti) * nh * kD + (kh * G + gi) * kD + d] =
+            __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+      }
+    } else {  // this split's normalised rows and log-sum-exp
+      const int64_t base = attn_partial_base(entries, e, n_entries, nh, nkv, 1);
+      for (int idx = tid; idx < R * kD; idx += kConsumers * 32) {
+        const int r = idx / kD, d = idx - r * kD;
+        float L = 0.f, acc = 0.f;
+        const float mm = merged_row(msm, lsm, osm, r, d, L, acc);
+        const float val = L > 0.f ? acc / L : 0.f;
+        const float lse = L > 0.f ? mm + __log2f(L) : -INFINITY;
+        if (cluster_merge) {  // -> this CTA's cluster buffer
+          cval[r * kD + d] = val;
+          if (d == 0) clse[r] = lse;
+        } else {  // -> global partials for the combine kernel
+          const int64_t slot = (base + static_cast<int64_t>(split) * R + r) * nkv + kh;
+          part_o[slot * kD + d] = val;
+          if (d == 0) part_lse[slot] = lse;
+        }
+      }
     }
   }
-  named_bar_sync(1, kConsumers * 32);
-  const int64_t base =
-      plan.n_splits > 1 ? attn_partial_base(entries, e, n_entries, nh, nkv, 1) : 0;
-  for (int idx = tid; idx < R * kD; idx += kConsumers * 32) {
-    const int r = idx / kD, d = idx - r * kD;
-    float mm = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kKeyGroups; ++w) mm = fmaxf(mm, msm[w * kQRows + r]);
-    const float mref = mm == -INFINITY ? 0.f : mm;
-    float L = 0.f, acc = 0.f;
-#pragma unroll
-    for (int w = 0; w < kKeyGroups; ++w) {
-      const float sc = fast_exp2(msm[w * kQRows + r] - mref);
-      L += lsm[w * kQRows + r] * sc;
-      acc += osm[(w * kQRows + r) * kD + d] * sc;
+
+  // ---- split merge across the cluster (distributed shared memory) ----
+  if (cluster_merge && plan.n_splits > 1) {
+    cluster_sync_all();  // every split's rows are in its cbuf
+    const uint32_t rank = cluster_ctarank();
+    const int cs = max_splits;  // cluster size
+    if (tid < kConsumers * 32) {
+      // per-row split weights 2^(lse_p - max) / sum, in split order
+      for (int i = tid; i < R; i += kConsumers * 32) {
+        float lmax = -INFINITY;
+        for (int p = 0; p < plan.n_splits; ++p)
+          lmax = fmaxf(lmax, dsmem_ld_f32(dsmem_map(smem_u32(clse + i), p)));
+        float wsum = 0.f;
+        for (int p = 0; p < plan.n_splits; ++p) {
+          const float lse = dsmem_ld_f32(dsmem_map(smem_u32(clse + i), p));
+          const float w = lse == -INFINITY ? 0.f : exp2f(lse - lmax);
+          cw[i * kDecodeMaxCluster + p] = w;
+          wsum += w;
+        }
+        const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+        for (int p = 0; p < plan.n_splits; ++p) cw[i * kDecodeMaxCluster + p] *= inv;
+      }
+      named_bar_sync(1, kConsumers * 32);
+      for (int idx = static_cast<int>(rank) * kConsumers * 32 + tid; idx < R * kD;
+           idx += cs * kConsumers * 32) {
+        const int r = idx / kD, d = idx - r * kD;
+        const uint32_t a = smem_u32(cval + r * kD + d);
+        float acc = 0.f;
+#pragma unroll 4
+        for (int p = 0; p < plan.n_splits; ++p)
+          acc += cw[r * kDecodeMaxCluster + p] * dsmem_ld_f32(dsmem_map(a, p));
+        const int ti = r / G, gi = r - ti * G;
+        out[static_cast<int64_t>(en.q_start + ti) * nh * kD + (kh * G + gi) * kD + d] =
+            __float2bfloat16_rn(acc);
+      }
     }
-    const float val = L > 0.f ? acc / L : 0.f;
-    if (plan.n_splits == 1) {
-      const int ti = r / G, gi = r - ti * G;
-      out[static_cast<int64_t>(en.q_start + ti) * nh * kD + (kh * G + gi) * kD + d] =
-          __float2bfloat16_rn(val);
-    } else {
-      const int64_t slot = (base + static_cast<int64_t>(split) * R + r) * nkv + kh;
-      part_o[slot * kD + d] = val;
-      if (d == 0) part_lse[slot] = L > 0.f ? mm + __log2f(L) : -INFINITY;
-    }
+    cluster_sync_all();  // peers keep their smem until every read is done
   }
+  // PDL: the dependent projection launches only as this grid retires.  Any
+  // earlier trigger (even after the main loop) lets its CTAs onto the SMs
+  // while the attention runs, and the whole forward was measured ~25% slower.
+  pdl_trigger();
 }
 
 int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_entry* entries_dev,
@@ -350,11 +450,13 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
                        int max_splits, float scale, void* out, float* part_o, float* part_lse,
                        int* counters, cudaStream_t stream) {
   (void)entries_host;
+  if (max_R > kMaxRows) return DS_EUNSUPPORTED;
   const int smem = decode_smem_bytes();
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_decode_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attn_decode_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_decode_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   const CUtensorMap* tk = kv_tensor_map(k_pool, static_cast<int64_t>(nkv) * head_stride, kTile);
@@ -363,12 +465,23 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
   dim3 grid(1, nkv, n_entries * max_splits);
   const float sl2 = scale * 1.4426950408889634f;
   const int stride = (nh + 2 * nkv) * kD;
-  auto kern = max_R <= 16 ? attn_decode_kernel<1> : attn_decode_kernel<2>;
-  launch_pdl(kern, grid, dim3(kThreads), smem, stream, static_cast<const __nv_bfloat16*>(qkv),
-             stride, entries_dev, n_entries, max_splits,
-             static_cast<const __nv_bfloat16*>(k_pool), static_cast<const __nv_bfloat16*>(v_pool),
-             pos2cell, pos_stride, nh, nkv, sl2, static_cast<__nv_bfloat16*>(out), part_o,
-             part_lse, head_stride, counters, *tk, *tv);
+  auto kern = max_R <= 8 ? attn_decode_kernel<1>
+              : max_R <= 16 ? attn_decode_kernel<2>
+                            : attn_decode_kernel<3>;
+  if (max_splits <= kDecodeMaxCluster)
+    launch_pdl_cluster_z(kern, grid, dim3(kThreads), smem, max_splits, stream,
+                         static_cast<const __nv_bfloat16*>(qkv), stride, entries_dev, n_entries,
+                         max_splits, static_cast<const __nv_bfloat16*>(k_pool),
+                         static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv,
+                         sl2, static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride,
+                         counters, *tk, *tv);
+  else
+    launch_pdl(kern, grid, dim3(kThreads), smem, stream, static_cast<const __nv_bfloat16*>(qkv),
+               stride, entries_dev, n_entries, max_splits,
+               static_cast<const __nv_bfloat16*>(k_pool),
+               static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv, sl2,
+               static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride, counters, *tk,
+               *tv);
   return (int)cudaGetLastError();
 }
 

@@ -15,6 +15,15 @@
 namespace ds {
 
 constexpr int kNumSMs = 148;
+// packed query rows (q_len * G) the decode kernel K7 takes; longer entries run
+// on the tcgen05 kernel K6 (mirrored by DECODE_MAX_ROWS in engine.py)
+constexpr int kDecodeMaxRows = 24;
+// K7's key splits of one (entry, kv head) merge inside one thread-block
+// cluster (distributed shared memory) when there are at most this many; more
+// splits (long contexts: one CTA per SM) write global partials and a combine
+// kernel merges them.  A cluster must fit one GPC, so 8 (portable) - larger
+// clusters were measured to serialise on GPCs with fewer free SMs.
+constexpr int kDecodeMaxCluster = 8;
 constexpr int kSplitRows = 64;  // packed rows per split-kernel CTA (4 warps x 16)
 
 struct AttnSplitPlan {
@@ -31,8 +40,8 @@ DS_HD AttnSplitPlan attn_split_plan(int qblocks, int kv_len, int nkv, int n_entr
   if (n > by_len) n = by_len;
   if (n > 64) n = 64;
   if (n < 1) n = 1;
-  int split_len = ((kv_len + n - 1) / n + 63) / 64 * 64;
-  if (split_len < 64) split_len = 64;
+  const int gran = mode ? 128 : 64;  // key tile of the kernel
+  int split_len = ((kv_len + n - 1) / n + gran - 1) / gran * gran;
   n = (kv_len + split_len - 1) / split_len;
   if (n < 1) n = 1;
   return {n, split_len};

@@ -311,7 +311,7 @@ int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_en
     const int qb = (R + kSplitNW * 16 - 1) / (kSplitNW * 16);
     max_qblocks = qb > max_qblocks ? qb : max_qblocks;
   }
-  const int mode = max_R <= 32 ? 1 : 0;  // warp-specialised decode kernel vs split kernel
+  const int mode = max_R <= kDecodeMaxRows ? 1 : 0;  // warp-specialised decode kernel vs split kernel
   int max_splits = 1;
   bool any_split = false;  // some entry needs the combine kernel
   for (int e = 0; e < n_entries; ++e) {
@@ -337,7 +337,9 @@ int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_en
     const int rc = launch_attn_decode(qkv, entries_host, entries_dev, n_entries, k_pool, v_pool,
                                       head_stride, pos2cell, pos_stride, nh, nkv, max_R,
                                       max_splits, scale, out, part_o, part_lse, counters, stream);
-    if (rc != 0 || !any_split) return rc;
+    // K7 merges up to kDecodeMaxCluster key splits in-cluster; more go through
+    // global partials and the combine kernel
+    if (rc != 0 || !any_split || max_splits <= kDecodeMaxCluster) return rc;
     dim3 cgrid(max_R, nkv, n_entries);
     launch_pdl(attn_combine_kernel, cgrid, dim3(kD), 0, stream, entries_dev, n_entries, nh, nkv,
                kSplitNW * 16, 1, (const float*)part_o, (const float*)part_lse,

@@ -191,8 +191,8 @@ int ds_attention(const void* qkv, const ds_entry* entries_host, const ds_entry* 
   if (n_entries <= 0 || n_kv_heads <= 0 || n_heads % n_kv_heads) return DS_EINVAL;
   int max_q = 0;
   for (int e = 0; e < n_entries; ++e) max_q = entries_host[e].q_len > max_q ? entries_host[e].q_len : max_q;
-  // auto: decode / verify rows (R <= 32) -> K7; delta prefill -> tcgen05 K6
-  if (impl == 0) impl = max_q * (n_heads / n_kv_heads) > 32 ? 2 : 1;
+  // auto: decode / verify rows (R <= kDecodeMaxRows) -> K7; delta prefill -> tcgen05 K6
+  if (impl == 0) impl = max_q * (n_heads / n_kv_heads) > kDecodeMaxRows ? 2 : 1;
   if (impl == 2)
     return launch_attn_prefill_sm100(qkv, entries_host, entries_dev, n_entries, k_pool_l, v_pool_l,
                                      kv_head_stride, pos2cell, pos_stride, n_heads, n_kv_heads,
@@ -229,11 +229,12 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
   for (int e = 0; e < a->n_entries; ++e)
     max_q = a->entries_host[e].q_len > max_q ? a->entries_host[e].q_len : max_q;
   const int attn_impl = 0;  // auto
-  // entries ordered long (q*G > 32: tcgen05 K6) first, then short (K7)
+  // entries ordered long (q*G > kDecodeMaxRows: tcgen05 K6) first, then short (K7)
   int n_long = 0;
-  while (n_long < a->n_entries && a->entries_host[n_long].q_len * (nh / nkv) > 32) ++n_long;
+  while (n_long < a->n_entries && a->entries_host[n_long].q_len * (nh / nkv) > kDecodeMaxRows)
+    ++n_long;
   for (int e = n_long; e < a->n_entries; ++e)
-    if (a->entries_host[e].q_len * (nh / nkv) > 32) n_long = 0;  // unsorted: auto dispatch
+    if (a->entries_host[e].q_len * (nh / nkv) > kDecodeMaxRows) n_long = 0;  // unsorted: auto
 
   DS_BLAS(cublasSetStream(rt.blas, stream));
   DS_BLAS(cublasSetWorkspace(rt.blas, b.blas_ws, kCublasWs));

@@ -38,6 +38,11 @@ _ENTRY_DT = np.dtype([("seq", "<i4"), ("past", "<i4"), ("q_len", "<i4"), ("q_sta
 assert _ENTRY_DT.itemsize == 40
 
 
+# packed query rows the decode kernel K7 takes (kDecodeMaxRows, csrc/attn_plan.h);
+# entries with more go to the tcgen05 kernel K6 and are ordered first
+DECODE_MAX_ROWS = 24
+
+
 class CostLedger:
     """Monotonic forward-pass counters (engine.py:72-102)."""
 
@@ -345,7 +350,8 @@ class GpuEngine:
         if n_e > self.max_entries:
             raise ValueError(f"{n_e} entries > engine max {self.max_entries}")
         G = self.shape.n_heads // self.shape.n_kv_heads
-        order = sorted(range(n_e), key=lambda i: 0 if len(reqs[i].batch) * G > 32 else 1)
+        order = sorted(range(n_e),
+                       key=lambda i: 0 if len(reqs[i].batch) * G > DECODE_MAX_ROWS else 1)
         ents = np.zeros(n_e, dtype=_ENTRY_DT)
         toks, rseq, rpos, orow = [], [], [], []
         q_start = out_start = 0
