@@ -6,10 +6,14 @@
 // positions in the M=128 rows, so every K/V tile is loaded once for all G
 // heads.  Two CTAs share an SM (256 TMEM columns and ~112 KB smem each), so
 // one CTA's softmax overlaps the other's tensor-core work.  Warp roles:
-//   warp 0  TMA producer: per 64-key tile, four 2D TMA boxes (K, V x two
-//           128-byte column halves, SWIZZLE_128B) when the tile's cells form
-//           one run, else a cell-by-cell cp.async gather into the same layout;
-//           2-stage ring with full/empty mbarriers.
+//   warp 0  TMA producer: per 64-key tile, two 2D TMA boxes each for K and
+//           V (128-byte column halves, SWIZZLE_128B) when the tile's cells
+//           form one run, else a cell-by-cell cp.async gather into the same
+//           layout.  K and V have their own rings (3 and 2 stages): a K stage
+//           frees as soon as its S = QK^T MMA completes, so K loads run three
+//           tiles ahead of the MMAs and V loads two - the load latency no
+//           longer gates the tensor pipe (with one shared 2-stage K|V ring the
+//           softmax warps sat ~45% of the time waiting for S).
 //   warp 1  MMA issuer (one elected thread): S_j = Q.K_j^T (M=128, N=64, K=128;
 //           8 x tcgen05.mma kind::f16, K-major SW128 descriptors) into a
 //           double-buffered TMEM S; O += P_j.V_j with P read straight from
@@ -37,14 +41,16 @@ constexpr int kBM = 128;                    // packed query rows per CTA
 constexpr int kBN = 64;                     // keys per tile
 constexpr int kQHalf = kBM * 128;           // Q: 64-column half of [128 rows][128 d] (16 KB)
 constexpr int kKHalf = kBN * 128;           // K/V: 64-column half of [64 keys][128 d] (8 KB)
-constexpr int kStages = 2;
+constexpr int kKStages = 3, kVStages = 2;
 constexpr int kThreads = 6 * 32;
 constexpr int kSmemQ = 0;                             // 32 KB
-constexpr int kSmemKV = 2 * kQHalf;                   // stages x (K 16 KB | V 16 KB)
-constexpr int kSmemBar = kSmemKV + kStages * 4 * kKHalf;
+constexpr int kSmemK = 2 * kQHalf;                    // K ring: 3 x 16 KB
+constexpr int kSmemV = kSmemK + kKStages * 2 * kKHalf;  // V ring: 2 x 16 KB
+constexpr int kSmemBar = kSmemV + kVStages * 2 * kKHalf;  // 112 KB: two CTAs per SM
 constexpr int kSmemBytes = kSmemBar + 128;
 constexpr int kTmemCols = 256;  // S0/P0 [0,64) S1/P1 [64,128) O [128,256)
 constexpr int kMaxSplits = 64;
+constexpr int kPolyPeriod = 8, kPolyPairs = 0;  // 3 of every 8 exp pairs on the FMA pipe
 constexpr int kMaxPartialCtas = 8 * 148;  // bounds the split-partial workspace
 
 // 16-byte chunk c (0..15 over d) of row r in a tile of `rows` rows, SW128
@@ -67,13 +73,14 @@ __global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
     const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
-  uint64_t* kv_full = bars;       // [2]
-  uint64_t* kv_empty = bars + 2;  // [2]
-  uint64_t* s_full = bars + 4;    // [2]
-  uint64_t* s_empty = bars + 6;   // [2]
-  uint64_t* pv_done = bars + 8;   // PV_j complete: P smem free, O stable
-  uint64_t* p_full = bars + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* k_full = bars;        // [3]
+  uint64_t* k_empty = bars + 3;   // [3]
+  uint64_t* v_full = bars + 6;    // [2]
+  uint64_t* v_empty = bars + 8;   // [2]
+  uint64_t* s_full = bars + 10;   // [2]
+  uint64_t* pv_done = bars + 12;  // PV_j complete: P_j's TMEM columns free, O stable
+  uint64_t* p_full = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
   if (smem_u32(smem) & 1023) __trap();  // SW128 tiles need 1 KB alignment
   pdl_wait();
   pdl_trigger();
@@ -98,12 +105,15 @@ __global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
   const int ntiles = j0 >= j1 ? 0 : j1 - j0;
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
+    for (int i = 0; i < kKStages; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
     }
+    for (int i = 0; i < kVStages; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
     mbar_init(pv_done, 1);
     mbar_init(p_full, 4);
     mbar_fence_init();
@@ -135,59 +145,77 @@ __global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
       tma_prefetch_desc(&tmv);
     }
     const int64_t hrow = kh * head_stride;
-    for (int jj = 0; jj < ntiles; ++jj) {
-      const int st = jj % kStages;
-      if (jj >= kStages) mbar_wait(&kv_empty[st], ((jj / kStages) - 1) & 1);
-      uint8_t* ks = smem + kSmemKV + st * 4 * kKHalf;
-      uint8_t* vs = ks + 2 * kKHalf;
+    // tile cells: one contiguous run -> TMA boxes, else a cp.async gather
+    struct Cells {
+      int lo, hi, c0;
+      bool run;
+    };
+    auto cells = [&](int jj) {
       const int kt = (j0 + jj) * kBN;
       const int nvalid = min(kBN, kv_hi - kt);
-      const int c_lo = lane < nvalid ? __ldg(p2c + kt + lane) : -1;
-      const int c_hi = lane + 32 < nvalid ? __ldg(p2c + kt + 32 + lane) : -1;
-      const int c0 = __shfl_sync(0xffffffffu, c_lo, 0);
-      const bool run = __all_sync(0xffffffffu, (c_lo < 0 || c_lo == c0 + lane) &&
-                                                    (c_hi < 0 || c_hi == c0 + 32 + lane));
-      if (run) {
+      Cells c;
+      c.lo = lane < nvalid ? __ldg(p2c + kt + lane) : -1;
+      c.hi = lane + 32 < nvalid ? __ldg(p2c + kt + 32 + lane) : -1;
+      c.c0 = __shfl_sync(0xffffffffu, c.lo, 0);
+      c.run = __all_sync(0xffffffffu, (c.lo < 0 || c.lo == c.c0 + lane) &&
+                                          (c.hi < 0 || c.hi == c.c0 + 32 + lane));
+      return c;
+    };
+    auto load = [&](const Cells& c, const CUtensorMap* map, const __nv_bfloat16* pool,
+                    uint8_t* dst, uint64_t* full) {
+      if (c.run) {
         if (lane == 0) {
-          mbar_expect_tx(&kv_full[st], 4 * kKHalf);
-          const int row = static_cast<int>(hrow + c0);
-          tma_load_2d(ks, &tmk, 0, row, &kv_full[st]);
-          tma_load_2d(ks + kKHalf, &tmk, 64, row, &kv_full[st]);
-          tma_load_2d(vs, &tmv, 0, row, &kv_full[st]);
-          tma_load_2d(vs + kKHalf, &tmv, 64, row, &kv_full[st]);
+          mbar_expect_tx(full, 2 * kKHalf);
+          const int row = static_cast<int>(hrow + c.c0);
+          tma_load_2d(dst, map, 0, row, full);
+          tma_load_2d(dst + kKHalf, map, 64, row, full);
         }
       } else {
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
           const int r = lane + 32 * h;
-          const int cv = h ? c_hi : c_lo;
-          const int64_t off = (hrow + (cv >= 0 ? cv : c0)) * kD;
+          const int cv = h ? c.hi : c.lo;
+          const int64_t off = (hrow + (cv >= 0 ? cv : c.c0)) * kD;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            cp_async16(ks + sw128(kBN, r, q), kpool + off + q * 8);
-            cp_async16(vs + sw128(kBN, r, q), vpool + off + q * 8);
-          }
+          for (int q = 0; q < 16; ++q) cp_async16(dst + sw128(kBN, r, q), pool + off + q * 8);
         }
         cp_async_commit();
         cp_async_wait<0>();
         tc::fence_proxy_async();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&kv_full[st]);
+        if (lane == 0) mbar_arrive(full);
       }
+    };
+    auto load_v = [&](int jj, const Cells& c) {
+      const int st = jj % kVStages;
+      if (jj >= kVStages) mbar_wait(&v_empty[st], ((jj / kVStages) - 1) & 1);
+      load(c, &tmv, vpool, smem + kSmemV + st * 2 * kKHalf, &v_full[st]);
+    };
+    // K_jj, then V_{jj-1}: V lags one tile (it is consumed a softmax later)
+    Cells prev{};
+    for (int jj = 0; jj < ntiles; ++jj) {
+      const Cells c = cells(jj);
+      const int st = jj % kKStages;
+      if (jj >= kKStages) mbar_wait(&k_empty[st], ((jj / kKStages) - 1) & 1);
+      load(c, &tmk, kpool, smem + kSmemK + st * 2 * kKHalf, &k_full[st]);
+      if (jj > 0) load_v(jj - 1, prev);
+      prev = c;
     }
+    if (ntiles > 0) load_v(ntiles - 1, prev);
   } else if (warp == 1) {
     // ======================= MMA issuer =======================
     if (lane == 0 && ntiles > 0) {
       constexpr uint32_t idesc_s = tc::idesc_bf16(kBM, kBN, false);
       constexpr uint32_t idesc_pv = tc::idesc_bf16(kBM, kD, true);
       const uint32_t q_base = smem_u32(smem + kSmemQ);
-      const uint32_t kv_base = smem_u32(smem + kSmemKV);
+      const uint32_t k_base = smem_u32(smem + kSmemK);
+      const uint32_t v_base = smem_u32(smem + kSmemV);
       auto issue_s = [&](int jj) {
-        const int st = jj % kStages, sb = jj & 1;
-        mbar_wait(&kv_full[st], (jj / kStages) & 1);
+        const int st = jj % kKStages, sb = jj & 1;
+        mbar_wait(&k_full[st], (jj / kKStages) & 1);
         // S/P buffer sb was last read by PV_{jj-2}, issued (in order) before us
         tc::fence_after();
-        const uint32_t kb = kv_base + st * 4 * kKHalf;
+        const uint32_t kb = k_base + st * 2 * kKHalf;
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk) {
           tc::mma(tmem + sb * kBN,
@@ -196,21 +224,23 @@ __global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
                   kk > 0);
         }
         tc::commit(&s_full[sb]);
+        tc::commit(&k_empty[st]);  // K stage free once S_jj's MMAs complete
       };
       issue_s(0);
       for (int jj = 0; jj < ntiles; ++jj) {
         if (jj + 1 < ntiles) issue_s(jj + 1);
-        const int st = jj % kStages;
+        const int st = jj % kVStages;
         mbar_wait(p_full, jj & 1);
+        mbar_wait(&v_full[st], (jj / kVStages) & 1);
         tc::fence_after();
-        const uint32_t vb = kv_base + st * 4 * kKHalf + 2 * kKHalf;
+        const uint32_t vb = v_base + st * 2 * kKHalf;
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk) {
           tc::mma_ts(tmem + 2 * kBN, tmem + (jj & 1) * kBN + kk * 8,
                      tc::smem_desc(vb + kk * 2048, kKHalf, 1024), idesc_pv, (jj | kk) > 0);
         }
         tc::commit(pv_done);
-        tc::commit(&kv_empty[st]);
+        tc::commit(&v_empty[st]);
       }
     }
   } else {
@@ -238,22 +268,34 @@ __global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
         for (int i = 0; i < kBN; ++i)
           if (!(kt + i <= pos && kt + i < kv_len)) sv[i] = __float_as_uint(-INFINITY);
       }
-      float mraw = -INFINITY;  // max of raw scores (scale > 0 commutes with max)
+      // max of raw scores (scale > 0 commutes with max); 8 independent chains
+      // instead of one 64-long dependent FMNMX chain
+      float mpart[8];
 #pragma unroll
-      for (int i = 0; i < kBN; ++i) mraw = fmaxf(mraw, __uint_as_float(sv[i]));
+      for (int c = 0; c < 8; ++c) mpart[c] = __uint_as_float(sv[c]);
+#pragma unroll
+      for (int i = 8; i < kBN; ++i) mpart[i & 7] = fmaxf(mpart[i & 7], __uint_as_float(sv[i]));
+      const float mraw = fmaxf(fmaxf(fmaxf(mpart[0], mpart[1]), fmaxf(mpart[2], mpart[3])),
+                               fmaxf(fmaxf(mpart[4], mpart[5]), fmaxf(mpart[6], mpart[7])));
       const float mx = mraw * scale_log2;
       const float new_ref = (mx > m_ref + 8.f) ? mx : m_ref;
       const float scale_old = (m_ref == -INFINITY) ? 0.f : fast_exp2(m_ref - new_ref);
       const float mref = new_ref == -INFINITY ? 0.f : new_ref;
-      float sum = 0.f;
+      float spart[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial sums
       uint32_t pk[kBN / 2];
+      // exponentials split between MUFU (ex2) and the FMA pipe (polynomial):
+      // MUFU alone caps the softmax at 16 exp/clk/SM, below the MMA rate
 #pragma unroll
       for (int i = 0; i < kBN; i += 2) {
-        const float p0 = fast_exp2(fmaf(__uint_as_float(sv[i]), scale_log2, -mref));
-        const float p1 = fast_exp2(fmaf(__uint_as_float(sv[i + 1]), scale_log2, -mref));
-        sum += p0 + p1;
+        const float x0 = fmaf(__uint_as_float(sv[i]), scale_log2, -mref);
+        const float x1 = fmaf(__uint_as_float(sv[i + 1]), scale_log2, -mref);
+        const bool poly = (i / 2) % kPolyPeriod < kPolyPairs;
+        const float p0 = poly ? poly_exp2(x0) : fast_exp2(x0);
+        const float p1 = poly ? poly_exp2(x1) : fast_exp2(x1);
+        spart[(i / 2) & 3] += p0 + p1;
         pk[i / 2] = pack_bf16(p0, p1);
       }
+      const float sum = (spart[0] + spart[1]) + (spart[2] + spart[3]);
       tc::st32(trow + sb * kBN, pk);  // P_j over its own S columns
       // PV_{j-1} done (O stable) before an O correction and before PV_j is issued
       if (jj > 0) {
