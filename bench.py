@@ -428,6 +428,13 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "turn_ms_all": [round(r.latency_ms, 2) for r in recs[: min(nturns, 12)]],
         "prefill_tok_s": round(prefill_tok / max(fwd["prefill"]["seconds"], 1e-9), 1),
         "decode_tok_s": round(gen_tok / max(fwd["decode"]["seconds"], 1e-9), 1),
+        "forward_split_ms_per_step": {  # device time of the forwards vs wall clock
+            "prefill": round(1000 * fwd["prefill"]["seconds"] / args.steps, 3),
+            "prefill_forwards": fwd["prefill"]["n"] // args.steps,
+            "decode": round(1000 * fwd["decode"]["seconds"] / args.steps, 3),
+            "decode_forwards": fwd["decode"]["n"] // args.steps,
+            "device": round(1000 * gpu_s / args.steps, 3),
+            "wall": round(1000 * elapsed / args.steps, 3)},
         "gpu_launches": launches,
         "e2e": {"value": round(total_turns / elapsed, 3), "unit": UNIT,
                 "h2d_bytes_per_step": int(eng.h2d_bytes / args.steps),

@@ -9,7 +9,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdeltaserve_b200.so")
+# DS_B200_LIB: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("DS_B200_LIB") or os.path.join(HERE, "libdeltaserve_b200.so")
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64

@@ -205,9 +205,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
       }
     }
     if (!waited) pdl_wait();
+    if (!cluster_merge) pdl_trigger();  // the combine kernel follows (see the end)
   } else {
     // ================= consumers =================
     pdl_wait();  // q comes from the preceding projection
+    if (!cluster_merge) pdl_trigger();
     const int g = lane >> 2, t = lane & 3;
     // Q^T as the B operand: qb[j][kk] covers rows 8j + g, d [16kk + 2t, +1] and
     // [16kk + 8 + 2t, +1] - registers for NT <= 2, else a swizzled smem copy
@@ -438,10 +440,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     }
     cluster_sync_all();  // peers keep their smem until every read is done
   }
-  // PDL: the dependent projection launches only as this grid retires.  Any
-  // earlier trigger (even after the main loop) lets its CTAs onto the SMs
-  // while the attention runs, and the whole forward was measured ~25% slower.
-  pdl_trigger();
+  // PDL: with the in-cluster merge the dependent is the next projection,
+  // launched only as this grid retires - any earlier trigger (even after the
+  // main loop) lets its CTAs onto the SMs while the attention runs, and the
+  // whole forward was measured ~25% slower.  Without it the dependent is the
+  // small combine kernel, which may launch early.
+  if (cluster_merge || !active) pdl_trigger();
 }
 
 int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_entry* entries_dev,

@@ -270,20 +270,29 @@ __global__ void attn_combine_kernel(const ds_entry* __restrict__ entries, int n_
   const AttnSplitPlan plan = attn_split_plan(qblocks, en.past + en.q_len, nkv, n_entries, mode);
   if (plan.n_splits <= 1) return;
   const int64_t base = attn_partial_base(entries, e, n_entries, nh, nkv, mode);
-  // splits are independent loads: unrolled so their L2 latencies overlap
+  // two dependent L2 round trips in all: the split lse values (one thread
+  // each) into smem, then every split's O column issued at once
   const int64_t s0 = (base + r) * nkv + kh, sstride = static_cast<int64_t>(R) * nkv;
-  float lmax = -INFINITY;
-#pragma unroll 8
-  for (int s = 0; s < plan.n_splits; ++s) lmax = fmaxf(lmax, __ldcg(part_lse + s0 + s * sstride));
-  float acc = 0.f, wsum = 0.f;
+  __shared__ float lse_s[64];
   const int d = threadIdx.x;
-#pragma unroll 8
-  for (int s = 0; s < plan.n_splits; ++s) {
-    const int64_t slot = s0 + s * sstride;
-    const float lse = __ldcg(part_lse + slot);
-    const float w = lse == -INFINITY ? 0.f : exp2f(lse - lmax);
-    wsum += w;
-    acc += w * __ldcg(part_o + slot * kD + d);
+  if (d < plan.n_splits) lse_s[d] = __ldcg(part_lse + s0 + d * sstride);
+  __syncthreads();
+  float lmax = -INFINITY;
+  for (int s = 0; s < plan.n_splits; ++s) lmax = fmaxf(lmax, lse_s[s]);
+  float acc = 0.f, wsum = 0.f;
+  for (int sb = 0; sb < plan.n_splits; sb += 16) {
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      v[i] = sb + i < plan.n_splits ? __ldcg(part_o + (s0 + (sb + i) * sstride) * kD + d) : 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (sb + i >= plan.n_splits) break;
+      const float lse = lse_s[sb + i];
+      const float w = lse == -INFINITY ? 0.f : exp2f(lse - lmax);
+      wsum += w;
+      acc += w * v[i];
+    }
   }
   const int ti = r / G, gi = r - (r / G) * G;
   out[static_cast<int64_t>(en.q_start + ti) * nh * kD + (kh * G + gi) * kD + d] =

@@ -104,20 +104,6 @@ DS_DEVICE float fast_exp2(float x) {
   return y;
 }
 
-// 2^x on the FMA pipe (no MUFU): round-to-nearest split x = n + f, f in
-// [-1/2, 1/2], degree-3 polynomial for 2^f (relative error < 1e-4, far below
-// the bf16 rounding of P), n added straight into the exponent field.  Lets a
-// softmax spread its exponentials over both pipes.
-DS_DEVICE float poly_exp2(float x) {
-  x = fmaxf(x, -126.f);
-  const float t = x + 12582912.f;  // 1.5 * 2^23: low mantissa bits = round(x)
-  const float f = x - (t - 12582912.f);
-  float p = fmaf(f, 0.0555041087f, 0.2402264923f);
-  p = fmaf(p, f, 0.6931471806f);
-  p = fmaf(p, f, 1.f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
-
 }  // namespace ds
 
 // ---------------------------------------------------------------------------

@@ -50,7 +50,9 @@ main.sort(key=lambda e: e["ts"] + e["dur"])
 inc = defaultdict(float)
 cnt = defaultdict(int)
 for a, b in zip(main, main[1:]):
-    name = b["name"].split("(")[0].split("<")[0][:60]
+    name = b["name"].split("(")[0].split("<")[0][:48]
+    if "gemm_skinny" in name:  # split by shape (grid size)
+        name += f" grid={b['args'].get('grid')}"
     inc[name] += (b["ts"] + b["dur"]) - (a["ts"] + a["dur"])
     cnt[name] += 1
 tot = sum(inc.values())
