@@ -6,15 +6,17 @@ OUT=gpurun_out
 mkdir -p $OUT
 python bench.py > $OUT/bench_ours.json 2> $OUT/bench_ours.err
 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+python bench.py --workload c5 --no-micro --no-cpu > $OUT/bench_ours_c5.json 2> $OUT/bench_ours_c5.err
 # launch list (cold-cache, serialised; shares only) of a short bench run, steady state
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 3000 -c 1500 --csv \
   --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu --no-micro \
   > $OUT/launches_bench.log 2>&1
-# full captures of the dominant kernels
+# full captures of the dominant kernels (the skinny GEMM: gate_up, M=5)
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:gemm_skinny -s 40 -c 2 \
   -o $OUT/ncu_gemm_skinny python tools/profile_forward.py llama3-8b 1000 5 > /dev/null 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:attn_decode -s 2 -c 1 \
   -o $OUT/ncu_k7_decode python tools/micro_attn.py 32768 5 0 4 > /dev/null 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:attn_prefill -s 2 -c 1 \
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:attn_prefill_kernel -s 2 -c 1 \
   -o $OUT/ncu_k6_prefill python tools/micro_attn.py 31489 881 2 4 > /dev/null 2>&1
+python tools/profile_forward.py llama3-8b 1000 5 > $OUT/forward_critical_path.txt 2>&1
 ls -la $OUT
