@@ -88,6 +88,15 @@ DS_DEVICE float merged_row(const float* msm, const float* lsm, const float* osm,
 }
 }  // namespace
 
+// one-shot hint from the forward runtime: bytes to pull into L2 while the
+// attention runs (consumed by the next decode launch on this thread)
+static thread_local const void* g_l2_ptr = nullptr;
+static thread_local int64_t g_l2_bytes = 0;
+void set_attn_l2_prefetch(const void* ptr, int64_t bytes) {
+  g_l2_ptr = ptr;
+  g_l2_bytes = bytes;
+}
+
 int decode_smem_bytes() { return 1024 + kStages * kStageBytes + kQBytes + 2 * kStages * 8; }
 
 template <int NT>  // n-tiles of 8 packed query rows
@@ -98,7 +107,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     int64_t pos_stride, int nh, int nkv, float scale_log2, __nv_bfloat16* __restrict__ out,
     float* __restrict__ part_o, float* __restrict__ part_lse, int64_t head_stride,
     int* __restrict__ counters, const __grid_constant__ CUtensorMap tmk,
-    const __grid_constant__ CUtensorMap tmv) {
+    const __grid_constant__ CUtensorMap tmv, const char* __restrict__ l2p, int64_t l2_bytes) {
   (void)counters;
   const bool cluster_merge = max_splits <= kDecodeMaxCluster;  // launched with clusters
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -206,6 +215,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     }
     if (!waited) pdl_wait();
     if (!cluster_merge) pdl_trigger();  // the combine kernel follows (see the end)
+    if (l2p && lane == 0) {  // this CTA's share of the next projection's weights -> L2
+      const int64_t n_cta = static_cast<int64_t>(gridDim.y) * gridDim.z;
+      const int64_t share = ((l2_bytes + n_cta - 1) / n_cta + 15) & ~15ll;
+      const int64_t beg = share * (blockIdx.z * gridDim.y + blockIdx.y);
+      const int64_t lim = l2_bytes & ~15ll;
+      const int64_t end = beg + share < lim ? beg + share : lim;
+      for (int64_t off = beg; off < end; off += 32768) {
+        const uint32_t n = static_cast<uint32_t>(end - off < 32768 ? end - off : 32768);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(l2p + off), "r"(n)
+                     : "memory");
+      }
+    }
   } else {
     // ================= consumers =================
     pdl_wait();  // q comes from the preceding projection
@@ -469,6 +490,10 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
   dim3 grid(1, nkv, n_entries * max_splits);
   const float sl2 = scale * 1.4426950408889634f;
   const int stride = (nh + 2 * nkv) * kD;
+  const char* l2p = static_cast<const char*>(g_l2_ptr);
+  const int64_t l2_bytes = g_l2_bytes;
+  g_l2_ptr = nullptr;
+  g_l2_bytes = 0;
   auto kern = max_R <= 8 ? attn_decode_kernel<1>
               : max_R <= 16 ? attn_decode_kernel<2>
                             : attn_decode_kernel<3>;
@@ -478,14 +503,14 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
                          max_splits, static_cast<const __nv_bfloat16*>(k_pool),
                          static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv,
                          sl2, static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride,
-                         counters, *tk, *tv);
+                         counters, *tk, *tv, l2p, l2_bytes);
   else
     launch_pdl(kern, grid, dim3(kThreads), smem, stream, static_cast<const __nv_bfloat16*>(qkv),
                stride, entries_dev, n_entries, max_splits,
                static_cast<const __nv_bfloat16*>(k_pool),
                static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv, sl2,
                static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride, counters, *tk,
-               *tv);
+               *tv, l2p, l2_bytes);
   return (int)cudaGetLastError();
 }
 

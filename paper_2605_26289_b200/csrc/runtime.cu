@@ -16,6 +16,7 @@
 
 namespace ds {
 
+void set_attn_l2_prefetch(const void* ptr, int64_t bytes);
 int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_entry* entries_dev,
                       int n_entries, const void* k_pool, const void* v_pool, int64_t head_stride,
                       const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv, int hd,
@@ -300,6 +301,10 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
                                 nh, nkv, hd, m->rope_cos, m->rope_sin, kp + l * kv_layer,
                                 vp + l * kv_layer, kv->capacity, stream));
     }
+    // the attention leaves HBM mostly idle (short contexts): K7's producer
+    // warps pull wo's weights into L2 for the next projection meanwhile
+    if (fused) set_attn_l2_prefetch(wo + static_cast<size_t>(l) * H * nh * hd,
+                                    static_cast<int64_t>(H) * nh * hd * 2);
     if (n_long > 0 && n_long < a->n_entries) {  // mixed plan: K6 for prefill chunks, K7 rest
       DS_CHECK(ds_attention(b.qkv, a->entries_host, a->entries, n_long, T, kp + l * kv_layer,
                             vp + l * kv_layer, kv->capacity, kv->pos2cell, kv->pos_stride, nh,
@@ -346,6 +351,7 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
       DS_CHECK(project(rt.blas, b.act, wd_l, b.x, T, H, F, true, true, stream));
     }
   }
+  set_attn_l2_prefetch(nullptr, 0);  // a hint not consumed (K6-only layer) must not leak
   // final norm on sampled rows only, LM head in fp32
   DS_CHECK(ds_rmsnorm(b.x, 1, a->out_rows, a->n_out, H, m->final_norm, m->rms_eps, b.hf, stream));
   DS_CHECK(project(rt.blas, b.hf, m->lm_head, a->logits, a->n_out, m->vocab, H, true, false,
