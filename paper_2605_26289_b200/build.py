@@ -20,7 +20,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")]
 
-SOURCES = ["policy.cu", "kvmeta.cu", "layers.cu", "attn_split.cu", "attn_decode.cu", "attn_prefill_sm100.cu",
+SOURCES = ["policy.cu", "kvmeta.cu", "layers.cu", "attn_split.cu", "attn_decode.cu", "attn_decode_tc.cu",
+           "attn_prefill_sm100.cu",
            "gemm_skinny.cu", "tma.cu",
            "runtime.cu"]
 

@@ -34,6 +34,7 @@
 // short-context case, where that fixed cost dominates).  Longer contexts write
 // split partials (O, lse) for attn_combine_kernel.
 #include "../../include/deltaserve_b200.h"
+#include "attn_decode_merge.cuh"
 #include "attn_plan.h"
 #include "common.cuh"
 #include "tma.h"
@@ -96,6 +97,12 @@ void set_attn_l2_prefetch(const void* ptr, int64_t bytes) {
   g_l2_ptr = ptr;
   g_l2_bytes = bytes;
 }
+
+int launch_attn_decode_tc(const ds_entry* entries_dev, int n_entries, const void* qkv,
+                          const void* k_pool, const void* v_pool, int64_t head_stride,
+                          const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv,
+                          int max_splits, float scale, void* out, float* part_o, float* part_lse,
+                          const void* l2p, int64_t l2_bytes, cudaStream_t stream);
 
 int decode_smem_bytes() { return 1024 + kStages * kStageBytes + kQBytes + 2 * kStages * 8; }
 
@@ -427,38 +434,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
   // ---- split merge across the cluster (distributed shared memory) ----
   if (cluster_merge && plan.n_splits > 1) {
     cluster_sync_all();  // every split's rows are in its cbuf
-    const uint32_t rank = cluster_ctarank();
-    const int cs = max_splits;  // cluster size
-    if (tid < kConsumers * 32) {
-      // per-row split weights 2^(lse_p - max) / sum, in split order
-      for (int i = tid; i < R; i += kConsumers * 32) {
-        float lmax = -INFINITY;
-        for (int p = 0; p < plan.n_splits; ++p)
-          lmax = fmaxf(lmax, dsmem_ld_f32(dsmem_map(smem_u32(clse + i), p)));
-        float wsum = 0.f;
-        for (int p = 0; p < plan.n_splits; ++p) {
-          const float lse = dsmem_ld_f32(dsmem_map(smem_u32(clse + i), p));
-          const float w = lse == -INFINITY ? 0.f : exp2f(lse - lmax);
-          cw[i * kDecodeMaxCluster + p] = w;
-          wsum += w;
-        }
-        const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
-        for (int p = 0; p < plan.n_splits; ++p) cw[i * kDecodeMaxCluster + p] *= inv;
-      }
-      named_bar_sync(1, kConsumers * 32);
-      for (int idx = static_cast<int>(rank) * kConsumers * 32 + tid; idx < R * kD;
-           idx += cs * kConsumers * 32) {
-        const int r = idx / kD, d = idx - r * kD;
-        const uint32_t a = smem_u32(cval + r * kD + d);
-        float acc = 0.f;
-#pragma unroll 4
-        for (int p = 0; p < plan.n_splits; ++p)
-          acc += cw[r * kDecodeMaxCluster + p] * dsmem_ld_f32(dsmem_map(a, p));
-        const int ti = r / G, gi = r - ti * G;
-        out[static_cast<int64_t>(en.q_start + ti) * nh * kD + (kh * G + gi) * kD + d] =
-            __float2bfloat16_rn(acc);
-      }
-    }
+    if (tid < kConsumers * 32)
+      decode_cluster_merge(cval, clse, cw, R, plan.n_splits, max_splits, tid, kConsumers * 32, 1,
+                           en, nh, kh, G, out);
     cluster_sync_all();  // peers keep their smem until every read is done
   }
   // PDL: with the in-cluster merge the dependent is the next projection,
@@ -474,8 +452,12 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
                        const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv, int max_R,
                        int max_splits, float scale, void* out, float* part_o, float* part_lse,
                        int* counters, cudaStream_t stream) {
-  (void)entries_host;
   if (max_R > kMaxRows) return DS_EUNSUPPORTED;
+  int max_kv = 0;
+  for (int e = 0; e < n_entries; ++e) {
+    const int kv = entries_host[e].past + entries_host[e].q_len;
+    max_kv = kv > max_kv ? kv : max_kv;
+  }
   const int smem = decode_smem_bytes();
   static bool attr = false;
   if (!attr) {
@@ -494,6 +476,12 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
   const int64_t l2_bytes = g_l2_bytes;
   g_l2_ptr = nullptr;
   g_l2_bytes = 0;
+  // more than 8 rows over a long prefix: the legacy HMMA pipe would bound the
+  // mma.sync kernel below the HBM rate - run the tcgen05 variant
+  if (max_R > kDecodeTcMinRows && max_kv >= kDecodeTcMinKeys)
+    return launch_attn_decode_tc(entries_dev, n_entries, qkv, k_pool, v_pool, head_stride,
+                                 pos2cell, pos_stride, nh, nkv, max_splits, scale, out, part_o,
+                                 part_lse, l2p, l2_bytes, stream);
   auto kern = max_R <= 8 ? attn_decode_kernel<1>
               : max_R <= 16 ? attn_decode_kernel<2>
                             : attn_decode_kernel<3>;

@@ -24,6 +24,10 @@ constexpr int kDecodeMaxRows = 24;
 // kernel merges them.  A cluster must fit one GPC, so 8 (portable) - larger
 // clusters were measured to serialise on GPCs with fewer free SMs.
 constexpr int kDecodeMaxCluster = 8;
+// K7 runs on tcgen05 (attn_decode_tc.cu) above this many rows when the prefix
+// is long enough for the MMA pipe, not the fixed latency, to matter
+constexpr int kDecodeTcMinRows = 8;
+constexpr int kDecodeTcMinKeys = 4096;
 constexpr int kSplitRows = 64;  // packed rows per split-kernel CTA (4 warps x 16)
 
 struct AttnSplitPlan {
