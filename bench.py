@@ -445,6 +445,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     }
     if not args.no_micro:
         line["kernels"] = kernel_micro(torch, dev, peaks)
+        from paper_2605_26289_b200.curve import prefix_curve
+
+        line["prefix_curve"] = prefix_curve(model=args.model, weights=eng.w)
     if not args.no_cpu:
         ref = reference_turns(args.workload, 2)
         n, aff, model = cpu_info()

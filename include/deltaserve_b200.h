@@ -272,6 +272,11 @@ typedef struct {
   void* k_pool_l;
   void* v_pool_l;
   int64_t kv_head_stride;
+  /* the next kernel's first weight bytes: the CTAs of the last wave pull
+   * [l2_next, l2_next + l2_next_bytes) into L2 once their own weight stream
+   * is issued, so HBM stays busy across the kernel boundary (0 = none) */
+  const void* l2_next;
+  int64_t l2_next_bytes;
 } ds_skinny_epi;
 
 int ds_gemm_skinny_ex(const void* X, const void* W, void* Y, int M, int N, int K, int y_f32,

@@ -59,7 +59,7 @@ class SkinnyEpi(ctypes.Structure):
                 ("n_heads", c_i32), ("n_kv_heads", c_i32), ("row_seq", c_vp), ("row_pos", c_vp),
                 ("pos2cell", c_vp), ("pos_stride", c_i64), ("rope_cos", c_vp),
                 ("rope_sin", c_vp), ("k_pool_l", c_vp), ("v_pool_l", c_vp),
-                ("kv_head_stride", c_i64)]
+                ("kv_head_stride", c_i64), ("l2_next", c_vp), ("l2_next_bytes", c_i64)]
 
 
 class ForwardArgs(ctypes.Structure):

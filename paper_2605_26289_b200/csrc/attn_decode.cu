@@ -114,8 +114,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     int64_t pos_stride, int nh, int nkv, float scale_log2, __nv_bfloat16* __restrict__ out,
     float* __restrict__ part_o, float* __restrict__ part_lse, int64_t head_stride,
     int* __restrict__ counters, const __grid_constant__ CUtensorMap tmk,
-    const __grid_constant__ CUtensorMap tmv, const char* __restrict__ l2p, int64_t l2_bytes) {
-  (void)counters;
+    const __grid_constant__ CUtensorMap tmv, const char* __restrict__ l2p, int64_t l2_bytes,
+    int last_merge) {
   const bool cluster_merge = max_splits <= kDecodeMaxCluster;  // launched with clusters
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // SW128 alignment
@@ -221,7 +221,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
       }
     }
     if (!waited) pdl_wait();
-    if (!cluster_merge) pdl_trigger();  // the combine kernel follows (see the end)
     if (l2p && lane == 0) {  // this CTA's share of the next projection's weights -> L2
       const int64_t n_cta = static_cast<int64_t>(gridDim.y) * gridDim.z;
       const int64_t share = ((l2_bytes + n_cta - 1) / n_cta + 15) & ~15ll;
@@ -237,7 +236,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
   } else {
     // ================= consumers =================
     pdl_wait();  // q comes from the preceding projection
-    if (!cluster_merge) pdl_trigger();
     const int g = lane >> 2, t = lane & 3;
     // Q^T as the B operand: qb[j][kk] covers rows 8j + g, d [16kk + 2t, +1] and
     // [16kk + 8 + 2t, +1] - registers for NT <= 2, else a swizzled smem copy
@@ -371,6 +369,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
   #pragma unroll
         for (int j = 0; j < NT; ++j) mma_bf16_16816(o[i][j], a, pb[j][0], pb[j][1]);
       }
+      // generic-proxy reads of the stage complete before the producer's TMA
+      // (async proxy) refills it (measured necessary in the skinny GEMM ring)
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
@@ -428,6 +429,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
           if (d == 0) part_lse[slot] = lse;
         }
       }
+      if (!cluster_merge && last_merge)  // the last split to arrive merges the partials
+        decode_global_merge(part_o, part_lse, base, R, plan.n_splits, nkv, kh,
+                            counters + e * nkv + kh, cval, reinterpret_cast<int*>(clse), tid,
+                            kConsumers * 32, 1, en, nh, G, out);
     }
   }
 
@@ -439,12 +444,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
                            en, nh, kh, G, out);
     cluster_sync_all();  // peers keep their smem until every read is done
   }
-  // PDL: with the in-cluster merge the dependent is the next projection,
-  // launched only as this grid retires - any earlier trigger (even after the
-  // main loop) lets its CTAs onto the SMs while the attention runs, and the
-  // whole forward was measured ~25% slower.  Without it the dependent is the
-  // small combine kernel, which may launch early.
-  if (cluster_merge || !active) pdl_trigger();
+  // PDL: the dependent is the next projection, launched only as this grid
+  // retires - any earlier trigger (even after the main loop) lets its CTAs
+  // onto the SMs while the attention runs, and the whole forward was measured
+  // ~25% slower.
+  pdl_trigger();
 }
 
 int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_entry* entries_dev,
@@ -472,6 +476,9 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
   dim3 grid(1, nkv, n_entries * max_splits);
   const float sl2 = scale * 1.4426950408889634f;
   const int stride = (nh + 2 * nkv) * kD;
+  // more splits than a cluster: up to 8 rows the last split to arrive merges
+  // (cheap: R*128 values), more rows go to attn_combine_kernel (attn_split.cu)
+  const int last_merge = max_R <= kDecodeLastMergeRows;
   const char* l2p = static_cast<const char*>(g_l2_ptr);
   const int64_t l2_bytes = g_l2_bytes;
   g_l2_ptr = nullptr;
@@ -491,14 +498,14 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
                          max_splits, static_cast<const __nv_bfloat16*>(k_pool),
                          static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv,
                          sl2, static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride,
-                         counters, *tk, *tv, l2p, l2_bytes);
+                         counters, *tk, *tv, l2p, l2_bytes, last_merge);
   else
     launch_pdl(kern, grid, dim3(kThreads), smem, stream, static_cast<const __nv_bfloat16*>(qkv),
                stride, entries_dev, n_entries, max_splits,
                static_cast<const __nv_bfloat16*>(k_pool),
                static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv, sl2,
                static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride, counters, *tk,
-               *tv, l2p, l2_bytes);
+               *tv, l2p, l2_bytes, last_merge);
   return (int)cudaGetLastError();
 }
 

@@ -377,8 +377,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
                          kh, G, out);
     cluster_sync_all();  // peers keep their smem until every read is done
   }
-  // PDL: see K7 (the in-cluster path triggers only as the grid retires)
-  if (cluster_merge || !active) pdl_trigger();
+  // PDL: see K7 (triggers only as the grid retires; more splits than a
+  // cluster are merged by attn_combine_kernel, R > 8 here)
+  pdl_trigger();
 }
 
 int launch_attn_decode_tc(const ds_entry* entries_dev, int n_entries, const void* qkv,

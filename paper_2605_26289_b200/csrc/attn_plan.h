@@ -27,6 +27,10 @@ constexpr int kDecodeMaxCluster = 8;
 // K7 runs on tcgen05 (attn_decode_tc.cu) above this many rows when the prefix
 // is long enough for the MMA pipe, not the fixed latency, to matter
 constexpr int kDecodeTcMinRows = 8;
+// beyond a cluster's worth of splits, K7 merges in its last-arriving split CTA
+// up to this many rows (measured cheaper than a launch); more rows use the
+// combine kernel
+constexpr int kDecodeLastMergeRows = 8;
 constexpr int kDecodeTcMinKeys = 4096;
 constexpr int kSplitRows = 64;  // packed rows per split-kernel CTA (4 warps x 16)
 

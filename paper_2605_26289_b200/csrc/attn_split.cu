@@ -346,9 +346,12 @@ int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_en
     const int rc = launch_attn_decode(qkv, entries_host, entries_dev, n_entries, k_pool, v_pool,
                                       head_stride, pos2cell, pos_stride, nh, nkv, max_R,
                                       max_splits, scale, out, part_o, part_lse, counters, stream);
-    // K7 merges up to kDecodeMaxCluster key splits in-cluster; more go through
-    // global partials and the combine kernel
-    if (rc != 0 || !any_split || max_splits <= kDecodeMaxCluster) return rc;
+    // K7 merges up to kDecodeMaxCluster key splits in-cluster; more through
+    // global partials: merged by the last split to arrive for <= 8 rows,
+    // else by the combine kernel (launched early: K7 has not triggered it)
+    if (rc != 0 || !any_split || max_splits <= kDecodeMaxCluster ||
+        max_R <= kDecodeLastMergeRows)
+      return rc;
     dim3 cgrid(max_R, nkv, n_entries);
     launch_pdl(attn_combine_kernel, cgrid, dim3(kD), 0, stream, entries_dev, n_entries, nh, nkv,
                kSplitNW * 16, 1, (const float*)part_o, (const float*)part_lse,

@@ -2,59 +2,54 @@
 //
 // At M = 1..17 rows (decode, verify k+1) every weight byte is used M times, so
 // the projection is HBM-bound on the weight stream (the whole 8B forward is
-// ~16 GB of weights).  "Swap AB" on mma.sync m16n8k16: A = 16 weight rows,
-// B = X^T (8 tokens), D = 16 features x 8 tokens.  Weights are streamed
-// straight from HBM into registers with 128-bit L1-bypassing loads (no smem
-// round trip): lane (g, t) loads 8 consecutive k of rows g and g+8, and the
-// k order inside each 32-wide chunk is permuted identically for A and B (a dot
-// product is order free), so one 16-byte X load supplies both k16 steps.
-// A CTA owns 16 output features; its 8 warps split K and reduce through smem.
-// The activation operand (L2-resident) is software-pipelined one chunk ahead
-// in registers so its latency never serialises the MMAs; rows >= M are
-// predicated off (no load).
+// ~16 GB of weights).  Work unit = 16 output features x all of K.
+//
+// Data movement (TMA): persistent CTAs, two per SM (112 KB of shared memory
+// each), walk the units round-robin.  One producer thread streams, per stage,
+// ONE TMA box of the unit's 16 weight rows x KC columns and ONE box of the M
+// activation rows (3D tensor maps over 128-byte column slabs, SWIZZLE_128B)
+// into a ring of mbarrier-tracked stages; the weight boxes of the ring's first
+// round are issued before the programmatic-dependency wait (weights do not
+// depend on the previous kernel), so each projection's ring fills while its
+// predecessor drains.  Keeping the bytes in flight in shared memory (not in
+// L1 as register-streaming loads do) makes the kernel independent of the SM's
+// L1/shared carveout, which the decode attention (~200 KB of shared memory)
+// otherwise leaves behind - measured: the register-streaming version ran the
+// forward up to 1.5x slower after a non-cluster attention launch.
+//
+// Math: "swap AB" mma.sync m16n8k16, A = 16 weight rows, B = X^T (8 tokens per
+// n-tile), D = 16 features x 8 tokens.  Lane (g, t) reads 16 bytes at columns
+// [8t, 8t+8) of a k32 step for weight rows g, g+8 and token row g (the k order
+// inside a 32-column step is permuted identically for A and B - a dot product
+// is order free - so one 16-byte read feeds both k16 MMAs); the swizzle makes
+// those reads bank-conflict free.  8 math warps split each stage's k32 steps
+// and reduce through shared memory per unit.
 //
 // The epilogue absorbs the layer's elementwise kernels (ds_skinny_epi):
 //  * residual producer (wo, down; Y fp32 accumulate): also writes
-//    h = bf16(y * h_w) - the next RMSNorm's weight multiply - and this CTA's
+//    h = bf16(y * h_w) - the next RMSNorm's weight multiply - and this unit's
 //    per-row partial sum of y^2 over its 16 features, added into the row sums
 //    in 2^-24 fixed point (integer atomics: bit-identical whatever the CTA
 //    order); it also clears the other ss buffer (consumed upstream);
 //  * norm consumer (wqkv, gate_up): scales row m of the product by
 //    rsqrt(row sum / K + eps) - RMSNorm is a per-row scalar, so it commutes
-//    with the projection.  The row sum is loaded before the main loop and
-//    only consumed in the epilogue (no exposed latency);
+//    with the projection;
 //  * SwiGLU (gate_up with 8-row interleaved weights): feature rows g / g+8 of
-//    the CTA are gate / up of the same FFN unit, so the thread holding both
+//    the unit are gate / up of the same FFN unit, so the thread holding both
 //    writes act = bf16(silu(g) * u) directly (half the output bytes, no
 //    separate kernel);
 //  * RoPE + KV store (wqkv with RoPE-pair interleaved q/k rows): rows g / g+8
 //    are dims i / i+64 of one head, so the thread holding both rotates them;
 //    q goes to Y, k and v straight into the paged pools (the K5 kernel).
 #include "../../include/deltaserve_b200.h"
+#include "attn_plan.h"
 #include "common.cuh"
+#include "tma.h"
 
 namespace ds {
 
 constexpr int kGemvWarps = 8;
 constexpr float kSsScale = 16777216.f;  // 2^24 fixed point for the row sums of squares
-
-DS_DEVICE uint4 ldg_stream(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
-// predicated 16-byte activation load (zeros when off), no branch
-DS_DEVICE uint4 ldg_pred(const void* p, bool on) {
-  uint4 r = make_uint4(0, 0, 0, 0);
-  asm("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n"
-      " @q ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];\n}\n"
-      : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
-      : "l"(p), "r"(static_cast<int>(on)));
-  return r;
-}
 
 DS_DEVICE float bf16r(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
 
@@ -112,101 +107,14 @@ DS_DEVICE void rope_epilogue(const float (*red)[MT][4][32], const float* s_inv, 
   }
 }
 
-template <int MT, int U>
-__global__ void __launch_bounds__(kGemvWarps * 32) gemm_skinny_kernel(
-    const __nv_bfloat16* __restrict__ X, const __nv_bfloat16* __restrict__ W, void* __restrict__ Y,
-    int M, int N, int K, int y_f32, int accumulate, ds_skinny_epi epi) {
-  __shared__ float red[kGemvWarps][MT][4][32];
-  __shared__ float s_inv[32];
-  __shared__ float s_sq[32][17];
-  __shared__ int s_pos[32];
-  __shared__ int64_t s_cell[32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int n0 = blockIdx.x * 16;
-  const int kslice = K / kGemvWarps;
-  const int kbeg = warp * kslice;
-  const __nv_bfloat16* w0 = W + static_cast<int64_t>(n0 + g) * K + kbeg + 8 * t;
-  const __nv_bfloat16* w1 = w0 + static_cast<int64_t>(8) * K;
-  const __nv_bfloat16* xr[MT];
-  bool xv[MT];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt) {
-    const int m = mt * 8 + g;
-    xv[mt] = m < M;
-    xr[mt] = X + static_cast<int64_t>(xv[mt] ? m : 0) * K + kbeg + 8 * t;
-  }
-  float acc[MT][4];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
-
-  uint4 a[U][2], bn[U][MT];
-  // weights do not depend on the previous kernel: stream the first chunk
-  // before waiting on the activations (programmatic dependent launch)
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    a[u][0] = ldg_stream(w0 + 32 * u);
-    a[u][1] = ldg_stream(w1 + 32 * u);
-  }
-  pdl_wait();
-  pdl_trigger();
-#pragma unroll
-  for (int u = 0; u < U; ++u)
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) bn[u][mt] = ldg_pred(xr[mt] + 32 * u, xv[mt]);
-  if (epi.ss_zero && blockIdx.x == 0 && threadIdx.x < 32) epi.ss_zero[threadIdx.x] = 0;
-  // norm consumer: the producer's row sum of squares, needed only in the epilogue
-  const unsigned long long row_sum =
-      epi.row_ss && threadIdx.x < M ? __ldcg(reinterpret_cast<const unsigned long long*>(epi.row_ss) + threadIdx.x) : 0ull;
-  // RoPE/KV store: row positions and sequences (the cell lookup waits for the epilogue)
-  int r_pos = 0, r_seq = 0;
-  if (epi.rope && threadIdx.x < M) {
-    r_pos = __ldg(epi.row_pos + threadIdx.x);
-    r_seq = __ldg(epi.row_seq + threadIdx.x);
-  }
-
-  for (int kc = 0; kc < kslice; kc += 32 * U) {
-    if (kc) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        a[u][0] = ldg_stream(w0 + kc + 32 * u);
-        a[u][1] = ldg_stream(w1 + kc + 32 * u);
-      }
-    }
-    uint4 b[U][MT];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) b[u][mt] = bn[u][mt];
-    // next chunk (the last iteration re-reads its own chunk: harmless, branch-free)
-    const int kn = kc + 32 * U < kslice ? kc + 32 * U : kc;
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) bn[u][mt] = ldg_pred(xr[mt] + kn + 32 * u, xv[mt]);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t s0[4] = {a[u][0].x, a[u][1].x, a[u][0].y, a[u][1].y};
-      const uint32_t s1[4] = {a[u][0].z, a[u][1].z, a[u][0].w, a[u][1].w};
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        mma_bf16_16816(acc[mt], s0, b[u][mt].x, b[u][mt].y);
-        mma_bf16_16816(acc[mt], s1, b[u][mt].z, b[u][mt].w);
-      }
-    }
-  }
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) red[warp][mt][q][lane] = acc[mt][q];
-  if (epi.row_ss && threadIdx.x < M)
-    s_inv[threadIdx.x] =
-        rsqrtf(__ull2float_rn(row_sum) / (kSsScale * static_cast<float>(K)) + epi.eps);
-  if (epi.rope && threadIdx.x < M) {
-    s_pos[threadIdx.x] = r_pos;
-    s_cell[threadIdx.x] = __ldg(epi.pos2cell + static_cast<int64_t>(r_seq) * epi.pos_stride + r_pos);
-  }
-  __syncthreads();
+// The unit epilogue: reduce the 8 warps' partial accumulators (red) of the
+// 16 output features starting at n0 and apply the fused elementwise work.  Run
+// by the kGemvWarps*32 math threads (threadIdx.x < 256), after a barrier that
+// makes red visible; uses named barrier 1 over those threads.
+template <int MT>
+DS_DEVICE void unit_epilogue(const float (*red)[MT][4][32], const float* s_inv, const int* s_pos,
+                             const int64_t* s_cell, float (*s_sq)[17], const ds_skinny_epi& epi,
+                             void* Y, int M, int N, int n0, int y_f32, int accumulate) {
   if (epi.rope) {
     rope_epilogue<MT>(red, s_inv, s_pos, s_cell, epi, Y, M, N, n0);
     return;
@@ -265,7 +173,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemm_skinny_kernel(
     }
   }
   if (epi.ss_out) {
-    __syncthreads();
+    named_bar_sync(1, kGemvWarps * 32);
     if (threadIdx.x < M) {
       float v = 0.f;
 #pragma unroll
@@ -276,27 +184,216 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemm_skinny_kernel(
   }
 }
 
-template <int MT, int U>
-static void launch(const void* X, const void* W, void* Y, int M, int N, int K, int y_f32, int acc,
-                   const ds_skinny_epi& epi, cudaStream_t s) {
-  const int kslice = K / kGemvWarps;
-  if constexpr (U > 1) {
-    if (kslice % (32 * U)) {
-      launch<MT, U / 2>(X, W, Y, M, N, K, y_f32, acc, epi, s);
-      return;
+constexpr int kRingSmemBudget = 112 * 1024;  // two CTAs (two kernels) per SM
+
+DS_DEVICE uint4 lds128(uint32_t addr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(addr));
+  return r;
+}
+
+template <int MT, int NS>  // NS = k32 steps per math warp per stage (KC = 256*NS)
+__global__ void __launch_bounds__((kGemvWarps + 1) * 32, 1) gemm_ring_kernel(
+    void* __restrict__ Y, int M, int N, int K, int y_f32, int accumulate, int n_stages,
+    const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
+    ds_skinny_epi epi) {
+  constexpr int KC = 256 * NS;  // columns per stage = KC/64 slabs of 128 B
+  constexpr int kSlabs = KC / 64;
+  const int wbytes = 16 * KC * 2, xbytes = M * KC * 2;
+  const int SB = (wbytes + xbytes + 1023) & ~1023;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // SW128 atoms
+  float(*red)[MT][4][32] = reinterpret_cast<float(*)[MT][4][32]>(smem + n_stages * SB);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + n_stages * SB + kGemvWarps * MT * 4 * 32 * 4);
+  uint64_t* empty = full + n_stages;
+  __shared__ float s_inv[32];
+  __shared__ float s_sq[32][17];
+  __shared__ int s_pos[32];
+  __shared__ int64_t s_cell[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int units = N / 16, nst = K / KC;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < n_stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kGemvWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == kGemvWarps) {
+    // ---- producer (one thread): per stage one TMA box of 16 weight rows and
+    // one of the M activation rows.  Weights do not depend on the previous
+    // kernel: the ring's first round of weight boxes is issued before the
+    // dependency wait, those stages' activation boxes after it ----
+    if (lane == 0) {
+      tma_prefetch_desc(&tw);
+      tma_prefetch_desc(&tx);
+      const int my_units = static_cast<int>(blockIdx.x) < units
+                               ? (units - 1 - static_cast<int>(blockIdx.x)) / gridDim.x + 1 : 0;
+      const int total = my_units * nst;
+      const int pre = total < n_stages ? total : n_stages;
+      auto unit_of = [&](int it) { return static_cast<int>(blockIdx.x) + (it / nst) * gridDim.x; };
+      for (int it = 0; it < pre; ++it) {
+        mbar_expect_tx(&full[it], wbytes + xbytes);
+        tma_load_3d(smem + it * SB, &tw, 0, unit_of(it) * 16, (it % nst) * kSlabs, &full[it]);
+      }
+      pdl_wait();
+      for (int it = 0; it < pre; ++it)
+        tma_load_3d(smem + it * SB + wbytes, &tx, 0, 0, (it % nst) * kSlabs, &full[it]);
+      for (int it = pre; it < total; ++it) {
+        const int slot = it % n_stages, round = it / n_stages;
+        mbar_wait(&empty[slot], (round - 1) & 1);
+        uint8_t* st = smem + slot * SB;
+        mbar_expect_tx(&full[slot], wbytes + xbytes);
+        tma_load_3d(st, &tw, 0, unit_of(it) * 16, (it % nst) * kSlabs, &full[slot]);
+        tma_load_3d(st + wbytes, &tx, 0, 0, (it % nst) * kSlabs, &full[slot]);
+      }
+      // prefetch the next kernel's first weights into L2 (optional)
+      if (epi.l2_next) {
+        const char* base = static_cast<const char*>(epi.l2_next);
+        const int64_t share = ((epi.l2_next_bytes + gridDim.x - 1) / gridDim.x + 15) & ~15ll;
+        const int64_t lim = epi.l2_next_bytes & ~15ll;
+        const int64_t beg = share * blockIdx.x;
+        const int64_t end = beg + share < lim ? beg + share : lim;
+        for (int64_t off = beg; off < end; off += 32768) {
+          const uint32_t n = static_cast<uint32_t>(end - off < 32768 ? end - off : 32768);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(base + off), "r"(n)
+                       : "memory");
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- math warps ----
+  const int g = lane >> 2, t = lane & 3;
+  pdl_wait();  // the row scalars come from the previous kernel too
+  pdl_trigger();
+  if (epi.ss_zero && blockIdx.x == 0 && threadIdx.x < 32) epi.ss_zero[threadIdx.x] = 0;
+  if (threadIdx.x < M) {
+    if (epi.row_ss) {
+      const unsigned long long rs =
+          __ldcg(reinterpret_cast<const unsigned long long*>(epi.row_ss) + threadIdx.x);
+      s_inv[threadIdx.x] =
+          rsqrtf(__ull2float_rn(rs) / (kSsScale * static_cast<float>(K)) + epi.eps);
+    }
+    if (epi.rope) {
+      const int r_pos = __ldg(epi.row_pos + threadIdx.x);
+      const int r_seq = __ldg(epi.row_seq + threadIdx.x);
+      s_pos[threadIdx.x] = r_pos;
+      s_cell[threadIdx.x] =
+          __ldg(epi.pos2cell + static_cast<int64_t>(r_seq) * epi.pos_stride + r_pos);
     }
   }
-  launch_pdl(gemm_skinny_kernel<MT, U>, dim3(N / 16), dim3(kGemvWarps * 32), 0, s,
-             static_cast<const __nv_bfloat16*>(X), static_cast<const __nv_bfloat16*>(W), Y, M, N,
-             K, y_f32, acc, epi);
+  // k32 step j = warp + 8i of a stage lives in slab j/2, 16-byte chunks
+  // 4*(j&1) + t; smem row R holds chunk c at c ^ (R & 7) (SWIZZLE_128B)
+  const uint32_t ring = smem_u32(smem);
+  uint32_t a_off[NS], x_off[NS][MT];
+  bool xv[MT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) xv[mt] = mt * 8 + g < M;
+#pragma unroll
+  for (int i = 0; i < NS; ++i) {
+    const int j = warp + 8 * i, slab = j >> 1, c = 4 * (j & 1) + t;
+    a_off[i] = slab * 2048 + g * 128 + ((c ^ g) << 4);  // row g; row g+8 is +1024
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const int R = slab * M + (xv[mt] ? mt * 8 + g : 0);
+      x_off[i][mt] = wbytes + R * 128 + ((c ^ (R & 7)) << 4);
+    }
+  }
+  int it = 0;
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    float acc[MT][4];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+    for (int s = 0; s < nst; ++s, ++it) {
+      const int slot = it % n_stages, round = it / n_stages;
+      mbar_wait(&full[slot], round & 1);
+      const uint32_t st = ring + slot * SB;
+#pragma unroll
+      for (int i = 0; i < NS; ++i) {
+        const uint4 a0 = lds128(st + a_off[i]), a1 = lds128(st + a_off[i] + 1024);
+        uint4 bx[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+          bx[mt] = xv[mt] ? lds128(st + x_off[i][mt]) : make_uint4(0, 0, 0, 0);
+        const uint32_t s0[4] = {a0.x, a1.x, a0.y, a1.y};
+        const uint32_t s1[4] = {a0.z, a1.z, a0.w, a1.w};
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          mma_bf16_16816(acc[mt], s0, bx[mt].x, bx[mt].y);
+          mma_bf16_16816(acc[mt], s1, bx[mt].z, bx[mt].w);
+        }
+      }
+      // the reads above (generic proxy) complete before the TMA (async proxy)
+      // may overwrite the slot
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) red[warp][mt][q][lane] = acc[mt][q];
+    named_bar_sync(1, kGemvWarps * 32);
+    unit_epilogue<MT>(red, s_inv, s_pos, s_cell, s_sq, epi, Y, M, N, u * 16, y_f32, accumulate);
+    named_bar_sync(1, kGemvWarps * 32);  // red / s_sq reused by the next unit
+  }
+}
+
+template <int MT, int NS>
+static int launch_ring(const void* X, const void* W, void* Y, int M, int N, int K, int y_f32,
+                       int acc, const ds_skinny_epi& epi, cudaStream_t s) {
+  // DS_RING_KB / DS_RING_CTAS: smem budget per CTA and CTAs per SM (A/B knobs)
+  static const int budget =
+      getenv("DS_RING_KB") ? atoi(getenv("DS_RING_KB")) * 1024 : kRingSmemBudget;
+  static const int per_sm = getenv("DS_RING_CTAS") ? atoi(getenv("DS_RING_CTAS")) : 2;
+  constexpr int KC = 256 * NS;
+  const int SB = ((16 + M) * KC * 2 + 1023) & ~1023;
+  const int red_bytes = kGemvWarps * MT * 4 * 32 * 4;
+  const int fixed = red_bytes + 4096 /* static smem */ + 1024 /* reserved */ + 1024 /* align */;
+  int n_stages = (budget - fixed) / (SB + 16);
+  n_stages = n_stages < 2 ? 2 : n_stages > 12 ? 12 : n_stages;
+  const int smem = 1024 + n_stages * SB + red_bytes + 2 * n_stages * 8;
+  const CUtensorMap* tw = slab_tensor_map(W, N, K, 16, KC / 64);
+  const CUtensorMap* tx = slab_tensor_map(X, M, K, M, KC / 64);
+  if (!tw || !tx) return DS_EUNSUPPORTED;
+  static int attr_smem = 0;
+  if (smem > attr_smem) {
+    cudaFuncSetAttribute(gemm_ring_kernel<MT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
+    cudaFuncSetAttribute(gemm_ring_kernel<MT, NS>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    attr_smem = smem;
+  }
+  const int units = N / 16;
+  const int grid = units < per_sm * kNumSMs ? units : per_sm * kNumSMs;
+  launch_pdl(gemm_ring_kernel<MT, NS>, dim3(grid), dim3((kGemvWarps + 1) * 32), smem, s, Y, M, N,
+             K, y_f32, acc, n_stages, *tw, *tx, epi);
+  return (int)cudaGetLastError();
+}
+
+template <int MT>
+static int run_ring(const void* X, const void* W, void* Y, int M, int N, int K, int y_f32, int acc,
+                    const ds_skinny_epi& epi, cudaStream_t s) {
+  // stage width: 512 columns (measured best at M <= 16), 1024 at M > 16
+  static const int ns = getenv("DS_RING_NS") ? atoi(getenv("DS_RING_NS")) : (MT == 4 ? 4 : 2);
+  if (ns == 4 && K % 1024 == 0) return launch_ring<MT, 4>(X, W, Y, M, N, K, y_f32, acc, epi, s);
+  if (ns == 1) return launch_ring<MT, 1>(X, W, Y, M, N, K, y_f32, acc, epi, s);
+  if (MT == 4 && K % 1024 == 0) return launch_ring<MT, 4>(X, W, Y, M, N, K, y_f32, acc, epi, s);
+  if (K % 512 == 0) return launch_ring<MT, 2>(X, W, Y, M, N, K, y_f32, acc, epi, s);
+  return launch_ring<MT, 1>(X, W, Y, M, N, K, y_f32, acc, epi, s);
 }
 
 static int run(const void* X, const void* W, void* Y, int M, int N, int K, int y_f32, int acc,
                const ds_skinny_epi& epi, cudaStream_t s) {
-  if (M <= 8) launch<1, 8>(X, W, Y, M, N, K, y_f32, acc, epi, s);
-  else if (M <= 16) launch<2, 4>(X, W, Y, M, N, K, y_f32, acc, epi, s);
-  else launch<4, 2>(X, W, Y, M, N, K, y_f32, acc, epi, s);
-  return (int)cudaGetLastError();
+  if (M <= 8) return run_ring<1>(X, W, Y, M, N, K, y_f32, acc, epi, s);
+  if (M <= 16) return run_ring<2>(X, W, Y, M, N, K, y_f32, acc, epi, s);
+  return run_ring<4>(X, W, Y, M, N, K, y_f32, acc, epi, s);
 }
 
 }  // namespace ds

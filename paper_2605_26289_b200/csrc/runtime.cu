@@ -264,6 +264,12 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
   // the skinny GEMM epilogues - wo / down (residual producers) emit
   // h = bf16(x * next norm weight) and per-CTA row sums of x^2, wqkv / gate_up
   // scale their rows by the inverse RMS; gate_up emits silu(g)*u directly.
+  // bytes of the next projection's weights each skinny GEMM's last wave pulls
+  // into L2 (DS_L2_NEXT_MB overrides for A/B measurements; 0 disables)
+  static const int64_t l2_next_bytes = [] {
+    const char* e = getenv("DS_L2_NEXT_MB");
+    return static_cast<int64_t>(e ? atof(e) * 1048576.0 : 12.0 * 1048576.0);
+  }();
   const bool fused = T <= 32 && H % 256 == 0 && F % 256 == 0 && (nh * hd) % 256 == 0 &&
                      QKV % 16 == 0 && hd == 128;
   // two ss buffers, each producer clearing the one its consumer already read
@@ -324,6 +330,8 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
     const __nv_bfloat16* wd_l = wd + static_cast<size_t>(l) * H * F;
     if (fused) {
       ds_skinny_epi eo{};
+      eo.l2_next = wgu_l;
+      eo.l2_next_bytes = l2_next_bytes;
       eo.ss_out = ss_mlp;
       eo.ss_zero = ss_attn;
       eo.h_out = b.h;
@@ -333,10 +341,15 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
       eg.row_ss = ss_mlp;
       eg.eps = m->rms_eps;
       eg.swiglu = 1;
+      eg.l2_next = wd_l;
+      eg.l2_next_bytes = l2_next_bytes;
       DS_CHECK(ds_gemm_skinny_ex(b.h, wgu_l, b.act, T, 2 * F, H, 0, 0, &eg, stream));
       ds_skinny_epi ed{};
       ed.ss_out = ss_attn;  // (last layer: unused, keeps the clear/fill cycle uniform)
       ed.ss_zero = ss_mlp;
+      ed.l2_next = l + 1 < L ? static_cast<const void*>(wqkv_l + static_cast<size_t>(QKV) * H)
+                             : m->lm_head;
+      ed.l2_next_bytes = l2_next_bytes;
       if (l + 1 < L) {
         ed.h_out = b.h;
         ed.h_w = an + static_cast<size_t>(l + 1) * H;

@@ -50,4 +50,28 @@ const CUtensorMap* kv_tensor_map(const void* base, int64_t rows, int box_rows) {
   return &(cache[key] = map);
 }
 
+const CUtensorMap* slab_tensor_map(const void* base, int64_t rows, int64_t cols, int box_rows,
+                                   int box_slabs) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int64_t, int64_t, int, int>, CUtensorMap> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_tuple(base, rows, cols, box_rows, box_slabs);
+  auto it = cache.find(key);
+  if (it != cache.end()) return &it->second;
+  auto fn = encode_fn();
+  if (!fn || cols % 64) return nullptr;
+  CUtensorMap map;
+  const cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols / 64)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols) * 2, 128};
+  const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows),
+                             static_cast<cuuint32_t>(box_slabs)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return nullptr;
+  return &(cache[key] = map);
+}
+
 }  // namespace ds
