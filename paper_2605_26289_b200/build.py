@@ -13,12 +13,15 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libdeltaserve_b200.so")
+# DS_LIB_OUT / DS_NVCC_EXTRA: an instrumented or A/B variant built elsewhere
+# (e.g. -DDS_K7_TRACE); the default is the in-tree product library
+LIB = os.environ.get("DS_LIB_OUT") or os.path.join(HERE, "libdeltaserve_b200.so")
+BUILD = os.path.join(os.path.dirname(LIB), "_build") if os.environ.get("DS_LIB_OUT") else \
+    os.path.join(HERE, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
-         "-I" + os.path.join(ROOT, "include")]
+         "-I" + os.path.join(ROOT, "include")] + os.environ.get("DS_NVCC_EXTRA", "").split()
 
 SOURCES = ["policy.cu", "kvmeta.cu", "layers.cu", "attn_split.cu", "attn_decode.cu", "attn_decode_tc.cu",
            "attn_prefill_sm100.cu",

@@ -41,6 +41,21 @@
 
 namespace ds {
 
+#ifdef DS_K7_TRACE
+// debug build only: per-CTA globaltimer stamps (tools/k7_trace.py)
+__device__ unsigned long long g_k7_trace[1024][8];
+DS_DEVICE unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define K7_STAMP(i)                                                                        \
+  if (threadIdx.x == 0)                                                                    \
+  g_k7_trace[(blockIdx.z * gridDim.y + blockIdx.y) & 1023][i] = gtime()
+#else
+#define K7_STAMP(i)
+#endif
+
 namespace {
 constexpr int kD = 128;
 constexpr int kTile = 128;                   // keys per stage
@@ -71,22 +86,7 @@ DS_DEVICE uint32_t movm_t(uint32_t x) {
   asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(y) : "r"(x));
   return y;
 }
-// merge the 8 consumer warps' online-softmax states for (row r, column d):
-// returns the row max; L = sum of exp, acc = weighted O
-DS_DEVICE float merged_row(const float* msm, const float* lsm, const float* osm, int r, int d,
-                           float& L, float& acc) {
-  float mm = -INFINITY;
-#pragma unroll
-  for (int w = 0; w < kConsumers; ++w) mm = fmaxf(mm, msm[w * kMaxRows + r]);
-  const float mref = mm == -INFINITY ? 0.f : mm;
-#pragma unroll
-  for (int w = 0; w < kConsumers; ++w) {
-    const float sc = fast_exp2(msm[w * kMaxRows + r] - mref);
-    L += lsm[w * kMaxRows + r] * sc;
-    acc += osm[(w * kMaxRows + r) * kD + d] * sc;
-  }
-  return mm;
-}
+constexpr int kOsmStride = kD + 4;  // padded [warp][row] stride of the merge buffer (no conflicts)
 }  // namespace
 
 // one-shot hint from the forward runtime: bytes to pull into L2 while the
@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     int* __restrict__ counters, const __grid_constant__ CUtensorMap tmk,
     const __grid_constant__ CUtensorMap tmv, const char* __restrict__ l2p, int64_t l2_bytes,
     int last_merge) {
+  K7_STAMP(6);
   const bool cluster_merge = max_splits <= kDecodeMaxCluster;  // launched with clusters
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // SW128 alignment
@@ -235,7 +236,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     }
   } else {
     // ================= consumers =================
+    K7_STAMP(0);
     pdl_wait();  // q comes from the preceding projection
+    K7_STAMP(1);
     const int g = lane >> 2, t = lane & 3;
     // Q^T as the B operand: qb[j][kk] covers rows 8j + g, d [16kk + 2t, +1] and
     // [16kk + 8 + 2t, +1] - registers for NT <= 2, else a swizzled smem copy
@@ -291,6 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     for (int it = 0; it < ntiles; ++it) {
       const int st = it % kStages;
       mbar_wait(&full[st], (it / kStages) & 1);
+      if (it == 0) K7_STAMP(2);
       const uint32_t ks_u = smem_u32(smem + st * kStageBytes), vs_u = ks_u + kHalfBytes;
       float s[NT][4];
   #pragma unroll
@@ -376,11 +380,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
       if (lane == 0) mbar_arrive(&empty[st]);
     }
     named_bar_sync(1, kConsumers * 32);  // all consumers done with the ring
+    K7_STAMP(3);
 
     // ---- merge the 8 warps' states (ring memory is free now) ----
-    float* osm = reinterpret_cast<float*>(smem);     // [8][24][128]
-    float* msm = osm + kConsumers * kMaxRows * kD;   // [8][24]
-    float* lsm = msm + kConsumers * kMaxRows;        // [8][24]
+    // O partials into a padded buffer, then per-row weights 2^(m_w - max)/L
+    // computed once, then each output element is an 8-term dot product with
+    // all loads independent (no per-element exp, no serialised chains)
+    float* osm = reinterpret_cast<float*>(smem);             // [8][24][132]
+    float* msm = osm + kConsumers * kMaxRows * kOsmStride;   // [8][24]
+    float* lsm = msm + kConsumers * kMaxRows;                // [8][24]
+    float* wsm = lsm + kConsumers * kMaxRows;                // [24][8] row weights
+    float* rlse = wsm + kMaxRows * kConsumers;               // [24] row log2-sum-exp
   #pragma unroll
     for (int j = 0; j < NT; ++j) {
   #pragma unroll
@@ -399,44 +409,65 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
       for (int i = 0; i < 8; ++i)
   #pragma unroll
         for (int q = 0; q < 4; ++q)
-          osm[(warp * kMaxRows + 8 * j + 2 * t + (q & 1)) * kD + 16 * i + g + ((q >> 1) << 3)] =
-              o[i][j][q];
+          osm[(warp * kMaxRows + 8 * j + 2 * t + (q & 1)) * kOsmStride + 16 * i + g +
+              ((q >> 1) << 3)] = o[i][j][q];
     }
     named_bar_sync(1, kConsumers * 32);
-    if (plan.n_splits == 1) {  // no split: write the rows directly
-      for (int idx = tid; idx < R * kD; idx += kConsumers * 32) {
-        const int r = idx / kD, d = idx - r * kD;
-        float L = 0.f, acc = 0.f;
-        merged_row(msm, lsm, osm, r, d, L, acc);
+    if (tid < R) {
+      float mv[kConsumers], lv[kConsumers];
+  #pragma unroll
+      for (int w = 0; w < kConsumers; ++w) {
+        mv[w] = msm[w * kMaxRows + tid];
+        lv[w] = lsm[w * kMaxRows + tid];
+      }
+      float mm = -INFINITY;
+  #pragma unroll
+      for (int w = 0; w < kConsumers; ++w) mm = fmaxf(mm, mv[w]);
+      const float mref = mm == -INFINITY ? 0.f : mm;
+      float L = 0.f;
+  #pragma unroll
+      for (int w = 0; w < kConsumers; ++w) {
+        mv[w] = fast_exp2(mv[w] - mref);
+        L += lv[w] * mv[w];
+      }
+      const float inv = L > 0.f ? 1.f / L : 0.f;
+  #pragma unroll
+      for (int w = 0; w < kConsumers; ++w) wsm[tid * kConsumers + w] = mv[w] * inv;
+      rlse[tid] = L > 0.f ? mm + __log2f(L) : -INFINITY;
+    }
+    named_bar_sync(1, kConsumers * 32);
+    const int64_t base =
+        plan.n_splits > 1 && !cluster_merge ? attn_partial_base(entries, e, n_entries, nh, nkv, 1)
+                                            : 0;
+    for (int idx = tid; idx < R * kD; idx += kConsumers * 32) {
+      const int r = idx / kD, d = idx - r * kD;
+      float ov[kConsumers];
+  #pragma unroll
+      for (int w = 0; w < kConsumers; ++w) ov[w] = osm[(w * kMaxRows + r) * kOsmStride + d];
+      float val = 0.f;
+  #pragma unroll
+      for (int w = 0; w < kConsumers; ++w) val += wsm[r * kConsumers + w] * ov[w];
+      if (plan.n_splits == 1) {  // no split: write the row directly
         const int ti = r / G, gi = r - ti * G;
         out[static_cast<int64_t>(en.q_start + ti) * nh * kD + (kh * G + gi) * kD + d] =
-            __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+            __float2bfloat16_rn(val);
+      } else if (cluster_merge) {  // this split's normalised rows -> its cluster buffer
+        cval[r * kD + d] = val;
+        if (d == 0) clse[r] = rlse[r];
+      } else {  // -> global partials
+        const int64_t slot = (base + static_cast<int64_t>(split) * R + r) * nkv + kh;
+        part_o[slot * kD + d] = val;
+        if (d == 0) part_lse[slot] = rlse[r];
       }
-    } else {  // this split's normalised rows and log-sum-exp
-      const int64_t base = attn_partial_base(entries, e, n_entries, nh, nkv, 1);
-      for (int idx = tid; idx < R * kD; idx += kConsumers * 32) {
-        const int r = idx / kD, d = idx - r * kD;
-        float L = 0.f, acc = 0.f;
-        const float mm = merged_row(msm, lsm, osm, r, d, L, acc);
-        const float val = L > 0.f ? acc / L : 0.f;
-        const float lse = L > 0.f ? mm + __log2f(L) : -INFINITY;
-        if (cluster_merge) {  // -> this CTA's cluster buffer
-          cval[r * kD + d] = val;
-          if (d == 0) clse[r] = lse;
-        } else {  // -> global partials for the combine kernel
-          const int64_t slot = (base + static_cast<int64_t>(split) * R + r) * nkv + kh;
-          part_o[slot * kD + d] = val;
-          if (d == 0) part_lse[slot] = lse;
-        }
-      }
-      if (!cluster_merge && last_merge)  // the last split to arrive merges the partials
-        decode_global_merge(part_o, part_lse, base, R, plan.n_splits, nkv, kh,
-                            counters + e * nkv + kh, cval, reinterpret_cast<int*>(clse), tid,
-                            kConsumers * 32, 1, en, nh, G, out);
     }
+    if (plan.n_splits > 1 && !cluster_merge && last_merge)  // last split to arrive merges
+      decode_global_merge(part_o, part_lse, base, R, plan.n_splits, nkv, kh,
+                          counters + e * nkv + kh, cval, reinterpret_cast<int*>(clse), tid,
+                          kConsumers * 32, 1, en, nh, G, out);
   }
 
   // ---- split merge across the cluster (distributed shared memory) ----
+  K7_STAMP(4);
   if (cluster_merge && plan.n_splits > 1) {
     cluster_sync_all();  // every split's rows are in its cbuf
     if (tid < kConsumers * 32)
@@ -448,8 +479,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
   // retires - any earlier trigger (even after the main loop) lets its CTAs
   // onto the SMs while the attention runs, and the whole forward was measured
   // ~25% slower.
+  K7_STAMP(5);
   pdl_trigger();
 }
+
+#ifdef DS_K7_TRACE
+extern "C" int ds_debug_k7_trace(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_k7_trace, sizeof(g_k7_trace));
+}
+#endif
 
 int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_entry* entries_dev,
                        int n_entries, const void* k_pool, const void* v_pool, int64_t head_stride,

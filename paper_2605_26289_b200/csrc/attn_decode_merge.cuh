@@ -18,29 +18,37 @@ DS_DEVICE void decode_cluster_merge(const float* cval, const float* clse, float*
                                     __nv_bfloat16* __restrict__ out) {
   constexpr int kD = 128;
   const uint32_t rank = cluster_ctarank();
-  // per-row split weights 2^(lse_p - max) / sum, in split order
+  // per-row split weights 2^(lse_p - max) / sum, in split order; all remote
+  // loads are issued before any is consumed (DSMEM round trips overlap)
   for (int i = tid; i < R; i += nthreads) {
+    float lv[kDecodeMaxCluster];
+#pragma unroll
+    for (int p = 0; p < kDecodeMaxCluster; ++p)
+      lv[p] = p < n_splits ? dsmem_ld_f32(dsmem_map(smem_u32(clse + i), p)) : -INFINITY;
     float lmax = -INFINITY;
-    for (int p = 0; p < n_splits; ++p)
-      lmax = fmaxf(lmax, dsmem_ld_f32(dsmem_map(smem_u32(clse + i), p)));
+#pragma unroll
+    for (int p = 0; p < kDecodeMaxCluster; ++p) lmax = fmaxf(lmax, lv[p]);
     float wsum = 0.f;
-    for (int p = 0; p < n_splits; ++p) {
-      const float lse = dsmem_ld_f32(dsmem_map(smem_u32(clse + i), p));
-      const float w = lse == -INFINITY ? 0.f : exp2f(lse - lmax);
-      cw[i * kDecodeMaxCluster + p] = w;
-      wsum += w;
+#pragma unroll
+    for (int p = 0; p < kDecodeMaxCluster; ++p) {
+      lv[p] = lv[p] == -INFINITY ? 0.f : exp2f(lv[p] - lmax);
+      wsum += lv[p];
     }
     const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
-    for (int p = 0; p < n_splits; ++p) cw[i * kDecodeMaxCluster + p] *= inv;
+#pragma unroll
+    for (int p = 0; p < kDecodeMaxCluster; ++p) cw[i * kDecodeMaxCluster + p] = lv[p] * inv;
   }
   named_bar_sync(bar_id, nthreads);
   for (int idx = static_cast<int>(rank) * nthreads + tid; idx < R * kD; idx += cluster * nthreads) {
     const int r = idx / kD, d = idx - r * kD;
     const uint32_t a = smem_u32(cval + r * kD + d);
+    float v[kDecodeMaxCluster];
+#pragma unroll
+    for (int p = 0; p < kDecodeMaxCluster; ++p)
+      v[p] = p < n_splits ? dsmem_ld_f32(dsmem_map(a, p)) : 0.f;
     float acc = 0.f;
-#pragma unroll 4
-    for (int p = 0; p < n_splits; ++p)
-      acc += cw[r * kDecodeMaxCluster + p] * dsmem_ld_f32(dsmem_map(a, p));
+#pragma unroll
+    for (int p = 0; p < kDecodeMaxCluster; ++p) acc += cw[r * kDecodeMaxCluster + p] * v[p];
     const int ti = r / G, gi = r - ti * G;
     out[static_cast<int64_t>(en.q_start + ti) * nh * kD + (kh * G + gi) * kD + d] =
         __float2bfloat16_rn(acc);

@@ -214,7 +214,7 @@ DS_DEVICE uint32_t dsmem_map(uint32_t smem_addr, uint32_t rank) {
 }
 DS_DEVICE float dsmem_ld_f32(uint32_t cluster_addr) {
   float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];\n" : "=f"(v) : "r"(cluster_addr) : "memory");
+  asm volatile("ld.shared::cluster.f32 %0, [%1];\n" : "=f"(v) : "r"(cluster_addr));
   return v;
 }
 }  // namespace ds
