@@ -104,7 +104,11 @@ int launch_attn_decode_tc(const ds_entry* entries_dev, int n_entries, const void
                           int max_splits, float scale, void* out, float* part_o, float* part_lse,
                           const void* l2p, int64_t l2_bytes, cudaStream_t stream);
 
-int decode_smem_bytes() { return 1024 + kStages * kStageBytes + kQBytes + 2 * kStages * 8; }
+constexpr int kBarBytes = 64;                                     // full/empty mbarriers
+constexpr int kMergeBytes = (kMaxRows * kD + kMaxRows + kMaxRows * 8) * 4;  // cval/clse/cw
+int decode_smem_bytes(int n_stages) {
+  return 1024 + n_stages * kStageBytes + kQBytes + kBarBytes + kMergeBytes;
+}
 
 template <int NT>  // n-tiles of 8 packed query rows
 __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
@@ -115,18 +119,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     float* __restrict__ part_o, float* __restrict__ part_lse, int64_t head_stride,
     int* __restrict__ counters, const __grid_constant__ CUtensorMap tmk,
     const __grid_constant__ CUtensorMap tmv, const char* __restrict__ l2p, int64_t l2_bytes,
-    int last_merge) {
+    int last_merge, int n_stages, int early_trigger) {
   K7_STAMP(6);
   const bool cluster_merge = max_splits <= kDecodeMaxCluster;  // launched with clusters
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // SW128 alignment
-  uint8_t* qs = smem + kStages * kStageBytes;
-  // split-merge buffers inside the ring, past the warp-merge area (used after both)
-  float* cval = reinterpret_cast<float*>(smem + 128 * 1024);  // [R][128] this split's rows
-  float* clse = cval + kMaxRows * kD;                          // [R]
-  float* cw = clse + kMaxRows;                                 // [R][16] split weights
+  // [ring: n_stages x 64 KB][q 8 KB][barriers][split-merge buffers].  With one
+  // stage (every split one tile) the CTA needs < 100 KB, so the next
+  // projection's CTA fits beside it and fills its weight ring meanwhile.
+  uint8_t* qs = smem + n_stages * kStageBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(qs + kQBytes);
   uint64_t* empty = full + kStages;
+  float* cval = reinterpret_cast<float*>(qs + kQBytes + kBarBytes);  // [R][128] this split's rows
+  float* clse = cval + kMaxRows * kD;                                 // [R]
+  float* cw = clse + kMaxRows;                                        // [R][8] split weights
 
   const int e = blockIdx.z / max_splits;
   const int split = blockIdx.z - e * max_splits;
@@ -143,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   if (warp == kConsumers && lane == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < n_stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumers);
     }
@@ -174,8 +180,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     bool waited = false;
     for (int it = 0; it < ntiles; ++it) {
       cells(it + 2, nx2);
-      const int st = it % kStages;
-      if (it >= kStages) mbar_wait(&empty[st], ((it / kStages) - 1) & 1);
+      const int st = it % n_stages;
+      if (it >= n_stages) mbar_wait(&empty[st], ((it / n_stages) - 1) & 1);
       uint8_t* ks = smem + st * kStageBytes;
       uint8_t* vs = ks + kHalfBytes;
       const int kt = k_begin + it * kTile;
@@ -222,6 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
       }
     }
     if (!waited) pdl_wait();
+    if (early_trigger) pdl_trigger();  // combine kernel / co-resident projection
     if (l2p && lane == 0) {  // this CTA's share of the next projection's weights -> L2
       const int64_t n_cta = static_cast<int64_t>(gridDim.y) * gridDim.z;
       const int64_t share = ((l2_bytes + n_cta - 1) / n_cta + 15) & ~15ll;
@@ -239,6 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     K7_STAMP(0);
     pdl_wait();  // q comes from the preceding projection
     K7_STAMP(1);
+    if (early_trigger) pdl_trigger();
     const int g = lane >> 2, t = lane & 3;
     // Q^T as the B operand: qb[j][kk] covers rows 8j + g, d [16kk + 2t, +1] and
     // [16kk + 8 + 2t, +1] - registers for NT <= 2, else a swizzled smem copy
@@ -292,8 +300,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     const int v_row = kw + (lane & 7) + ((lane >> 4) << 3), v_chunk = (lane >> 3) & 1;
 
     for (int it = 0; it < ntiles; ++it) {
-      const int st = it % kStages;
-      mbar_wait(&full[st], (it / kStages) & 1);
+      const int st = it % n_stages;
+      mbar_wait(&full[st], (it / n_stages) & 1);
       if (it == 0) K7_STAMP(2);
       const uint32_t ks_u = smem_u32(smem + st * kStageBytes), vs_u = ks_u + kHalfBytes;
       float s[NT][4];
@@ -383,56 +391,95 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     K7_STAMP(3);
 
     // ---- merge the 8 warps' states (ring memory is free now) ----
-    // O partials into a padded buffer, then per-row weights 2^(m_w - max)/L
-    // computed once, then each output element is an 8-term dot product with
-    // all loads independent (no per-element exp, no serialised chains)
-    float* osm = reinterpret_cast<float*>(smem);             // [8][24][132]
-    float* msm = osm + kConsumers * kMaxRows * kOsmStride;   // [8][24]
-    float* lsm = msm + kConsumers * kMaxRows;                // [8][24]
-    float* wsm = lsm + kConsumers * kMaxRows;                // [24][8] row weights
-    float* rlse = wsm + kMaxRows * kConsumers;               // [24] row log2-sum-exp
+    // Two rounds through a [4][24][132] buffer (fits the one-stage ring):
+    // warps 4-7 publish (m, l, O), warps 0-3 fold their partner's state into
+    // registers and publish the result; then per-row weights are computed once
+    // and every output element is a 4-term dot product (independent loads).
+    constexpr int kHalfW = kConsumers / 2;
+    float* osm = reinterpret_cast<float*>(smem);             // [4][24][132]
+    float* msm = osm + kHalfW * kMaxRows * kOsmStride;       // [4][24]
+    float* lsm = msm + kHalfW * kMaxRows;                    // [4][24]
+    float* wsm = lsm + kHalfW * kMaxRows;                    // [24][4] row weights
+    float* rlse = wsm + kMaxRows * kHalfW;                   // [24] row log2-sum-exp
+    const int slotw = warp & (kHalfW - 1);
   #pragma unroll
-    for (int j = 0; j < NT; ++j) {
+    for (int j = 0; j < NT; ++j)
   #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float l = l_run[j][h];
         l += __shfl_xor_sync(0xffffffffu, l, 4);
         l += __shfl_xor_sync(0xffffffffu, l, 8);
         l += __shfl_xor_sync(0xffffffffu, l, 16);
-        const int r = 8 * j + 2 * t + h;
-        if (g == 0) {
-          msm[warp * kMaxRows + r] = m_run[j][h];
-          lsm[warp * kMaxRows + r] = l;
-        }
+        l_run[j][h] = l;  // the warp's row total
       }
+    auto publish = [&]() {
   #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < NT; ++j) {
   #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          osm[(warp * kMaxRows + 8 * j + 2 * t + (q & 1)) * kOsmStride + 16 * i + g +
-              ((q >> 1) << 3)] = o[i][j][q];
+        for (int h = 0; h < 2; ++h) {
+          const int r = 8 * j + 2 * t + h;
+          if (g == 0) {
+            msm[slotw * kMaxRows + r] = m_run[j][h];
+            lsm[slotw * kMaxRows + r] = l_run[j][h];
+          }
+        }
+  #pragma unroll
+        for (int i = 0; i < 8; ++i)
+  #pragma unroll
+          for (int q = 0; q < 4; ++q)
+            osm[(slotw * kMaxRows + 8 * j + 2 * t + (q & 1)) * kOsmStride + 16 * i + g +
+                ((q >> 1) << 3)] = o[i][j][q];
+      }
+    };
+    if (warp >= kHalfW) publish();
+    named_bar_sync(1, kConsumers * 32);
+    if (warp < kHalfW) {  // fold the partner warp (warp + 4): same fragment positions
+  #pragma unroll
+      for (int j = 0; j < NT; ++j)
+  #pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = 8 * j + 2 * t + h;
+          const float mb = msm[slotw * kMaxRows + r], lb = lsm[slotw * kMaxRows + r];
+          const float ma = m_run[j][h];
+          const float mm = fmaxf(ma, mb);
+          const float mref = mm == -INFINITY ? 0.f : mm;
+          const float sa = fast_exp2(ma - mref), sb = fast_exp2(mb - mref);
+          m_run[j][h] = mm;
+          l_run[j][h] = l_run[j][h] * sa + lb * sb;
+  #pragma unroll
+          for (int i = 0; i < 8; ++i)
+  #pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if ((q & 1) == h) {
+                const float ob = osm[(slotw * kMaxRows + r) * kOsmStride + 16 * i + g +
+                                     ((q >> 1) << 3)];
+                o[i][j][q] = o[i][j][q] * sa + ob * sb;
+              }
+        }
     }
     named_bar_sync(1, kConsumers * 32);
+    if (warp < kHalfW) publish();
+    named_bar_sync(1, kConsumers * 32);
     if (tid < R) {
-      float mv[kConsumers], lv[kConsumers];
+      float mv[kHalfW], lv[kHalfW];
   #pragma unroll
-      for (int w = 0; w < kConsumers; ++w) {
+      for (int w = 0; w < kHalfW; ++w) {
         mv[w] = msm[w * kMaxRows + tid];
         lv[w] = lsm[w * kMaxRows + tid];
       }
       float mm = -INFINITY;
   #pragma unroll
-      for (int w = 0; w < kConsumers; ++w) mm = fmaxf(mm, mv[w]);
+      for (int w = 0; w < kHalfW; ++w) mm = fmaxf(mm, mv[w]);
       const float mref = mm == -INFINITY ? 0.f : mm;
       float L = 0.f;
   #pragma unroll
-      for (int w = 0; w < kConsumers; ++w) {
+      for (int w = 0; w < kHalfW; ++w) {
         mv[w] = fast_exp2(mv[w] - mref);
         L += lv[w] * mv[w];
       }
       const float inv = L > 0.f ? 1.f / L : 0.f;
   #pragma unroll
-      for (int w = 0; w < kConsumers; ++w) wsm[tid * kConsumers + w] = mv[w] * inv;
+      for (int w = 0; w < kHalfW; ++w) wsm[tid * kHalfW + w] = mv[w] * inv;
       rlse[tid] = L > 0.f ? mm + __log2f(L) : -INFINITY;
     }
     named_bar_sync(1, kConsumers * 32);
@@ -441,12 +488,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
                                             : 0;
     for (int idx = tid; idx < R * kD; idx += kConsumers * 32) {
       const int r = idx / kD, d = idx - r * kD;
-      float ov[kConsumers];
+      float ov[kHalfW];
   #pragma unroll
-      for (int w = 0; w < kConsumers; ++w) ov[w] = osm[(w * kMaxRows + r) * kOsmStride + d];
+      for (int w = 0; w < kHalfW; ++w) ov[w] = osm[(w * kMaxRows + r) * kOsmStride + d];
       float val = 0.f;
   #pragma unroll
-      for (int w = 0; w < kConsumers; ++w) val += wsm[r * kConsumers + w] * ov[w];
+      for (int w = 0; w < kHalfW; ++w) val += wsm[r * kHalfW + w] * ov[w];
       if (plan.n_splits == 1) {  // no split: write the row directly
         const int ti = r / G, gi = r - ti * G;
         out[static_cast<int64_t>(en.q_start + ti) * nh * kD + (kh * G + gi) * kD + d] =
@@ -475,10 +522,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
                            en, nh, kh, G, out);
     cluster_sync_all();  // peers keep their smem until every read is done
   }
-  // PDL: the dependent is the next projection, launched only as this grid
-  // retires - any earlier trigger (even after the main loop) lets its CTAs
-  // onto the SMs while the attention runs, and the whole forward was measured
-  // ~25% slower.
+  // PDL: when the dependent is the next projection it launches only as this
+  // grid retires - an earlier trigger (even after the main loop) let its CTAs
+  // onto the SMs while the attention ran and the forward was measured ~25%
+  // slower; the small combine kernel (R > 8 beyond a cluster) is triggered
+  // early above.
   K7_STAMP(5);
   pdl_trigger();
 }
@@ -495,17 +543,23 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
                        int max_splits, float scale, void* out, float* part_o, float* part_lse,
                        int* counters, cudaStream_t stream) {
   if (max_R > kMaxRows) return DS_EUNSUPPORTED;
-  int max_kv = 0;
+  int max_kv = 0, max_split_len = 0;
   for (int e = 0; e < n_entries; ++e) {
     const int kv = entries_host[e].past + entries_host[e].q_len;
     max_kv = kv > max_kv ? kv : max_kv;
+    const AttnSplitPlan p = attn_split_plan(1, kv, nkv, n_entries, 1);
+    max_split_len = p.split_len > max_split_len ? p.split_len : max_split_len;
   }
-  const int smem = decode_smem_bytes();
+  // one K/V tile per split (short prefixes): a one-stage ring keeps the CTA
+  // small enough for the next projection's CTA to sit beside it
+  const int n_stages = max_split_len <= kTile ? 1 : kStages;
+  const int smem = decode_smem_bytes(n_stages);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_decode_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(attn_decode_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(attn_decode_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int mx = decode_smem_bytes(kStages);
+    cudaFuncSetAttribute(attn_decode_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(attn_decode_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(attn_decode_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     attr = true;
   }
   const CUtensorMap* tk = kv_tensor_map(k_pool, static_cast<int64_t>(nkv) * head_stride, kTile);
@@ -517,6 +571,11 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
   // more splits than a cluster: up to 8 rows the last split to arrive merges
   // (cheap: R*128 values), more rows go to attn_combine_kernel (attn_split.cu)
   const int last_merge = max_R <= kDecodeLastMergeRows;
+  // PDL trigger right after the dependency wait when the dependent is the
+  // combine kernel, or (DS_K7_EARLY) when a one-stage CTA leaves room for the
+  // next projection's
+  static const int early_env = getenv("DS_K7_EARLY") ? atoi(getenv("DS_K7_EARLY")) : 1;
+  const int early = (max_splits > kDecodeMaxCluster && !last_merge) || (early_env && n_stages == 1);
   const char* l2p = static_cast<const char*>(g_l2_ptr);
   const int64_t l2_bytes = g_l2_bytes;
   g_l2_ptr = nullptr;
@@ -536,14 +595,14 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
                          max_splits, static_cast<const __nv_bfloat16*>(k_pool),
                          static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv,
                          sl2, static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride,
-                         counters, *tk, *tv, l2p, l2_bytes, last_merge);
+                         counters, *tk, *tv, l2p, l2_bytes, last_merge, n_stages, early);
   else
     launch_pdl(kern, grid, dim3(kThreads), smem, stream, static_cast<const __nv_bfloat16*>(qkv),
                stride, entries_dev, n_entries, max_splits,
                static_cast<const __nv_bfloat16*>(k_pool),
                static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv, sl2,
                static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride, counters, *tk,
-               *tv, l2p, l2_bytes, last_merge);
+               *tv, l2p, l2_bytes, last_merge, n_stages, early);
   return (int)cudaGetLastError();
 }
 

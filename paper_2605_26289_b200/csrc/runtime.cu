@@ -309,8 +309,10 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
     }
     // the attention leaves HBM mostly idle (short contexts): K7's producer
     // warps pull wo's weights into L2 for the next projection meanwhile
-    if (fused) set_attn_l2_prefetch(wo + static_cast<size_t>(l) * H * nh * hd,
-                                    static_cast<int64_t>(H) * nh * hd * 2);
+    static const double wo_l2_frac = getenv("DS_WO_L2_FRAC") ? atof(getenv("DS_WO_L2_FRAC")) : 1.0;
+    if (fused && wo_l2_frac > 0)
+      set_attn_l2_prefetch(wo + static_cast<size_t>(l) * H * nh * hd,
+                           static_cast<int64_t>(wo_l2_frac * H * nh * hd * 2) & ~15ll);
     if (n_long > 0 && n_long < a->n_entries) {  // mixed plan: K6 for prefill chunks, K7 rest
       DS_CHECK(ds_attention(b.qkv, a->entries_host, a->entries, n_long, T, kp + l * kv_layer,
                             vp + l * kv_layer, kv->capacity, kv->pos2cell, kv->pos_stride, nh,

@@ -11,13 +11,14 @@ from paper_2605_26289_b200.engine import EntryRequest, GpuEngine
 from paper_2605_26289_b200.kvcache import UnifiedKvCache
 
 model, past, q = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+edges = len(sys.argv) > 4 and sys.argv[4] == "edges"
 cfg = CoreConfig(model=model, capacity_cells=past + q + 512)
 kv = UnifiedKvCache(cfg.capacity_cells)
 eng = GpuEngine(cfg, kv, n_seqs=1)
 toks = [(7 * i + 3) % 30000 for i in range(past + q + 8)]
 eng.load_prompt(0, toks, 0, 0xCBF29CE484222325)
 kv.append_cells(0, past + q)
-kind = _lib.ENTRY_VERIFY if q > 1 else _lib.ENTRY_DECODE
+kind = _lib.ENTRY_PREFILL if q > 24 else _lib.ENTRY_VERIFY if q > 1 else _lib.ENTRY_DECODE
 req = EntryRequest(kind, 0, past, toks[past:past + q], toks, n_draft=q - 1 if q > 1 else 0)
 for _ in range(5):
     eng.run([req], count=False)
@@ -33,6 +34,16 @@ s = cfg.shape
 g_qkv = s.qkv_width // 16
 starts = [i - 1 for i, e in enumerate(main) if "attn_" in e["name"] and "combine" not in e["name"]]
 i0, i1 = starts[4], starts[5]
+if edges:  # the forward's head (up to layer 1) and tail (from the last layer's attention)
+    sel = main[: starts[1]] + main[starts[-1]:]
+    t0 = main[0]["ts"]
+    print(f"past={past} q={q} forward {main[-1]['ts'] + main[-1]['dur'] - t0:.1f} us (edges)")
+    for e in sorted(ev, key=lambda e: e["ts"]):
+        if e in sel or e not in main:
+            nm = e["name"].split("(")[0].replace("void ds::", "").replace("ds::", "")[:28]
+            print(f"  s{e['args'].get('stream')} {nm:28s} grid={str(e['args'].get('grid')):16s} "
+                  f"start {e['ts'] - t0:8.2f} end {e['ts'] + e['dur'] - t0:8.2f} dur {e['dur']:7.2f}")
+    sys.exit(0)
 t0 = main[i0]["ts"]
 print(f"past={past} q={q} forward {main[-1]['ts'] + main[-1]['dur'] - main[0]['ts']:.1f} us")
 t1 = main[i1]["ts"]
