@@ -316,12 +316,12 @@ def gemm_roofline(torch, eng, rows: int, peaks) -> dict:
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
-            traffic = json.load(fh).get("gemm_skinny_traffic_bytes_per_byte")
+            traffic = json.load(fh).get("gemm_ring_traffic_bytes_per_byte")
         if traffic is not None:
             traffic = round(traffic * algo)
     except Exception:
         traffic = None
-    return {"kernel": "gemm_skinny_kernel (decode/verify weight-streaming projections, "
+    return {"kernel": "gemm_ring_kernel (decode/verify weight-streaming projections, "
                       f"M={rows})", "bound": "hbm",
             "achieved": round(algo / per_launch / 1e9, 1), "peak": peaks[0], "unit": "GB/s",
             "frac": round(algo / per_launch / 1e9 / peaks[0], 3), "traffic": traffic,

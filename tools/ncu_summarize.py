@@ -56,7 +56,7 @@ def main(tag: str) -> None:
     md = [f"# ncu summaries ({tag})\n",
           "Captured with `tools/profile_round.sh` under gpurun on one B200 "
           "(`ncu --set full --clock-control none`); numbers per launch.\n"]
-    for name in ("ncu_gemm_skinny", "ncu_k7_decode", "ncu_k6_prefill"):
+    for name in ("ncu_gemm_ring", "ncu_k7_decode", "ncu_k7_decode_q1", "ncu_k6_prefill"):
         rep = os.path.join(OUT, name + ".ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -106,11 +106,16 @@ def main(tag: str) -> None:
         summary["launch_share"] = share
         with open(os.path.join(dst, "launches.csv"), "w") as fh:
             fh.write(open(lpath).read())
-    g = summary.get("ncu_gemm_skinny")
+    g = summary.get("ncu_gemm_ring")
     if g:
-        # traffic per algorithmic byte of the first capture (weights dominate)
-        r0 = g[0]
-        summary["gemm_skinny_dram"] = [r0["dram__bytes_read.sum"], r0["dram__bytes_write.sum"]]
+        summary["gemm_ring_dram"] = [[r["dram__bytes_read.sum"], r["dram__bytes_write.sum"]]
+                                     for r in g]
+    for f in ("timeline_verify_m1000.txt", "timeline_prefill_m1000.txt", "fwd_time.txt",
+              "forward_critical_path.txt"):
+        src = os.path.join(OUT, f)
+        if os.path.exists(src):
+            with open(src) as fi, open(os.path.join(dst, f), "w") as fo:
+                fo.write(fi.read())
     with open(os.path.join(dst, "summary.md"), "w") as fh:
         fh.write("\n".join(md) + "\n")
     with open(os.path.join(dst, "summary.json"), "w") as fh:

@@ -7,16 +7,23 @@ mkdir -p $OUT
 python bench.py > $OUT/bench_ours.json 2> $OUT/bench_ours.err
 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 python bench.py --workload c5 --no-micro --no-cpu > $OUT/bench_ours_c5.json 2> $OUT/bench_ours_c5.err
+python bench.py --workload c4 --steps 1 --warmup 1 --no-micro --no-cpu > $OUT/bench_ours_c4.json 2> $OUT/bench_ours_c4.err
 # launch list (cold-cache, serialised; shares only) of a short bench run, steady state
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 3000 -c 1500 --csv \
   --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu --no-micro \
   > $OUT/launches_bench.log 2>&1
-# full captures of the dominant kernels (the skinny GEMM: gate_up, M=5)
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:gemm_skinny -s 40 -c 2 \
-  -o $OUT/ncu_gemm_skinny python tools/profile_forward.py llama3-8b 1000 5 > /dev/null 2>&1
+# full captures of the dominant kernels (the skinny GEMM ring: gate_up and down, M=5)
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:gemm_ring -s 42 -c 2 \
+  -o $OUT/ncu_gemm_ring python tools/profile_forward.py llama3-8b 1000 5 > /dev/null 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:attn_decode -s 2 -c 2 \
+  -o $OUT/ncu_k7_decode python tools/micro_attn.py 32768 5 1 4 > /dev/null 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:attn_decode -s 2 -c 1 \
-  -o $OUT/ncu_k7_decode python tools/micro_attn.py 32768 5 0 4 > /dev/null 2>&1
+  -o $OUT/ncu_k7_decode_q1 python tools/micro_attn.py 32768 1 1 4 > /dev/null 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:attn_prefill_kernel -s 2 -c 1 \
   -o $OUT/ncu_k6_prefill python tools/micro_attn.py 31489 881 2 4 > /dev/null 2>&1
 python tools/profile_forward.py llama3-8b 1000 5 > $OUT/forward_critical_path.txt 2>&1
+python tools/timeline.py llama3-8b 1000 5 > $OUT/timeline_verify_m1000.txt 2>&1
+python tools/timeline.py llama3-8b 1000 5 edges >> $OUT/timeline_verify_m1000.txt 2>&1
+python tools/timeline.py llama3-8b 1000 150 > $OUT/timeline_prefill_m1000.txt 2>&1
+python tools/fwd_time.py llama3-8b 1000:5 2048:5 8192:5 32768:5 1000:1 32768:1 1000:150 > $OUT/fwd_time.txt 2>&1
 ls -la $OUT
