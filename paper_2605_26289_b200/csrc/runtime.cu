@@ -128,6 +128,12 @@ int project(cublasHandle_t h, const void* X, const void* W, void* Y, int M, int 
             bool y_f32, bool accumulate, cudaStream_t s) {
   if (M <= 32 && N % 16 == 0 && K % 256 == 0)
     return ds_gemm_skinny(X, W, Y, M, N, K, y_f32, accumulate, s);
+  // DS_GEMM_TC=1: K9 (tcgen05) instead of the library GEMM.  Opt-in: K9 is
+  // correct and deterministic but still slower than cuBLAS on these shapes
+  // (its TMA ring is too shallow for the load latency)
+  static const bool use_tc = getenv("DS_GEMM_TC") && atoi(getenv("DS_GEMM_TC")) == 1;
+  if (use_tc && N % 128 == 0 && K % 64 == 0 && K >= 128)
+    return ds_gemm_tc(X, W, Y, M, N, K, y_f32, accumulate, s);
   const cublasStatus_t st = gemm(h, X, W, Y, M, N, K, accumulate ? 1.f : 0.f,
                                  y_f32 ? CUDA_R_32F : CUDA_R_16BF);
   return st == CUBLAS_STATUS_SUCCESS ? 0 : 1000 + static_cast<int>(st);
