@@ -7,7 +7,10 @@
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <mutex>
+#include <string>
+#include <unordered_map>
 
 #include "../../include/deltaserve_b200.h"
 #include "attn_plan.h"
@@ -39,6 +42,10 @@ struct Runtime {
   cublasHandle_t blas = nullptr;
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  // graph capture/replay stream (the caller's may be the legacy default stream,
+  // which cannot be captured), ordered against the caller's by two events
+  cudaStream_t gs = nullptr;
+  cudaEvent_t g_in = nullptr, g_out = nullptr;
   int device = -1;
 };
 
@@ -53,6 +60,9 @@ Runtime& runtime() {
     cudaStreamCreateWithFlags(&rt.side, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&rt.fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&rt.join, cudaEventDisableTiming);
+    cudaStreamCreateWithFlags(&rt.gs, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&rt.g_in, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&rt.g_out, cudaEventDisableTiming);
     rt.device = dev;
   }
   return rt;
@@ -216,10 +226,99 @@ size_t ds_forward_workspace_bytes(const ds_model* model, int max_rows, int max_o
   return layout(model, max_rows, max_out, nullptr, nullptr) + kAlign;
 }
 
+static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forward_args* a,
+                        cudaStream_t stream);
+
+// ---- CUDA graphs for the decode / verify forward ----
+// A single-entry forward of <= 32 rows launches ~165 kernels whose launch
+// parameters depend only on the argument pointers/counts and, through the
+// attention split plan, on (q_len, n_splits, split_len, >= 4k keys).  The
+// second time a signature is seen its launch sequence is captured (PDL edges,
+// the side-stream fork/join and the cluster launches included) and replayed
+// with one cudaGraphLaunch from then on; the first sighting runs eagerly (it
+// also performs every one-time attribute / tensor-map setup outside capture).
+// Every pointer the graph bakes in is part of the key, so a moved buffer is a
+// new signature.  DS_GRAPHS=0 disables.
+namespace {
+struct GraphEntry {
+  int seen = 0;
+  cudaGraphExec_t exec = nullptr;
+};
+
+std::string graph_key(const ds_model* m, const ds_kv_store* kv, const ds_forward_args* a) {
+  std::string k;
+  k.append(reinterpret_cast<const char*>(m), sizeof(*m));
+  k.append(reinterpret_cast<const char*>(kv), sizeof(*kv));
+  k.append(reinterpret_cast<const char*>(a), sizeof(*a));
+  const int G = m->n_heads / m->n_kv_heads;
+  for (int e = 0; e < a->n_entries; ++e) {
+    const ds_entry& en = a->entries_host[e];
+    const int kv_len = en.past + en.q_len;
+    const AttnSplitPlan p = attn_split_plan(1, kv_len, m->n_kv_heads, a->n_entries, 1);
+    const int sig[5] = {en.q_len, p.n_splits, p.split_len, kv_len >= kDecodeTcMinKeys ? 1 : 0,
+                        en.q_len * G};
+    k.append(reinterpret_cast<const char*>(sig), sizeof(sig));
+  }
+  return k;
+}
+}  // namespace
+
 int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_args* a,
                      ds_stream_t stream_) {
   if (!m || !kv || !a || a->n_rows <= 0 || a->n_entries <= 0 || a->n_out <= 0) return DS_EINVAL;
   cudaStream_t stream = (cudaStream_t)stream_;
+  static const bool graphs = !(getenv("DS_GRAPHS") && atoi(getenv("DS_GRAPHS")) == 0);
+  if (graphs && a->n_rows <= 32 && a->n_entries == 1 &&
+      a->entries_host[0].q_len * (m->n_heads / m->n_kv_heads) <= kDecodeMaxRows) {
+    static thread_local std::unordered_map<std::string, GraphEntry> cache;
+    if (cache.size() > 512) {  // bound: drop everything (rare - signatures repeat)
+      for (auto& kv_ : cache)
+        if (kv_.second.exec) cudaGraphExecDestroy(kv_.second.exec);
+      cache.clear();
+    }
+    GraphEntry& ge = cache[graph_key(m, kv, a)];
+    if (ge.exec || ge.seen >= 1) {
+      Runtime& rt = runtime();
+      const cudaStream_t gs = rt.gs;
+      DS_CUDA(cudaEventRecord(rt.g_in, stream));
+      DS_CUDA(cudaStreamWaitEvent(gs, rt.g_in, 0));
+      if (!ge.exec) {
+        DS_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeRelaxed));
+        int rc = forward_body(m, kv, a, gs);
+        const cudaError_t pe = cudaGetLastError();  // an unchecked call that refused capture
+        if (rc == DS_OK && pe != cudaSuccess) rc = static_cast<int>(pe);
+        cudaGraph_t g = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(gs, &g);
+        cudaError_t ie = cudaSuccess;
+        if (rc == DS_OK && ce == cudaSuccess && g) ie = cudaGraphInstantiate(&ge.exec, g, 0);
+        if (g) cudaGraphDestroy(g);
+        if (rc != DS_OK || ce != cudaSuccess || !g || ie != cudaSuccess) {
+          ge.exec = nullptr;
+          ge.seen = -1000000;  // this signature is not capturable: stay eager
+          cudaGetLastError();
+          static bool warned = false;
+          if (!warned) {
+            warned = true;
+            fprintf(stderr, "deltaserve_b200: forward graph capture failed (%d / %s / %s)\n",
+                    rc, cudaGetErrorString(ce), cudaGetErrorString(ie));
+          }
+          DS_CUDA(cudaEventRecord(rt.g_out, gs));
+          DS_CUDA(cudaStreamWaitEvent(stream, rt.g_out, 0));
+          return forward_body(m, kv, a, stream);
+        }
+      }
+      DS_CUDA(cudaGraphLaunch(ge.exec, gs));
+      DS_CUDA(cudaEventRecord(rt.g_out, gs));
+      DS_CUDA(cudaStreamWaitEvent(stream, rt.g_out, 0));
+      return DS_OK;
+    }
+    ++ge.seen;
+  }
+  return forward_body(m, kv, a, stream);
+}
+
+static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forward_args* a,
+                        cudaStream_t stream) {
   Runtime& rt = runtime();
   uint8_t* base = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(a->workspace) + kAlign - 1) / kAlign * kAlign);
@@ -243,8 +342,10 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
   for (int e = n_long; e < a->n_entries; ++e)
     if (a->entries_host[e].q_len * (nh / nkv) > kDecodeMaxRows) n_long = 0;  // unsorted: auto
 
-  DS_BLAS(cublasSetStream(rt.blas, stream));
-  DS_BLAS(cublasSetWorkspace(rt.blas, b.blas_ws, kCublasWs));
+  if (T > 32) {  // the library GEMM serves only prefill chunks / batched plans
+    DS_BLAS(cublasSetStream(rt.blas, stream));
+    DS_BLAS(cublasSetWorkspace(rt.blas, b.blas_ws, kCublasWs));
+  }
 
   // batch tokens -> sequence history (the copy rule scans it), then the
   // per-row FNV states on a side stream (overlaps the layer stack).

@@ -41,6 +41,9 @@ assert _ENTRY_DT.itemsize == 40
 # packed query rows the decode kernel K7 takes (kDecodeMaxRows, csrc/attn_plan.h);
 # entries with more go to the tcgen05 kernel K6 and are ordered first
 DECODE_MAX_ROWS = 24
+# forwards of at most this many rows (one entry) replay a captured CUDA graph in
+# the native runtime (csrc/runtime.cu); their arguments sit at fixed offsets
+GRAPH_MAX_ROWS = 32
 
 
 class CostLedger:
@@ -133,6 +136,17 @@ class _Staging:
             self.host_np[off:off + a.size] = a
         if self.n:
             self.dev[: self.n].copy_(self.host[: self.n], non_blocking=True)
+
+    def add_fixed(self, arr: np.ndarray, words: int) -> int:
+        """Like add(), but reserves `words` so the next part's offset does not
+        depend on this part's length (stable pointers for CUDA-graph replay)."""
+        a = np.ascontiguousarray(arr).view(np.int32).reshape(-1)
+        if a.size > words:
+            raise ValueError("part larger than its fixed slot")
+        off = self.n
+        self.parts.append((off, a))
+        self.n = off + ((words + 3) // 4) * 4
+        return off
 
     def dptr(self, off: int) -> int:
         return self.dev.data_ptr() + 4 * off
@@ -383,12 +397,22 @@ class GpuEngine:
             raise ValueError("forward exceeds engine buffers")
         st = self.stage
         st.reset()
-        meta = self._stage_metadata(scratch_ops)
-        o_ent = st.add(ents.view(np.int32))
-        o_tok = st.add(np.concatenate(toks))
-        o_seq = st.add(np.concatenate(rseq))
-        o_pos = st.add(np.concatenate(rpos))
-        o_out = st.add(np.concatenate(orow))
+        if q_start <= GRAPH_MAX_ROWS:
+            # decode / verify: the forward's arguments at fixed offsets (first in the
+            # buffer), so the native runtime can replay its captured CUDA graph
+            o_ent = st.add_fixed(ents.view(np.int32), GRAPH_MAX_ROWS * _ENTRY_DT.itemsize // 4)
+            o_tok = st.add_fixed(np.concatenate(toks), GRAPH_MAX_ROWS)
+            o_seq = st.add_fixed(np.concatenate(rseq), GRAPH_MAX_ROWS)
+            o_pos = st.add_fixed(np.concatenate(rpos), GRAPH_MAX_ROWS)
+            o_out = st.add_fixed(np.concatenate(orow), GRAPH_MAX_ROWS)
+            meta = self._stage_metadata(scratch_ops)
+        else:
+            meta = self._stage_metadata(scratch_ops)
+            o_ent = st.add(ents.view(np.int32))
+            o_tok = st.add(np.concatenate(toks))
+            o_seq = st.add(np.concatenate(rseq))
+            o_pos = st.add(np.concatenate(rpos))
+            o_out = st.add(np.concatenate(orow))
         st.upload()
         self.h2d_bytes += 4 * st.n
         stream = torch.cuda.current_stream()
