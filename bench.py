@@ -199,6 +199,10 @@ def run_reference_arm(args, rank: int, world: int) -> None:
 # ---------------------------------------------------------------------------
 
 WORKLOAD_DESC = {
+    "c1": "C1: tiny random-init transformer (2 layers, hidden 1024, GQA 8q/2kv, d=128), single "
+          "agent 5 turns: 200-token system prompt + 150 tokens/turn (run with --model tiny)",
+    "c3": "C3: 3 interleaved coding agents sharing a tool-schema prefix via radix-cache metadata "
+          "aliasing, plus a 16-slot burst with grouped leader-follower prefill",
     "c2": "C2: Llama-3-8B-shaped random-init (GQA 32q/8kv, d=128), 6-turn agentic tool-call "
           "workflow, delta-only prefill over radix-restored prefix, prompt-lookup speculation k=4",
     "c4": "C4: 35-turn coding workflow growing to a 32,370-token prefix (split-KV decode/verify)",
