@@ -127,14 +127,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
       int c[4], c0;
       bool run;
     };
-    auto cells = [&](int jj) {
+    // page-table entries of a tile: loaded two tiles ahead (raw), resolved
+    // (run detection) when the tile is issued - their latency would otherwise
+    // serialise every TMA issue (ncu: the producer's top stall)
+    auto cells_load = [&](int jj, int (&c)[4]) {
       const int kt = k_begin + jj * kBN;
-      const int nvalid = min(kBN, k_end - kt);
+      const int nvalid = jj < ntiles ? min(kBN, k_end - kt) : 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c[i] = lane + 32 * i < nvalid ? __ldg(p2c + kt + lane + 32 * i) : -1;
+    };
+    auto cells_resolve = [&](const int (&c)[4]) {
       Cells cc;
       bool mine = true;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        cc.c[i] = lane + 32 * i < nvalid ? __ldg(p2c + kt + lane + 32 * i) : -1;
+      for (int i = 0; i < 4; ++i) cc.c[i] = c[i];
       cc.c0 = __shfl_sync(0xffffffffu, cc.c[0], 0);
 #pragma unroll
       for (int i = 0; i < 4; ++i) mine &= cc.c[i] < 0 || cc.c[i] == cc.c0 + lane + 32 * i;
@@ -180,8 +186,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
       load(cc, &tmv, vpool, smem + kSmemV + st * kTileBytes, &v_full[st]);
     };
     Cells prev{};
+    int raw0[4], raw1[4], raw2[4];
+    cells_load(0, raw0);
+    cells_load(1, raw1);
     for (int jj = 0; jj < ntiles; ++jj) {  // K_jj, then V_{jj-1}
-      const Cells cc = cells(jj);
+      cells_load(jj + 2, raw2);
+      const Cells cc = cells_resolve(raw0);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        raw0[i] = raw1[i];
+        raw1[i] = raw2[i];
+      }
       const int st = jj % kKStages;
       if (jj >= kKStages) mbar_wait(&k_empty[st], ((jj / kKStages) - 1) & 1);
       wait_if_new(jj);
