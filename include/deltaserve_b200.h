@@ -185,6 +185,15 @@ typedef struct {
   float* logits;                /* device [n_out][vocab] fp32 */
   void* workspace;               /* zero-initialised once, then reused across calls */
   size_t workspace_bytes;
+  /* Next prompt-lookup proposal computed in the same launch (0 = off).  For
+   * every DECODE / VERIFY entry the sampled bonus token is written to the
+   * history at its position past + accepted + 1, and the longest-suffix match
+   * (speculator.py:52-65) runs over the last next_window tokens of the
+   * history as the scheduler will hold it after committing: next_out[n_entries
+   * x (3 + next_cap)] = e[n], len[n], draft_len[n], drafts[n][next_cap], then
+   * int32 scratch[4n + 2].  A later proposal with cap <= next_cap is its prefix. */
+  int32_t next_window, next_min_match, next_cap;
+  int32_t* next_out;
 } ds_forward_args;
 
 size_t ds_forward_workspace_bytes(const ds_model* model, int max_rows, int max_out,

@@ -67,7 +67,9 @@ class ForwardArgs(ctypes.Structure):
                 ("copy_min_match", c_i32), ("policy_vocab", c_i32), ("entries_host", c_vp),
                 ("entries", c_vp), ("tokens", c_vp), ("row_seq", c_vp), ("row_pos", c_vp),
                 ("out_rows", c_vp), ("out_tok", c_vp), ("out_src", c_vp), ("out_accept", c_vp),
-                ("logits", c_vp), ("workspace", c_vp), ("workspace_bytes", ctypes.c_size_t)]
+                ("logits", c_vp), ("workspace", c_vp), ("workspace_bytes", ctypes.c_size_t),
+                ("next_window", c_i32), ("next_min_match", c_i32), ("next_cap", c_i32),
+                ("next_out", c_vp)]
 
 
 assert ctypes.sizeof(Entry) == 40

@@ -308,6 +308,48 @@ void launch_token_policy(const ds_forward_args* a, const ds_kv_store* kv, uint64
              (const int32_t*)a->out_tok, a->out_accept);
 }
 
+// next proposal, fused into the forward: the bonus token into the history and
+// the suffix-match ring of every decode / verify entry as the scheduler will
+// hold it after committing (accepted drafts + bonus)
+__global__ void next_draft_prep_kernel(const ds_entry* __restrict__ entries, int n_entries,
+                                       const int32_t* __restrict__ out_tok,
+                                       const int32_t* __restrict__ out_accept, int32_t* hist,
+                                       int64_t pos_stride, int window, int cap, int64_t* ring_off,
+                                       int32_t* ring_len, int32_t* caps) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_entries) return;
+  const ds_entry en = entries[e];
+  int n = 0;
+  if (en.kind == DS_ENTRY_DECODE || en.kind == DS_ENTRY_VERIFY) {
+    const int acc = en.kind == DS_ENTRY_VERIFY ? out_accept[e] : 0;
+    n = en.past + acc + 2;  // committed tokens incl. the pending bonus
+    hist[static_cast<int64_t>(en.seq) * pos_stride + n - 1] = out_tok[en.out_start + acc];
+  }
+  const int ln = n < window ? n : window;
+  ring_off[e] = static_cast<int64_t>(en.seq) * pos_stride + n - ln;
+  ring_len[e] = ln;
+  caps[e] = cap;
+}
+
+void launch_next_draft(const ds_forward_args* a, const ds_kv_store* kv, cudaStream_t stream) {
+  const int n = a->n_entries, cap = a->next_cap;
+  int32_t* base = a->next_out;
+  int32_t* e_out = base;
+  int32_t* len_out = base + n;
+  int32_t* dlen_out = base + 2 * n;
+  int32_t* draft_out = base + 3 * n;
+  int32_t* scratch = base + 3 * n + n * cap;
+  int64_t* ring_off = reinterpret_cast<int64_t*>(scratch + (reinterpret_cast<uintptr_t>(scratch) & 4 ? 1 : 0));
+  int32_t* ring_len = reinterpret_cast<int32_t*>(ring_off + n);
+  int32_t* caps = ring_len + n;
+  next_draft_prep_kernel<<<(n + 63) / 64, 64, 0, stream>>>(
+      a->entries, n, a->out_tok, a->out_accept, kv->hist, kv->pos_stride, a->next_window, cap,
+      ring_off, ring_len, caps);
+  suffix_match_kernel<128><<<n, 128, 0, stream>>>(kv->hist, ring_off, ring_len, kv->hist, ring_off,
+                                                  ring_len, a->next_min_match, caps, cap, e_out,
+                                                  len_out, draft_out, dlen_out);
+}
+
 void launch_row_hash(const ds_forward_args* a, const ds_kv_store* kv, uint64_t* row_hash,
                      cudaStream_t stream) {
   row_hash_kernel<<<(a->n_entries + 31) / 32, 32, 0, stream>>>(a->entries, a->n_entries, kv->hist,

@@ -482,6 +482,10 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
   DS_CUDA(cudaStreamWaitEvent(stream, rt.join, 0));
   launch_token_policy(a, kv, b.row_hash, nullptr, m->vocab, rt.side, stream);
   DS_CUDA(cudaGetLastError());
+  if (a->next_window > 0 && a->next_cap > 0 && a->next_out) {
+    launch_next_draft(a, kv, stream);
+    DS_CUDA(cudaGetLastError());
+  }
   return DS_OK;
 }
 

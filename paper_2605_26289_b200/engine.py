@@ -206,7 +206,15 @@ class GpuEngine:
         self.max_entries = n_seqs if cfg.batched_forward else 1
         self.max_rows = cfg.n_batch + self.max_out
         self.logits = torch.empty((self.max_out, s.vocab), dtype=torch.float32, device=dev)
-        self.res_dev = torch.zeros(2 * self.max_out + self.max_entries, dtype=torch.int32, device=dev)
+        # next prompt-lookup proposal computed inside decode/verify forwards
+        # (ds_forward_args.next_*): [e, len, draft_len][n] + drafts [n][cap] + scratch
+        self.nd_cap = max(1, cfg.spec_max_lookahead)
+        self.nd_off = 2 * self.max_out + self.max_entries
+        self.nd_off += self.nd_off & 1
+        nd_words = self.max_entries * (3 + self.nd_cap) + 4 * self.max_entries + 2
+        self.res_dev = torch.zeros(self.nd_off + nd_words, dtype=torch.int32, device=dev)
+        self._draft_cache: dict[int, tuple[int, list]] = {}  # seq -> (len(tokens), draft)
+        self.fused_drafts = bool(cfg.speculation_enabled)
         self.res_host = torch.zeros_like(self.res_dev, device="cpu").pin_memory()
         self.stage = _Staging(dev)
         self.k1_dev = torch.zeros(4 * n_seqs + n_seqs * cfg.spec_max_lookahead + 16,
@@ -281,6 +289,7 @@ class GpuEngine:
         prefix_hash (scheduler.py:237)."""
         self._pending_hist.append((seq, 0, np.asarray(tokens, dtype=np.int32)))
         self._hash[seq] = (cursor, prefix_hash)
+        self._draft_cache.pop(seq, None)
 
     def _hash_in(self, seq: int, past: int, tokens) -> int:
         ln, st = self._hash.get(seq, (0, FNV64_OFFSET))
@@ -420,12 +429,17 @@ class GpuEngine:
         self._apply_metadata(*meta, sp)
         res = self.res_dev
         self._ev[0].record(stream)
+        # decode / verify only: the next proposal rides in the same launch
+        nd = self.fused_drafts and all(r.kind != _lib.ENTRY_PREFILL and not r.scratch
+                                       for r in reqs)
         args = _lib.ForwardArgs(
             n_e, q_start, out_start, self.policy, self.cfg.copy_min_match, self.cfg.vocab,
             st.hptr(o_ent), st.dptr(o_ent), st.dptr(o_tok), st.dptr(o_seq), st.dptr(o_pos),
             st.dptr(o_out), res.data_ptr(), res.data_ptr() + 4 * self.max_out,
             res.data_ptr() + 8 * self.max_out, self.logits.data_ptr(),
-            self.workspace.data_ptr(), self.workspace.numel())
+            self.workspace.data_ptr(), self.workspace.numel(),
+            self.cfg.spec_buffer if nd else 0, self.cfg.spec_min_match, self.nd_cap if nd else 0,
+            res.data_ptr() + 4 * self.nd_off)
         check(lib().ds_model_forward(ctypes.byref(self.model_c), ctypes.byref(self.kv_c),
                                      ctypes.byref(args), sp), "ds_model_forward")
         self.gpu_launches += self.launches_per_forward(reqs)
@@ -441,6 +455,14 @@ class GpuEngine:
         f[3] += sum(r.past + len(r.batch) for r in reqs)
         h = self.res_host.numpy()
         tok, src, acc = h[: self.max_out], h[self.max_out: 2 * self.max_out], h[2 * self.max_out:]
+        if nd:  # cache the proposals for the token lists the scheduler will hold next
+            o = self.nd_off
+            dlen = h[o + 2 * n_e: o + 3 * n_e]
+            drafts = h[o + 3 * n_e: o + 3 * n_e + n_e * self.nd_cap].reshape(n_e, self.nd_cap)
+            for i, ri in enumerate(order):
+                r = reqs[ri]
+                a = int(acc[i]) if r.kind == _lib.ENTRY_VERIFY else 0
+                self._draft_cache[r.seq] = (r.past + a + 2, drafts[i, : dlen[i]].tolist())
         out = [None] * n_e
         for i, ri in enumerate(order):
             r = reqs[ri]
@@ -473,7 +495,8 @@ class GpuEngine:
 
     # -- K1: batched prompt-lookup proposals -----------------------------------------
 
-    def propose(self, slots: list[tuple[int, list, int]], window: int, min_match: int) -> list:
+    def propose(self, slots: list[tuple[int, list, int]], window: int, min_match: int,
+                use_cache: bool = True) -> list:
         """Drafts for many decoding slots in one launch.
 
         slots: (seq, tokens, cap) with tokens the full committed list (its last
@@ -483,6 +506,24 @@ class GpuEngine:
         n = len(slots)
         if n == 0:
             return []
+        # proposals computed by the previous forward (the token list it assumed
+        # is the one held now): a prefix of the max-cap draft, no launch
+        out: list = [None] * n
+        miss = []
+        for i, (seq, tokens, cap) in enumerate(slots):
+            hit = self._draft_cache.get(seq) if use_cache else None
+            if hit is not None and hit[0] == len(tokens) and window == self.cfg.spec_buffer \
+                    and min_match == self.cfg.spec_min_match and cap <= self.nd_cap:
+                out[i] = hit[1][:cap]
+            else:
+                miss.append(i)
+        if not miss:
+            return out
+        if len(miss) < n:
+            sub = self.propose([slots[i] for i in miss], window, min_match, use_cache=False)
+            for i, d in zip(miss, sub):
+                out[i] = d
+            return out
         for seq, tokens, _ in slots:
             self._pending_hist.append((seq, len(tokens) - 1, np.asarray(tokens[-1:], np.int32)))
         offs = np.zeros(n, dtype=np.int64)
