@@ -81,7 +81,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
   uint64_t* p_full = bars + 13;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
   if (smem_u32(smem) & 1023) __trap();  // SW128 tiles need 1 KB alignment
-  pdl_wait();
+  // programmatic dependent launch: only q and this chunk's own K/V rows come
+  // from the preceding kernels (projection, RoPE/KV store) - the prologue and
+  // the tiles of older keys run before the dependency wait (producer: before
+  // the first tile holding new keys; softmax warps: before loading q)
   pdl_trigger();
 
   const int e = blockIdx.z / splits;
@@ -119,6 +122,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
   }
   if (warp == 1) tc::alloc(tmem_slot, kTmemCols);
   if (warp >= 2) {  // Q rows (packed r = t*G + g) -> smem, UMMA A layout
+    pdl_wait();
     const int r = tid - 64;
     const int t = t0 + r / G, g = r - (r / G) * G;
     const bool ok = t < en.q_len;
@@ -191,11 +195,19 @@ __global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
       load(c, &tmv, vpool, smem + kSmemV + st * 2 * kKHalf, &v_full[st]);
     };
     // K_jj, then V_{jj-1}: V lags one tile (it is consumed a softmax later)
+    bool waited = false;
+    auto wait_if_new = [&](int jj) {  // before the first tile holding this chunk's K/V
+      if (!waited && min((j0 + jj + 1) * kBN, kv_hi) > en.past) {
+        pdl_wait();
+        waited = true;
+      }
+    };
     Cells prev{};
     for (int jj = 0; jj < ntiles; ++jj) {
       const Cells c = cells(jj);
       const int st = jj % kKStages;
       if (jj >= kKStages) mbar_wait(&k_empty[st], ((jj / kKStages) - 1) & 1);
+      wait_if_new(jj);
       load(c, &tmk, kpool, smem + kSmemK + st * 2 * kKHalf, &k_full[st]);
       if (jj > 0) load_v(jj - 1, prev);
       prev = c;
