@@ -385,7 +385,8 @@ class GpuEngine:
         order = sorted(range(n_e),
                        key=lambda i: 0 if len(reqs[i].batch) * G > DECODE_MAX_ROWS else 1)
         ents = np.zeros(n_e, dtype=_ENTRY_DT)
-        toks, rseq, rpos, orow = [], [], [], []
+        erows = []  # entry tuples, one structured-array assignment at the end
+        tok_l, seq_l, pos_l, out_l = [], [], [], []
         q_start = out_start = 0
         scratch_ops, scratch_of, s_off = [], {}, 0
         for i, ri in enumerate(order):
@@ -394,12 +395,12 @@ class GpuEngine:
             if q == 0:
                 raise ValueError("batch must be non-empty")
             n_out = q if r.kind == _lib.ENTRY_VERIFY else 1
-            ents[i] = (r.seq, r.past, q, q_start, r.kind, r.n_draft, out_start, n_out,
-                       self._hash_in(r.seq, r.past, r.tokens))
-            toks.append(np.asarray(r.batch, dtype=np.int32))
-            rseq.append(np.full(q, r.seq, dtype=np.int32))
-            rpos.append(np.arange(r.past, r.past + q, dtype=np.int32))
-            orow.append(np.arange(q_start + q - n_out, q_start + q, dtype=np.int32))
+            erows.append((r.seq, r.past, q, q_start, r.kind, r.n_draft, out_start, n_out,
+                          self._hash_in(r.seq, r.past, r.tokens)))
+            tok_l.extend(r.batch)
+            seq_l.extend([r.seq] * q)
+            pos_l.extend(range(r.past, r.past + q))
+            out_l.extend(range(q_start + q - n_out, q_start + q))
             if r.scratch:
                 if s_off + q > self.n_scratch:
                     raise ValueError("scratch cells exhausted")
@@ -413,6 +414,11 @@ class GpuEngine:
                 self.ledger.count_forward(q)
         if q_start > self.max_rows or out_start > self.max_out:
             raise ValueError("forward exceeds engine buffers")
+        ents[:] = erows
+        toks = [np.asarray(tok_l, dtype=np.int32)]
+        rseq = [np.asarray(seq_l, dtype=np.int32)]
+        rpos = [np.asarray(pos_l, dtype=np.int32)]
+        orow = [np.asarray(out_l, dtype=np.int32)]
         st = self.stage
         st.reset()
         if q_start <= GRAPH_MAX_ROWS:
