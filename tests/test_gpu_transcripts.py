@@ -37,3 +37,37 @@ def test_trace_parity_gpu(cuda, name, batched):
     assert core.engine.ledger.snapshot() == final["ledger"]
     assert core.radix.dump() == final["radix_dump"]
     _device_invariants(core)
+
+
+@pytest.mark.parametrize("name", ["c2", "c4_small"])
+def test_fused_next_proposal_matches_k1(cuda, name):
+    """The proposal computed inside each decode/verify forward (bonus token
+    written on device, suffix match over the post-commit ring) equals a fresh
+    K1 launch over the host's token list, for every proposal the scheduler
+    makes; and every cached proposal is actually used (no silent misses)."""
+    from paper_2605_26289_b200 import engine as E
+
+    tr = load_trace(name)
+    core = InferenceCore(core_config_for(tr, model="tiny"))
+    eng = core.engine
+    stats = {"hits": 0, "calls": 0}
+    orig = E.GpuEngine.propose
+
+    def checked(self, slots, window, min_match, use_cache=True):
+        got = orig(self, slots, window, min_match, use_cache)
+        if use_cache:
+            stats["calls"] += 1
+            stats["hits"] += sum(1 for seq, toks, _ in slots
+                                 if self._draft_cache.get(seq, (None,))[0] == len(toks))
+            fresh = orig(self, slots, window, min_match, use_cache=False)
+            assert got == fresh
+        return got
+
+    E.GpuEngine.propose = checked
+    try:
+        recs = replay(core, tr)
+    finally:
+        E.GpuEngine.propose = orig
+    assert mismatches(recs) == []
+    assert stats["calls"] > 0 and stats["hits"] >= stats["calls"] // 2, stats
+    assert eng.fused_drafts
