@@ -7,7 +7,7 @@ Tolerances (stated here and in DESIGN.md "parity"):
 * end to end through 2 layers: bf16 storage at 7 points per layer makes the
   result discontinuous in summation order - the oracle against ITSELF with
   fp64 instead of fp32 accumulation already differs by max-abs 8.9e-3 /
-  relative RMS 0.33% (tools/noise_floor.py) - so the end-to-end bound is
+  relative RMS 0.33% (tests/test_oracle_noise_floor.py) - so the end-to-end bound is
   max-abs <= 3e-2 and relative RMS <= 1e-2 (3x the floor), with greedy argmax
   equal wherever the oracle's top-1 margin exceeds 2 x 3e-2."""
 from __future__ import annotations
