@@ -191,20 +191,11 @@ TcPlan tc_plan(int T, int N, int K) {
   p.NT = ((T + p.n_tt - 1) / p.n_tt + 15) / 16 * 16;
   if (p.NT < 32) p.NT = 32;
   const int tiles = (N / kBM) * p.n_tt, slabs = K / 64;
-  // splits: fewest per-SM waves of work (2 CTAs per SM), a small charge per
-  // extra split for the cluster reduction
-  double best = 1e30;
+  // splits: only to give every SM a CTA (wo/down/wqkv have 32-48 row tiles);
+  // a split costs a cluster reduction, so take the fewest that reach 148 CTAs
   p.splits = 1;
-  for (int s = 1; s <= kMaxSplits; ++s) {
-    if (slabs / s < 2) break;
-    const int ctas = tiles * s;
-    const double waves = static_cast<double>((ctas + 2 * 148 - 1) / (2 * 148));
-    const double cost = waves / s + 0.04 * (s - 1);
-    if (cost < best - 1e-9) {
-      best = cost;
-      p.splits = s;
-    }
-  }
+  while (p.splits < kMaxSplits && tiles * p.splits < 148 && slabs / (p.splits + 1) >= 4)
+    ++p.splits;
   static const int budget = getenv("DS_TC_KB") ? atoi(getenv("DS_TC_KB")) * 1024 : kSmemBudget;
   static const int ks_env = getenv("DS_TC_KS") ? atoi(getenv("DS_TC_KS")) : 1;
   p.ks = ks_env;
