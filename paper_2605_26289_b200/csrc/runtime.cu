@@ -255,8 +255,11 @@ std::string graph_key(const ds_model* m, const ds_kv_store* kv, const ds_forward
     const ds_entry& en = a->entries_host[e];
     const int kv_len = en.past + en.q_len;
     const AttnSplitPlan p = attn_split_plan(1, kv_len, m->n_kv_heads, a->n_entries, 1);
-    const int sig[5] = {en.q_len, p.n_splits, p.split_len, kv_len >= kDecodeTcMinKeys ? 1 : 0,
-                        en.q_len * G};
+    // decode / verify (K7): the split plan fixes every launch shape; prefill
+    // chunks (K6 + library GEMMs): the exact (past, q_len)
+    const bool k6 = en.q_len * G > kDecodeMaxRows;
+    const int sig[5] = {en.q_len, k6 ? en.past : p.n_splits, k6 ? -1 : p.split_len,
+                        kv_len >= kDecodeTcMinKeys ? 1 : 0, en.q_len * G};
     k.append(reinterpret_cast<const char*>(sig), sizeof(sig));
   }
   return k;
@@ -268,8 +271,10 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
   if (!m || !kv || !a || a->n_rows <= 0 || a->n_entries <= 0 || a->n_out <= 0) return DS_EINVAL;
   cudaStream_t stream = (cudaStream_t)stream_;
   static const bool graphs = !(getenv("DS_GRAPHS") && atoi(getenv("DS_GRAPHS")) == 0);
-  if (graphs && a->n_rows <= 32 && a->n_entries == 1 &&
-      a->entries_host[0].q_len * (m->n_heads / m->n_kv_heads) <= kDecodeMaxRows) {
+  // single-entry forwards: decode / verify (<= 32 rows) and prefill chunks
+  // (DS_GRAPHS=2: decode / verify only)
+  static const bool graph_prefill = !(getenv("DS_GRAPHS") && atoi(getenv("DS_GRAPHS")) == 2);
+  if (graphs && a->n_entries == 1 && (a->n_rows <= 32 || graph_prefill)) {
     static thread_local std::unordered_map<std::string, GraphEntry> cache;
     if (cache.size() > 512) {  // bound: drop everything (rare - signatures repeat)
       for (auto& kv_ : cache)

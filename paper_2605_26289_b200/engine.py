@@ -421,14 +421,17 @@ class GpuEngine:
         orow = [np.asarray(out_l, dtype=np.int32)]
         st = self.stage
         st.reset()
-        if q_start <= GRAPH_MAX_ROWS:
-            # decode / verify: the forward's arguments at fixed offsets (first in the
-            # buffer), so the native runtime can replay its captured CUDA graph
+        if q_start <= GRAPH_MAX_ROWS or n_e == 1:
+            # the forward's arguments at fixed offsets (first in the buffer), so
+            # the native runtime can replay its captured CUDA graph: a compact
+            # layout for decode / verify, a max-rows one for a prefill chunk
+            rows = GRAPH_MAX_ROWS if q_start <= GRAPH_MAX_ROWS else self.max_rows
             o_ent = st.add_fixed(ents.view(np.int32), GRAPH_MAX_ROWS * _ENTRY_DT.itemsize // 4)
-            o_tok = st.add_fixed(np.concatenate(toks), GRAPH_MAX_ROWS)
-            o_seq = st.add_fixed(np.concatenate(rseq), GRAPH_MAX_ROWS)
-            o_pos = st.add_fixed(np.concatenate(rpos), GRAPH_MAX_ROWS)
-            o_out = st.add_fixed(np.concatenate(orow), GRAPH_MAX_ROWS)
+            o_tok = st.add_fixed(np.concatenate(toks), rows)
+            o_seq = st.add_fixed(np.concatenate(rseq), rows)
+            o_pos = st.add_fixed(np.concatenate(rpos), rows)
+            o_out = st.add_fixed(np.concatenate(orow), GRAPH_MAX_ROWS if rows == GRAPH_MAX_ROWS
+                                 else self.max_out)
             meta = self._stage_metadata(scratch_ops)
         else:
             meta = self._stage_metadata(scratch_ops)

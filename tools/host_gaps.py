@@ -72,7 +72,7 @@ class _Proxy:
 _proxy = _Proxy()
 E.lib = lambda: _proxy
 tr = load_trace(sys.argv[1] if len(sys.argv) > 1 else "c2")
-core = InferenceCore(core_config_for(tr, model="llama3-8b"))
+core = InferenceCore(core_config_for(tr, model=os.environ.get("DS_MODEL", "llama3-8b")))
 for _ in range(2):
     core.reset_state(); replay(core, tr)
 for k in acc: acc[k] = 0 if k in ("n", "np") else 0.0

@@ -7,7 +7,7 @@ from paper_2605_26289_b200.scheduler import InferenceCore
 from paper_2605_26289_b200.workload import core_config_for, load_trace, replay
 
 tr = load_trace(sys.argv[1] if len(sys.argv) > 1 else "c2")
-core = InferenceCore(core_config_for(tr, model="llama3-8b"))
+core = InferenceCore(core_config_for(tr, model=os.environ.get("DS_MODEL", "llama3-8b")))
 for _ in range(2):
     core.reset_state(); replay(core, tr)
 torch.cuda.synchronize()
@@ -21,4 +21,4 @@ pr.disable()
 wall = time.perf_counter() - t0
 dev = core.engine.device_seconds()
 print(f"wall {wall * 1000 / 3:.1f} ms/step, device forwards {dev * 1000 / 3:.1f} ms/step")
-st = pstats.Stats(pr); st.sort_stats("tottime").print_stats(25)
+st = pstats.Stats(pr); st.sort_stats("tottime").print_stats(40)
