@@ -152,6 +152,8 @@ int project(cublasHandle_t h, const void* X, const void* W, void* Y, int M, int 
 __global__ void scatter_tokens_kernel(const int32_t* tok, const int32_t* row_seq,
                                       const int32_t* row_pos, int n, int32_t* hist,
                                       int64_t stride) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < n) hist[static_cast<int64_t>(row_seq[r]) * stride + row_pos[r]] = tok[r];
 }
@@ -352,18 +354,18 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
     DS_BLAS(cublasSetWorkspace(rt.blas, b.blas_ws, kCublasWs));
   }
 
-  // batch tokens -> sequence history (the copy rule scans it), then the
-  // per-row FNV states on a side stream (overlaps the layer stack).
-  scatter_tokens_kernel<<<(T + 127) / 128, 128, 0, stream>>>(a->tokens, a->row_seq, a->row_pos, T,
-                                                             kv->hist, kv->pos_stride);
-  DS_CUDA(cudaGetLastError());
+  // the embedding first (it depends only on the uploaded tokens): the first
+  // node of a replayed graph starts at once; then batch tokens -> history (the
+  // copy rule scans it) and the per-row FNV states on a side stream
+  DS_CHECK(ds_embed(a->tokens, T, m->embed, H, b.x, 1, stream));
+  DS_CUDA(launch_pdl(scatter_tokens_kernel, dim3((T + 127) / 128), dim3(128), 0, stream,
+                     a->tokens, a->row_seq, a->row_pos, T, kv->hist, kv->pos_stride));
   DS_CUDA(cudaEventRecord(rt.fork, stream));
   DS_CUDA(cudaStreamWaitEvent(rt.side, rt.fork, 0));
   launch_row_hash(a, kv, b.row_hash, rt.side);
   DS_CUDA(cudaGetLastError());
   DS_CUDA(cudaEventRecord(rt.join, rt.side));
 
-  DS_CHECK(ds_embed(a->tokens, T, m->embed, H, b.x, 1, stream));
   const __nv_bfloat16* wqkv = static_cast<const __nv_bfloat16*>(m->wqkv);
   const __nv_bfloat16* wo = static_cast<const __nv_bfloat16*>(m->wo);
   const __nv_bfloat16* wgu = static_cast<const __nv_bfloat16*>(m->w_gate_up);
