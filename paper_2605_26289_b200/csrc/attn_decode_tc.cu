@@ -31,7 +31,7 @@ constexpr int kBM = 128;                       // MMA rows (R <= 24 real, rest p
 constexpr int kBN = 128;                       // keys per tile
 constexpr int kHalf = kBN * 128;               // 64-column half of a [128][128] bf16 tile
 constexpr int kTileBytes = 2 * kHalf;          // 32 KB
-constexpr int kKStages = 3, kVStages = 2;
+constexpr int kKStages = 3, kVStages = 3;
 constexpr int kSmemQ = 0;                      // 32 KB
 constexpr int kSmemK = kSmemQ + kTileBytes;    // 96 KB
 constexpr int kSmemV = kSmemK + kKStages * kTileBytes;  // 64 KB
@@ -61,12 +61,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
   uint64_t* k_full = bars;        // [3]
   uint64_t* k_empty = bars + 3;   // [3]
-  uint64_t* v_full = bars + 6;    // [2]
-  uint64_t* v_empty = bars + 8;   // [2]
-  uint64_t* s_full = bars + 10;   // [2]
-  uint64_t* pv_done = bars + 12;
-  uint64_t* p_full = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* v_full = bars + 6;    // [kVStages <= 3]
+  uint64_t* v_empty = bars + 9;   // [kVStages]
+  uint64_t* s_full = bars + 12;   // [2]
+  uint64_t* pv_done = bars + 14;
+  uint64_t* p_full = bars + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
   // split-merge buffers over the K ring (free once the last PV completed)
   float* cval = reinterpret_cast<float*>(smem + kSmemK);  // [R][128]
   float* clse = cval + kMaxRows * kD;                     // [R]
