@@ -25,6 +25,21 @@
 
 namespace ds {
 
+#ifdef DS_K7_TRACE
+// debug build only: per-CTA globaltimer stamps (tools/k7tc_trace.py)
+__device__ unsigned long long g_k7tc_trace[1024][8];
+DS_DEVICE unsigned long long gtime_tc() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TC_STAMP(i)                                                                        \
+  if (threadIdx.x == 0)                                                                    \
+  g_k7tc_trace[(blockIdx.z * gridDim.y + blockIdx.y) & 1023][i] = gtime_tc()
+#else
+#define TC_STAMP(i)
+#endif
+
 namespace {
 constexpr int kD = 128;
 constexpr int kBM = 128;                       // MMA rows (R <= 24 real, rest padding)
@@ -56,6 +71,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
     float* __restrict__ part_o, float* __restrict__ part_lse, int64_t head_stride,
     const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
     const char* __restrict__ l2p, int64_t l2_bytes) {
+  TC_STAMP(6);
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // SW128 alignment
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
@@ -261,7 +277,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
     }
   } else {
     // ================ softmax / epilogue (warp 0: rows 0-31) ================
+    TC_STAMP(0);
     pdl_wait();  // q comes from the preceding projection
+    TC_STAMP(1);
     if (!cluster_merge) pdl_trigger();
     const int r = lane;
     const bool real = r < R;
@@ -287,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
       const int sb = jj & 1;
       const int kt = k_begin + jj * kBN;
       mbar_wait(&s_full[sb], (jj >> 1) & 1);
+      if (jj == 0) TC_STAMP(2);
       tc::fence_after();
 #pragma unroll
       for (int c = 0; c < 4; ++c) tc::ld32_issue(trow + sb * kBN + 32 * c, sv + 32 * c);
@@ -341,6 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
     }
+    TC_STAMP(3);
     mbar_wait(pv_done, (ntiles - 1) & 1);
     tc::fence_after();
 #pragma unroll
@@ -394,8 +414,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
   }
   // PDL: see K7 (triggers only as the grid retires; more splits than a
   // cluster are merged by attn_combine_kernel, R > 8 here)
+  TC_STAMP(5);
   pdl_trigger();
 }
+
+#ifdef DS_K7_TRACE
+extern "C" int ds_debug_k7tc_trace(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_k7tc_trace, sizeof(g_k7tc_trace));
+}
+#endif
 
 int launch_attn_decode_tc(const ds_entry* entries_dev, int n_entries, const void* qkv,
                           const void* k_pool, const void* v_pool, int64_t head_stride,
