@@ -423,8 +423,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "data": "synthetic: reference scenario token streams (recorded trace), random-init "
                 "weights N(0,0.02)",
         "config": {"workload": WORKLOAD_DESC.get(args.workload, args.workload),
-                   "model": s.name, "global_batch": world, "seq_len": max(r.n_t for r in
-                                                                          [x.result for x in recs]),
+                   "trace": args.workload, "transformer_shape": s.name,
+                   "conversations_per_step_per_gpu": 1 if not args.workload.startswith("c5")
+                   else "all sessions routed to this rank",
+                   "max_tokens_per_session": max(r.n_t for r in [x.result for x in recs]),
                    "parallelism": f"session-sharded x{world} (one process per GPU)",
                    "token_policy": cfg.token_policy, "batched_forward": cfg.batched_forward,
                    "l2": "weights 16 GB >> 126 MB L2 each forward (no flush needed)"},
