@@ -194,6 +194,12 @@ typedef struct {
    * int32 scratch[4n + 2].  A later proposal with cap <= next_cap is its prefix. */
   int32_t next_window, next_min_match, next_cap;
   int32_t* next_out;
+  /* 1: store the fp32 logits [n_out][vocab]; 0: no logits materialisation -
+   * when n_out <= 32 the LM head's epilogue reduces each row to its argmax
+   * (DS_POLICY_ARGMAX reads that, the copy policy ignores it); larger n_out
+   * still use `logits` as scratch.  The argmax policy's result is the same
+   * either way (lowest id on ties). */
+  int32_t logits_out;
 } ds_forward_args;
 
 size_t ds_forward_workspace_bytes(const ds_model* model, int max_rows, int max_out,
@@ -286,6 +292,12 @@ typedef struct {
    * is issued, so HBM stays busy across the kernel boundary (0 = none) */
   const void* l2_next;
   int64_t l2_next_bytes;
+  /* fused row argmax (the LM head): argmax_out[m] = max over the product's
+   * columns n of (ordered(y[m][n]) << 32) | (0xFFFFFFFF - n), i.e. the largest
+   * value and the lowest column on ties (np.argmax); the caller zeroes it
+   * before the launch.  Y may then be NULL: no product is stored (needs
+   * y_f32 = 1, accumulate = 0, no other fusion). */
+  uint64_t* argmax_out;
 } ds_skinny_epi;
 
 int ds_gemm_skinny_ex(const void* X, const void* W, void* Y, int M, int N, int K, int y_f32,

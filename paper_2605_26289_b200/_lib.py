@@ -59,7 +59,8 @@ class SkinnyEpi(ctypes.Structure):
                 ("n_heads", c_i32), ("n_kv_heads", c_i32), ("row_seq", c_vp), ("row_pos", c_vp),
                 ("pos2cell", c_vp), ("pos_stride", c_i64), ("rope_cos", c_vp),
                 ("rope_sin", c_vp), ("k_pool_l", c_vp), ("v_pool_l", c_vp),
-                ("kv_head_stride", c_i64), ("l2_next", c_vp), ("l2_next_bytes", c_i64)]
+                ("kv_head_stride", c_i64), ("l2_next", c_vp), ("l2_next_bytes", c_i64),
+                ("argmax_out", c_vp)]
 
 
 class ForwardArgs(ctypes.Structure):
@@ -69,7 +70,7 @@ class ForwardArgs(ctypes.Structure):
                 ("out_rows", c_vp), ("out_tok", c_vp), ("out_src", c_vp), ("out_accept", c_vp),
                 ("logits", c_vp), ("workspace", c_vp), ("workspace_bytes", ctypes.c_size_t),
                 ("next_window", c_i32), ("next_min_match", c_i32), ("next_cap", c_i32),
-                ("next_out", c_vp)]
+                ("next_out", c_vp), ("logits_out", c_i32)]
 
 
 assert ctypes.sizeof(Entry) == 40

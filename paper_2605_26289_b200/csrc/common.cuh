@@ -197,6 +197,16 @@ inline cudaError_t launch_pdl_cluster_z(void (*kern)(KArgs...), dim3 grid, dim3 
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// ---- packed row argmax: one u64 max = (largest value, lowest index) ----
+DS_DEVICE unsigned long long argmax_key(float v, int idx) {
+  uint32_t u = __float_as_uint(v + 0.f);  // -0 -> +0 (equal values tie on the index)
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return (static_cast<unsigned long long>(u) << 32) | (0xFFFFFFFFu - static_cast<uint32_t>(idx));
+}
+DS_DEVICE int argmax_key_index(unsigned long long key) {
+  return static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(key));
+}
+
 // ---- thread-block cluster / distributed shared memory ----
 DS_DEVICE uint32_t cluster_ctarank() {
   uint32_t r;
@@ -215,6 +225,13 @@ DS_DEVICE uint32_t dsmem_map(uint32_t smem_addr, uint32_t rank) {
 DS_DEVICE float dsmem_ld_f32(uint32_t cluster_addr) {
   float v;
   asm volatile("ld.shared::cluster.f32 %0, [%1];\n" : "=f"(v) : "r"(cluster_addr));
+  return v;
+}
+DS_DEVICE float4 dsmem_ld_f32x4(uint32_t cluster_addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(cluster_addr));
   return v;
 }
 }  // namespace ds

@@ -113,8 +113,9 @@ DS_DEVICE void rope_epilogue(const float (*red)[MT][4][32], const float* s_inv, 
 // makes red visible; uses named barrier 1 over those threads.
 template <int MT>
 DS_DEVICE void unit_epilogue(const float (*red)[MT][4][32], const float* s_inv, const int* s_pos,
-                             const int64_t* s_cell, float (*s_sq)[17], const ds_skinny_epi& epi,
-                             void* Y, int M, int N, int n0, int y_f32, int accumulate) {
+                             const int64_t* s_cell, float (*s_sq)[17],
+                             unsigned long long* s_amax, const ds_skinny_epi& epi, void* Y, int M,
+                             int N, int n0, int y_f32, int accumulate) {
   if (epi.rope) {
     rope_epilogue<MT>(red, s_inv, s_pos, s_cell, epi, Y, M, N, n0);
     return;
@@ -155,6 +156,11 @@ DS_DEVICE void unit_epilogue(const float (*red)[MT][4][32], const float* s_inv, 
     if (epi.row_ss) s *= s_inv[m];
     const int64_t o = static_cast<int64_t>(m) * N + feat;
     float y;
+    if (epi.argmax_out) {  // LM head: running per-row best of this CTA
+      if (Y) static_cast<float*>(Y)[o] = s;
+      atomicMax(&s_amax[m], argmax_key(s, feat));
+      continue;
+    }
     if (y_f32) {
       float* yp = static_cast<float*>(Y) + o;
       y = accumulate ? *yp + s : s;
@@ -212,8 +218,10 @@ __global__ void __launch_bounds__((kGemvWarps + 1) * 32, 1) gemm_ring_kernel(
   __shared__ float s_sq[32][17];
   __shared__ int s_pos[32];
   __shared__ int64_t s_cell[32];
+  __shared__ unsigned long long s_amax[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int units = N / 16, nst = K / KC;
+  if (threadIdx.x < 32) s_amax[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < n_stages; ++i) {
       mbar_init(&full[i], 1);
@@ -340,9 +348,15 @@ __global__ void __launch_bounds__((kGemvWarps + 1) * 32, 1) gemm_ring_kernel(
 #pragma unroll
       for (int q = 0; q < 4; ++q) red[warp][mt][q][lane] = acc[mt][q];
     named_bar_sync(1, kGemvWarps * 32);
-    unit_epilogue<MT>(red, s_inv, s_pos, s_cell, s_sq, epi, Y, M, N, u * 16, y_f32, accumulate);
+    unit_epilogue<MT>(red, s_inv, s_pos, s_cell, s_sq, s_amax, epi, Y, M, N, u * 16, y_f32,
+                      accumulate);
     named_bar_sync(1, kGemvWarps * 32);  // red / s_sq reused by the next unit
   }
+  // one global max per row and CTA (not per unit: 8k units on M addresses
+  // would serialise in L2)
+  if (epi.argmax_out && threadIdx.x < M && s_amax[threadIdx.x])
+    atomicMax(reinterpret_cast<unsigned long long*>(epi.argmax_out) + threadIdx.x,
+              s_amax[threadIdx.x]);
 }
 
 template <int MT, int NS>
@@ -417,5 +431,9 @@ extern "C" int ds_gemm_skinny_ex(const void* X, const void* W, void* Y, int M, i
     return DS_EINVAL;
   if (epi->ss_out && !y_f32) return DS_EINVAL;
   if (epi->h_out && (!epi->ss_out || !epi->h_w)) return DS_EINVAL;
+  if (epi->argmax_out && (!y_f32 || accumulate || epi->ss_out || epi->swiglu || epi->rope ||
+                          epi->row_ss))
+    return DS_EINVAL;
+  if (!Y && !epi->argmax_out) return DS_EINVAL;
   return ds::run(X, W, Y, M, N, K, y_f32, accumulate, *epi, (cudaStream_t)stream);
 }

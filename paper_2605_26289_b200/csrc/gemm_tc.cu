@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int splits = gridDim.z, split = blockIdx.z;
-  const int f0 = blockIdx.x * kBM, t0 = blockIdx.y * NT;
+  const int f0 = blockIdx.y * kBM, t0 = blockIdx.x * NT;  // token tiles of one weight tile adjacent
   const int slabs = K / (64 * ks);  // stages along K
   const int s_beg = split * slabs / splits, s_end = (split + 1) * slabs / splits;
   const int nsl = s_end - s_beg;
@@ -148,27 +148,60 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(
   tc::fence_before();
   __syncthreads();
   if (splits > 1) {
-    // cluster reduction: CTA `split` owns token rows j = split, split + S, ...
+    // cluster reduction: CTA `split` owns token rows j = split, split + S, ...;
+    // item = (owned row, 4 features), all 6 warps, two items in flight per
+    // thread with every split's float4 loaded before the fixed-order sum
     cluster_sync_all();  // every split's partial tile is in its smem
-    if (warp >= 2) {
-      const int f = (warp & 3) * 32 + lane;
-      for (int j = split; j < NT; j += splits) {
-        const int t = t0 + j;
-        if (t >= T) break;
-        const uint32_t a = smem_u32(red + j * kBM + f);
-        float p[kMaxSplits];
+    const int own = (NT - split + splits - 1) / splits, items = own * (kBM / 4);
+    for (int i0 = threadIdx.x; i0 < items; i0 += 2 * kThreads) {
+      float4 p[2][kMaxSplits];
 #pragma unroll
-        for (int q = 0; q < kMaxSplits; ++q) p[q] = q < splits ? dsmem_ld_f32(dsmem_map(a, q)) : 0.f;
-        float s = 0.f;
+      for (int u = 0; u < 2; ++u) {
+        const int it = i0 + u * kThreads;
+        const int j = split + (it >> 5) * splits;
+        const uint32_t a = smem_u32(red + j * kBM + (it & 31) * 4);
 #pragma unroll
-        for (int q = 0; q < kMaxSplits; ++q) s += p[q];  // fixed split order
-        const int64_t o = static_cast<int64_t>(t) * N + f0 + f;
+        for (int q = 0; q < kMaxSplits; ++q)
+          p[u][q] = (q < splits && it < items) ? dsmem_ld_f32x4(dsmem_map(a, q))
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int it = i0 + u * kThreads;
+        const int t = t0 + split + (it >> 5) * splits;
+        if (it >= items || t >= T) continue;
+        float4 s = p[u][0];
+#pragma unroll
+        for (int q = 1; q < kMaxSplits; ++q) {  // fixed split order
+          s.x += p[u][q].x;
+          s.y += p[u][q].y;
+          s.z += p[u][q].z;
+          s.w += p[u][q].w;
+        }
+        const int64_t o = static_cast<int64_t>(t) * N + f0 + (it & 31) * 4;
         if (y_f32) {
-          float* yp = static_cast<float*>(Y) + o;
-          *yp = accumulate ? *yp + s : s;
+          float4* yp = reinterpret_cast<float4*>(static_cast<float*>(Y) + o);
+          if (accumulate) {
+            const float4 r = *yp;
+            s.x += r.x;
+            s.y += r.y;
+            s.z += r.z;
+            s.w += r.w;
+          }
+          *yp = s;
         } else {
-          __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(Y) + o;
-          *yp = __float2bfloat16_rn(accumulate ? __bfloat162float(*yp) + s : s);
+          uint2* yp = reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(Y) + o);
+          if (accumulate) {
+            const uint2 r = *yp;
+            const float2 r0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.x));
+            const float2 r1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.y));
+            s.x += r0.x;
+            s.y += r0.y;
+            s.z += r1.x;
+            s.w += r1.y;
+          }
+          __nv_bfloat162 b0 = __floats2bfloat162_rn(s.x, s.y), b1 = __floats2bfloat162_rn(s.z, s.w);
+          *yp = make_uint2(*reinterpret_cast<uint32_t*>(&b0), *reinterpret_cast<uint32_t*>(&b1));
         }
       }
     }
@@ -233,7 +266,7 @@ extern "C" int ds_gemm_tc(const void* X, const void* W, void* Y, int T, int N, i
     cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr_smem = p.smem;
   }
-  const dim3 grid(N / kBM, p.n_tt, p.splits);
+  const dim3 grid(p.n_tt, N / kBM, p.splits);
   cudaError_t e;
   if (p.splits > 1)
     e = launch_pdl_cluster_z(gemm_tc_kernel, grid, dim3(kThreads), p.smem, p.splits,

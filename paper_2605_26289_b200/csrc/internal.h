@@ -8,6 +8,6 @@ void launch_next_draft(const ds_forward_args* a, const ds_kv_store* kv, cudaStre
 void launch_row_hash(const ds_forward_args* a, const ds_kv_store* kv, uint64_t* row_hash,
                      cudaStream_t stream);
 void launch_token_policy(const ds_forward_args* a, const ds_kv_store* kv, uint64_t* row_hash,
-                         int32_t* out_entry, int model_vocab, cudaStream_t hash_stream,
+                         uint64_t* amax, int model_vocab, cudaStream_t hash_stream,
                          cudaStream_t stream);
 }  // namespace ds

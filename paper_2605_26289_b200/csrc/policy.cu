@@ -246,8 +246,8 @@ __global__ void row_hash_kernel(const ds_entry* entries, int n_entries, const in
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) token_policy_kernel(
     const ds_entry* entries, int n_entries, const int32_t* hist, int64_t stride,
-    const uint64_t* row_hash, const float* logits, int model_vocab, int policy, int mm,
-    int policy_vocab, int32_t* out_tok, int32_t* out_src) {
+    const uint64_t* row_hash, const float* logits, unsigned long long* amax, int model_vocab,
+    int policy, int mm, int policy_vocab, int32_t* out_tok, int32_t* out_src) {
   __shared__ int s_best;
   pdl_wait();
   pdl_trigger();
@@ -269,6 +269,11 @@ __global__ void __launch_bounds__(BLOCK) token_policy_kernel(
         out_src[o] = -1;
       }
     }
+  } else if (amax) {  // argmax fused into the LM head's epilogue
+    if (threadIdx.x == 0) {
+      out_tok[o] = argmax_key_index(amax[o]);
+      out_src[o] = -1;
+    }
   } else {
     const int bi = block_argmax<BLOCK>(logits + static_cast<size_t>(o) * model_vocab, model_vocab);
     if (threadIdx.x == 0) {
@@ -276,6 +281,7 @@ __global__ void __launch_bounds__(BLOCK) token_policy_kernel(
       out_src[o] = -1;
     }
   }
+  if (amax && threadIdx.x == 0) amax[o] = 0;  // re-arm for the next forward
 }
 
 __global__ void verify_accept_kernel(const ds_entry* entries, int n_entries, const int32_t* hist,
@@ -295,13 +301,13 @@ __global__ void verify_accept_kernel(const ds_entry* entries, int n_entries, con
 }
 
 void launch_token_policy(const ds_forward_args* a, const ds_kv_store* kv, uint64_t* row_hash,
-                         int32_t* out_entry, int model_vocab, cudaStream_t hash_stream,
+                         uint64_t* amax, int model_vocab, cudaStream_t hash_stream,
                          cudaStream_t stream) {
   (void)hash_stream;
   constexpr int B = 256;
   launch_pdl(token_policy_kernel<B>, dim3(a->n_out), dim3(B), 0, stream, a->entries,
              a->n_entries, kv->hist, kv->pos_stride, (const uint64_t*)row_hash,
-             (const float*)a->logits, model_vocab, a->policy, a->copy_min_match, a->policy_vocab,
+             (const float*)a->logits, (unsigned long long*)amax, model_vocab, a->policy, a->copy_min_match, a->policy_vocab,
              a->out_tok, a->out_src);
   launch_pdl(verify_accept_kernel, dim3((a->n_entries + 63) / 64), dim3(64), 0, stream,
              a->entries, a->n_entries, (const int32_t*)kv->hist, kv->pos_stride,

@@ -83,6 +83,7 @@ struct Buffers {
   float* x;  // fp32 residual stream
   __nv_bfloat16 *h, *qkv, *attn, *gu, *act, *hf;
   uint64_t* ss;  // 2 x 32: fixed-point row sums of squares (skinny GEMM epilogues)
+  uint64_t* amax;  // 32: fused LM-head argmax keys (re-armed by the token policy)
   uint64_t* row_hash;
   void* attn_ws;
   size_t attn_ws_bytes;
@@ -99,6 +100,7 @@ size_t layout(const ds_model* m, int rows, int outs, Buffers* b, uint8_t* base) 
   // split-merge counters are zero between calls (self re-arming), which must
   // hold whatever the previous call's batch size was
   t.ss = c.take<uint64_t>(2 * DS_SKINNY_SS_WORDS * 8);
+  t.amax = c.take<uint64_t>(DS_SKINNY_SS_WORDS * 8);
   t.attn_ws_bytes = attn_partial_bytes_bound();
   t.attn_ws = c.take<uint8_t>(t.attn_ws_bytes);
   t.x = c.take<float>(rows * H * 4);
@@ -483,11 +485,22 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
   set_attn_l2_prefetch(nullptr, 0);  // a hint not consumed (K6-only layer) must not leak
   // final norm on sampled rows only, LM head in fp32
   DS_CHECK(ds_rmsnorm(b.x, 1, a->out_rows, a->n_out, H, m->final_norm, m->rms_eps, b.hf, stream));
-  DS_CHECK(project(rt.blas, b.hf, m->lm_head, a->logits, a->n_out, m->vocab, H, true, false,
-                   stream));
+  // LM head: <= 32 sampled rows reduce to their argmax in the GEMM epilogue
+  // (logits stored only on request); more rows go through the library GEMM
+  // and the K8 row argmax
+  const bool fused_head = a->n_out <= 32;
+  if (fused_head) {
+    ds_skinny_epi eh{};
+    eh.argmax_out = b.amax;
+    DS_CHECK(ds_gemm_skinny_ex(b.hf, m->lm_head, a->logits_out ? a->logits : nullptr, a->n_out,
+                               m->vocab, H, 1, 0, &eh, stream));
+  } else {
+    DS_CHECK(project(rt.blas, b.hf, m->lm_head, a->logits, a->n_out, m->vocab, H, true, false,
+                     stream));
+  }
 
   DS_CUDA(cudaStreamWaitEvent(stream, rt.join, 0));
-  launch_token_policy(a, kv, b.row_hash, nullptr, m->vocab, rt.side, stream);
+  launch_token_policy(a, kv, b.row_hash, fused_head ? b.amax : nullptr, m->vocab, rt.side, stream);
   DS_CUDA(cudaGetLastError());
   if (a->next_window > 0 && a->next_cap > 0 && a->next_out) {
     launch_next_draft(a, kv, stream);

@@ -163,7 +163,7 @@ class GpuEngine:
     """Weights, paged KV store and the per-forward plumbing on one B200."""
 
     def __init__(self, cfg: CoreConfig, kv: UnifiedKvCache, n_seqs: int, device=None,
-                 weights: dict | None = None):
+                 weights: dict | None = None, keep_logits: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("GpuEngine needs a CUDA device (no CPU fallback)")
         self.cfg = cfg
@@ -210,6 +210,9 @@ class GpuEngine:
         self.max_entries = n_seqs if cfg.batched_forward else 1
         self.max_rows = cfg.n_batch + self.max_out
         self.logits = torch.empty((self.max_out, s.vocab), dtype=torch.float32, device=dev)
+        # False: no logits materialisation - the LM head reduces each sampled
+        # row to its argmax in its epilogue (ds_forward_args.logits_out)
+        self.keep_logits = keep_logits
         # next prompt-lookup proposal computed inside decode/verify forwards
         # (ds_forward_args.next_*): [e, len, draft_len][n] + drafts [n][cap] + scratch
         self.nd_cap = max(1, cfg.spec_max_lookahead)
@@ -457,7 +460,7 @@ class GpuEngine:
             res.data_ptr() + 8 * self.max_out, self.logits.data_ptr(),
             self.workspace.data_ptr(), self.workspace.numel(),
             self.cfg.spec_buffer if nd else 0, self.cfg.spec_min_match, self.nd_cap if nd else 0,
-            res.data_ptr() + 4 * self.nd_off)
+            res.data_ptr() + 4 * self.nd_off, int(self.keep_logits))
         check(lib().ds_model_forward(ctypes.byref(self.model_c), ctypes.byref(self.kv_c),
                                      ctypes.byref(args), sp), "ds_model_forward")
         self.gpu_launches += self.launches_per_forward(reqs)
@@ -540,11 +543,12 @@ class GpuEngine:
                 res.data_ptr(), res.data_ptr() + 4 * self.max_out,
                 res.data_ptr() + 8 * self.max_out, self.logits.data_ptr(),
                 self.workspace.data_ptr(), self.workspace.numel(), 0, self.cfg.spec_min_match,
-                0, res.data_ptr() + 4 * self.nd_off)
+                0, res.data_ptr() + 4 * self.nd_off, int(self.keep_logits))
             self._fargs, self._fargs_key = fa, (st.dev.data_ptr(), st.host.data_ptr())
             self._fargs_ref = ctypes.byref(fa)
         fa.n_rows = q
         fa.n_out = n_out
+        fa.logits_out = int(self.keep_logits)
         fa.next_window = self.cfg.spec_buffer if nd else 0
         fa.next_cap = self.nd_cap if nd else 0
         self._ev[0].record(stream)

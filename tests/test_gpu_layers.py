@@ -286,6 +286,40 @@ def test_gemm_skinny_epilogue_fusions(cuda, M):
     assert err < 2e-2 * q_ref.abs().max().item(), err
 
 
+@pytest.mark.parametrize("M", [1, 5, 6, 17, 32])
+def test_gemm_skinny_argmax_epilogue(cuda, M):
+    """Fused LM-head argmax (ds_skinny_epi.argmax_out): the
+    packed per-row key decodes to np.argmax of the same kernel's fp32 product
+    (largest value, lowest column on exact ties - duplicated weight rows make
+    bit-identical columns), with and without the product stored."""
+    from paper_2605_26289_b200._lib import SkinnyEpi, check, lib
+
+    L = lib()
+    s = torch.cuda.current_stream().cuda_stream
+    V, H = 128256, 4096
+    g = torch.Generator(device=cuda).manual_seed(100 + M)
+    X = torch.randn(M, H, device=cuda, generator=g).bfloat16()
+    W = (0.02 * torch.randn(V, H, device=cuda, generator=g)).bfloat16()
+    W[77000] = W[90000] = W[5] = (0.5 * X[0].float() / X[0].float().norm()).bfloat16()
+    Y = torch.empty(M, V, device=cuda)
+    keys = torch.zeros(32, device=cuda, dtype=torch.int64)
+    epi = SkinnyEpi(argmax_out=keys.data_ptr())
+    check(L.ds_gemm_skinny_ex(X.data_ptr(), W.data_ptr(), Y.data_ptr(), M, V, H, 1, 0,
+                              ctypes.byref(epi), s))
+    keys2 = torch.zeros(32, device=cuda, dtype=torch.int64)
+    epi2 = SkinnyEpi(argmax_out=keys2.data_ptr())
+    check(L.ds_gemm_skinny_ex(X.data_ptr(), W.data_ptr(), None, M, V, H, 1, 0,
+                              ctypes.byref(epi2), s))
+    torch.cuda.synchronize()
+    idx = (0xFFFFFFFF - (keys[:M] & 0xFFFFFFFF)).cpu()
+    assert torch.equal(idx, Y.argmax(-1).cpu())  # torch: first maximal index
+    assert torch.equal(keys, keys2)
+    assert int(idx[0]) == 5  # three identical top columns: the lowest wins
+    assert keys[M:].eq(0).all()
+    ref = X.float() @ W.float().T
+    assert (Y - ref).abs().max().item() < 1e-2
+
+
 @pytest.mark.parametrize("M", [1, 5, 17, 32])
 @pytest.mark.parametrize("norm", [False, True])
 def test_gemm_skinny_rope_kv_epilogue(cuda, M, norm):

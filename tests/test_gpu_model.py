@@ -30,7 +30,7 @@ REL_RMS = 1e-2
 def test_tiny_model_logits_vs_oracle(cuda, policy):
     cfg = CoreConfig(model="tiny", token_policy=policy, capacity_cells=4096)
     kv = UnifiedKvCache(cfg.capacity_cells)
-    eng = GpuEngine(cfg, kv, n_seqs=4)
+    eng = GpuEngine(cfg, kv, n_seqs=4, keep_logits=True)
     w = eng.weights_cpu()
     g = torch.Generator().manual_seed(5)
     prompt = torch.randint(0, cfg.shape.vocab, (300,), generator=g).tolist()
@@ -43,6 +43,7 @@ def test_tiny_model_logits_vs_oracle(cuda, policy):
     kv.append_cells(seq, 100)
     res = eng.run([EntryRequest(_lib.ENTRY_PREFILL, seq, 0, prompt, prompt)])
     got = [eng.logits[:1].cpu()]
+    ids = [res[0].argmax_id]
     toks = list(prompt)
     rows = [len(toks) - 1]
     toks.append(res[0].argmax_id)
@@ -51,6 +52,7 @@ def test_tiny_model_logits_vs_oracle(cuda, policy):
         kv.append_cells(seq, 1)
         r = eng.run([EntryRequest(_lib.ENTRY_DECODE, seq, len(toks) - 1, [toks[-1]], toks)])
         got.append(eng.logits[:1].cpu())
+        ids.append(r[0].argmax_id)
         rows.append(len(toks) - 1)
         toks.append(r[0].argmax_id)
     drafts = [7, 8, 9, 10]
@@ -68,3 +70,33 @@ def test_tiny_model_logits_vs_oracle(cuda, policy):
     top2 = ref.topk(2, dim=-1).values
     sure = (top2[:, 0] - top2[:, 1]) > 2 * TOL
     assert torch.equal(gpu.argmax(-1)[sure], ref.argmax(-1)[sure])
+    # the token rule read the argmax fused into the LM head's epilogue: it is
+    # the argmax of the logits the same launch stored
+    assert ids == gpu[:3].argmax(-1).tolist()
+
+
+def test_no_logits_materialisation(cuda):
+    """keep_logits=False (the serving default): the LM head stores nothing and
+    the greedy ids equal those of the same weights with the logits stored."""
+    cfg = CoreConfig(model="tiny", token_policy="argmax", capacity_cells=4096)
+    ids = {}
+    engines = {}
+    for keep in (True, False):
+        kv = UnifiedKvCache(cfg.capacity_cells)
+        w = engines[True].w if keep is False else None
+        eng = engines[keep] = GpuEngine(cfg, kv, n_seqs=2, weights=w, keep_logits=keep)
+        eng.logits.fill_(float("nan"))
+        g = torch.Generator().manual_seed(9)
+        toks = torch.randint(0, cfg.shape.vocab, (200,), generator=g).tolist()
+        eng.load_prompt(1, toks, 0, 0xCBF29CE484222325)
+        kv.append_cells(1, len(toks))
+        out = [eng.run([EntryRequest(_lib.ENTRY_PREFILL, 1, 0, toks, toks)])[0].argmax_id]
+        toks.append(out[-1])
+        for _ in range(4):
+            kv.append_cells(1, 1)
+            r = eng.run([EntryRequest(_lib.ENTRY_DECODE, 1, len(toks) - 1, [toks[-1]], toks)])
+            out.append(r[0].argmax_id)
+            toks.append(out[-1])
+        ids[keep] = out
+        assert eng.logits.isnan().all().item() is (not keep)
+    assert ids[True] == ids[False]

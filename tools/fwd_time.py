@@ -13,7 +13,7 @@ pts = [tuple(int(v) for v in a.split(":")) for a in sys.argv[2:]]
 mx = max(p + q for p, q in pts)
 cfg = CoreConfig(model=model, capacity_cells=mx + 512)
 kv = UnifiedKvCache(cfg.capacity_cells)
-eng = GpuEngine(cfg, kv, n_seqs=1)
+eng = GpuEngine(cfg, kv, n_seqs=1, keep_logits=True)
 toks = [(7 * i + 3) % 30000 for i in range(mx + 8)]
 eng.load_prompt(0, toks, 0, 0xCBF29CE484222325)
 tag = os.environ.get("DS_B200_LIB", "tree") + f" L2={os.environ.get('DS_L2_NEXT_MB', 'dflt')}"
