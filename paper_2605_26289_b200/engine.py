@@ -29,7 +29,7 @@ import torch
 from . import _lib
 from ._lib import check, lib
 from .config import CoreConfig
-from .kernels import FNV64_OFFSET, host_fnv1a64_tokens
+from .kernels import FNV64_OFFSET, _as_i32, host_fnv1a64_tokens
 from .kvcache import UnifiedKvCache
 
 _ENTRY_DT = np.dtype([("seq", "<i4"), ("past", "<i4"), ("q_len", "<i4"), ("q_start", "<i4"),
@@ -296,7 +296,8 @@ class GpuEngine:
         """New request on `seq`: its token history is (re)uploaded with the next
         flush; the committed-prefix hash restarts from the scheduler's
         prefix_hash (scheduler.py:237)."""
-        self._pending_hist.append((seq, 0, np.asarray(tokens, dtype=np.int32)))
+        self._pending_hist.append((seq, 0, tokens if isinstance(tokens, np.ndarray)
+                                   and tokens.dtype == np.int32 else _as_i32(tokens)))
         self._hash[seq] = (cursor, prefix_hash)
         self._draft_cache.pop(seq, None)
 

@@ -51,3 +51,29 @@ def test_eviction_tie_break_lower_first_token():
     trie.evict(2)
     assert trie.longest_prefix([3, 3]).length == 0
     assert trie.longest_prefix([5, 5]).length == 2
+
+
+def test_common_prefix_len_chunked_matches_element_loop():
+    """The chunked slice comparison returns the element loop's answer (the
+    reference `_common_len`) for every mismatch position, chunk boundaries
+    and empty inputs included."""
+    import random
+
+    from paper_2605_26289_b200.radix import common_prefix_len
+
+    def loop(a, b):
+        n, i = min(len(a), len(b)), 0
+        while i < n and a[i] == b[i]:
+            i += 1
+        return i
+
+    rng = random.Random(3)
+    for n in [0, 1, 31, 32, 33, 511, 512, 513, 544, 1100, 4096]:
+        a = [rng.randrange(5) for _ in range(n)]
+        for k in sorted({0, n // 2, n - 1 if n else 0, n, 32, 512, 543} - {-1}):
+            if k > n:
+                continue
+            b = a[:k] + [9] + a[k:]  # mismatch at k (or b longer by one when k == n)
+            assert common_prefix_len(a, b) == loop(a, b) == k
+            assert common_prefix_len(b, a) == k
+        assert common_prefix_len(a, list(a)) == n
