@@ -36,6 +36,7 @@ constexpr int kSlabA = kBM * 128;         // one 64-column slab of the weight ti
 constexpr int kThreads = 6 * 32;
 constexpr int kTmemCols = 256;
 constexpr int kSmemBudget = 112 * 1024;   // two CTAs per SM
+constexpr int kSmemBudgetWide = 220 * 1024;  // one CTA per SM
 constexpr int kMaxSplits = 8;
 }  // namespace
 
@@ -214,6 +215,33 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(
 }
 
 namespace {
+// co-resident clusters of `size` one-CTA-per-SM CTAs (kSmemBudgetWide)
+int max_clusters(int size) {
+  static int cache[kMaxSplits + 1] = {0};
+  if (size < 1 || size > kMaxSplits) return 0;
+  if (cache[size]) return cache[size];
+  cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kSmemBudgetWide);
+  cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1, 1, size);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBudgetWide;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = size;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = 148 / size;
+  }
+  return cache[size] = n;
+}
+
 struct TcPlan {
   int NT, n_tt, splits, n_stages, smem, ks;
 };
@@ -224,12 +252,25 @@ TcPlan tc_plan(int T, int N, int K) {
   p.NT = ((T + p.n_tt - 1) / p.n_tt + 15) / 16 * 16;
   if (p.NT < 32) p.NT = 32;
   const int tiles = (N / kBM) * p.n_tt, slabs = K / 64;
-  // splits: only to give every SM a CTA (wo/down/wqkv have 32-48 row tiles);
-  // a split costs a cluster reduction, so take the fewest that reach 148 CTAs
+  // splits: tiles < 148 (wo/down/wqkv) split K so that one wave of one CTA
+  // per SM holds them all, each CTA with a deep (~200 KB) ring; tiles >= 148
+  // (gate_up) run unsplit, two 112 KB CTAs per SM
+  static const int splits_env = getenv("DS_TC_SPLITS") ? atoi(getenv("DS_TC_SPLITS")) : 0;
   p.splits = 1;
-  while (p.splits < kMaxSplits && tiles * p.splits < 148 && slabs / (p.splits + 1) >= 4)
-    ++p.splits;
-  static const int budget = getenv("DS_TC_KB") ? atoi(getenv("DS_TC_KB")) * 1024 : kSmemBudget;
+  int budget = kSmemBudget;
+  if (tiles < 148) {
+    p.splits = 148 / tiles;
+    if (p.splits > kMaxSplits) p.splits = kMaxSplits;
+    while (p.splits > 1 && slabs / p.splits < 4) --p.splits;
+    // a cluster is placed inside one GPC: fewer clusters of S fit than 148/S
+    // (e.g. 3-CTA clusters of 222 KB CTAs: < 48), and one more would be a
+    // second wave
+    while (p.splits > 1 && tiles > max_clusters(p.splits)) --p.splits;
+    budget = kSmemBudgetWide;
+  }
+  if (splits_env > 0) p.splits = splits_env;
+  static const int kb_env = getenv("DS_TC_KB") ? atoi(getenv("DS_TC_KB")) * 1024 : 0;
+  if (kb_env) budget = kb_env;
   static const int ks_env = getenv("DS_TC_KS") ? atoi(getenv("DS_TC_KS")) : 1;
   p.ks = ks_env;
   while (p.ks > 1 && (K / 64) % p.ks) --p.ks;
@@ -254,8 +295,12 @@ extern "C" int ds_gemm_tc(const void* X, const void* W, void* Y, int T, int N, i
   const TcPlan p = tc_plan(T, N, K);
   if (p.smem > 227 * 1024) return DS_EUNSUPPORTED;
   if (getenv("DS_TC_VERBOSE"))
-    fprintf(stderr, "gemm_tc T=%d N=%d K=%d: NT=%d tiles=%d splits=%d ks=%d stages=%d smem=%d\n", T,
-            N, K, p.NT, (N / kBM) * p.n_tt, p.splits, p.ks, p.n_stages, p.smem);
+    fprintf(stderr,
+            "gemm_tc T=%d N=%d K=%d: NT=%d tiles=%d splits=%d ks=%d stages=%d smem=%d "
+            "(clusters of 2..8: %d %d %d %d %d %d %d)\n",
+            T, N, K, p.NT, (N / kBM) * p.n_tt, p.splits, p.ks, p.n_stages, p.smem,
+            max_clusters(2), max_clusters(3), max_clusters(4), max_clusters(5), max_clusters(6),
+            max_clusters(7), max_clusters(8));
   const CUtensorMap* tw = slab_tensor_map(W, N, K, kBM, p.ks);
   const CUtensorMap* tx = slab_tensor_map(X, T, K, p.NT, p.ks);
   if (!tw || !tx) return DS_EUNSUPPORTED;
