@@ -33,6 +33,9 @@
 #include "tc.cuh"
 #include "tma.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace ds {
 
 namespace {
@@ -407,14 +410,23 @@ __global__ void __launch_bounds__(256) attn_prefill_combine(
   *dst = make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
 }
 
-// key splits that best fill whole waves of 2 CTAs per SM (>= 8 tiles each)
+// key splits (>= 8 tiles each).  A single wave of 2 CTAs per SM that is
+// >= 85% full wins outright: short query blocks (delta ~150) are latency
+// bound, and a second wave or more splits (more combine traffic) cost more
+// than the idle slots (measured at delta=150: 7 splits 6.89 ms per forward
+// at m=32k, 22 splits 8.03, 14 splits 7.44); otherwise the split count that
+// best fills whole waves.
 static int prefill_splits(int ctas, int max_tiles) {
+  const long slots = 2L * 148;
+  int one = 0;
+  for (int s = 1; s <= kMaxSplits && static_cast<long>(ctas) * s <= slots; ++s)
+    if (s == 1 || max_tiles / s >= 8) one = s;
+  if (one > 0 && static_cast<double>(ctas) * one >= 0.85 * slots) return one;
   int best = 1;
   double best_eff = 0.0;
   for (int s = 1; s <= kMaxSplits; ++s) {
     if (s > 1 && (max_tiles / s < 8 || ctas * s > kMaxPartialCtas)) break;
     const long total = static_cast<long>(ctas) * s;
-    const long slots = 2L * 148;
     const long waves = (total + slots - 1) / slots;
     const double eff = static_cast<double>(total) / static_cast<double>(waves * slots);
     if (eff > best_eff + 1e-3) {
@@ -453,7 +465,10 @@ int launch_attn_prefill_sm100(const void* qkv, const ds_entry* entries_host,
   constexpr size_t kCounterBytes = 64 << 10;  // reserved for the decode split counters
   workspace = static_cast<uint8_t*>(workspace) + kCounterBytes;
   ws_bytes = ws_bytes > kCounterBytes ? ws_bytes - kCounterBytes : 0;
-  int splits = prefill_splits(qb_total * nkv, max_tiles);
+  static const int splits_env = getenv("DS_K6_SPLITS") ? atoi(getenv("DS_K6_SPLITS")) : 0;
+  int splits = splits_env > 0 ? splits_env : prefill_splits(qb_total * nkv, max_tiles);
+  if (getenv("DS_K6_VERBOSE"))
+    fprintf(stderr, "K6 ctas=%d max_tiles=%d splits=%d\n", qb_total * nkv, max_tiles, splits);
   const size_t need = static_cast<size_t>(n_entries) * splits * max_qb * nkv * kBM *
                       (kD + 1) * sizeof(float);
   if (splits > 1 && need > ws_bytes) splits = 1;
