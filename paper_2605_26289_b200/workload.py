@@ -37,6 +37,7 @@ class TraceRequest:
     max_tokens: int
     tools: frozenset
     expect: dict
+    session: str | None = None  # session id (session path) or None (transient + radix)
 
 
 def load_trace(name: str) -> dict:
@@ -51,7 +52,7 @@ def load_trace(name: str) -> dict:
         pieces = pp[: r["common"]] + r["pieces"]
         last[r["stream"]] = (toks, pieces)
         reqs.append(TraceRequest(r["id"], r["wave"], r["stream"], toks, pieces, r["max_tokens"],
-                                 frozenset(r["tools"]), r.get("expect", {})))
+                                 frozenset(r["tools"]), r.get("expect", {}), r.get("session")))
     tr["reqs"] = reqs
     return tr
 
@@ -72,20 +73,25 @@ class TurnRecord:
 
 def replay(core, trace: dict, wave_limit: int | None = None, max_iters: int = 200_000,
            rid_suffix: str = "") -> list[TurnRecord]:
-    """Submit each wave's requests together and step the core until they finish."""
+    """Submit each wave's requests together and step the core until they finish.
+    Session traces (mode "sessions") bind one session per id first
+    (`InferenceCore.open_session`, POST /v1/sessions) and delete them all after
+    the last wave (`close_session`, DELETE /v1/sessions/{id})."""
     from .scheduler import GenerationRequest, RequestHandle
 
     records: list[TurnRecord] = []
+    sessions = {sid: core.open_session(sid) for sid in trace.get("sessions", [])}
     for wi, wave in enumerate(waves(trace)):
         if wave_limit is not None and wi >= wave_limit:
             break
         handles = []
         for r in wave:
-            guard = core.pool.acquire("transient", timeout=1.0)
+            session = sessions[r.session] if r.session is not None else None
+            guard = None if session is not None else core.pool.acquire("transient", timeout=1.0)
             req = GenerationRequest(request_id=r.id + rid_suffix, prompt_tokens=list(r.tokens),
                                     prompt_pieces=list(r.pieces), max_tokens=r.max_tokens,
                                     temperature=0.0, seed=prompt_seed(r.tokens),
-                                    declared_tools=r.tools, guard=guard)
+                                    declared_tools=r.tools, guard=guard, session=session)
             h = RequestHandle(req)
             core.submit(h)
             handles.append((r, h))
@@ -108,6 +114,9 @@ def replay(core, trace: dict, wave_limit: int | None = None, max_iters: int = 20
             if h.error is not None:
                 raise h.error
             records.append(TurnRecord(r, h.result, (h.completed_at - h.submitted_at) * 1000.0))
+    if wave_limit is None:
+        for sid in sorted(sessions):
+            core.close_session(sessions[sid])
     return records
 
 

@@ -50,7 +50,8 @@ from deltaserve.scenarios import (  # noqa: E402
     deep_workflow,
     turn_tool_result,
 )
-from deltaserve.scheduler import GenerationRequest, InferenceCore, RequestHandle  # noqa: E402
+from deltaserve.scheduler import (  # noqa: E402
+    GenerationRequest, InferenceCore, RequestHandle, SessionHandle)
 from deltaserve.speculator import lookup_ngram  # noqa: E402
 
 assert K.BACKEND == "native"
@@ -299,13 +300,14 @@ class Recorder:
         self.last_prompt = {}  # stream key -> (tokens, pieces) for delta coding
         self.wave = 0  # requests of one wave are submitted together, then run to completion
 
-    def submit(self, stream, tokens, pieces, max_tokens, tools, rid):
-        guard = self.core.pool.acquire("transient", timeout=1.0)
+    def submit(self, stream, tokens, pieces, max_tokens, tools, rid, session=None):
+        # a session request holds no transient guard (server.py:300-318)
+        guard = None if session is not None else self.core.pool.acquire("transient", timeout=1.0)
         declared = frozenset(t["function"]["name"] for t in tools if "function" in t)
         req = GenerationRequest(request_id=rid, prompt_tokens=list(tokens),
                                 prompt_pieces=list(pieces), max_tokens=max_tokens,
                                 temperature=0.0, seed=prompt_seed(tokens),
-                                declared_tools=declared, guard=guard)
+                                declared_tools=declared, guard=guard, session=session)
         h = RequestHandle(req)
         self.core.submit(h)
         prev_t, prev_p = self.last_prompt.get(stream, ([], []))
@@ -315,6 +317,8 @@ class Recorder:
         self.last_prompt[stream] = (list(tokens), list(pieces))
         rec = {"id": rid, "wave": self.wave, "stream": stream, "common": c, "tokens": tokens[c:],
                "pieces": pieces[c:], "max_tokens": max_tokens, "tools": sorted(declared)}
+        if session is not None:
+            rec["session"] = session.session_id
         self.requests.append((h, rec))
         return h
 
@@ -402,6 +406,38 @@ def trace_sequential(name, cfg_over, scenarios, interleave=True, bursts=()):
             "requests": rec.finish_records(), "snapshots": snaps}
 
 
+def trace_sessions(name, cfg_over, scenarios, session_convs):
+    """Session path (server.py:367-387): conversations in
+    `session_convs` run on a session-pool sequence bound once (POST
+    /v1/sessions) - admission matches against session.tokens, trims the KV
+    to the match and prefills only the delta (scheduler.py:431-458); the
+    others are transient requests (radix path).  Turns interleaved; at the
+    end every session is deleted (kv.release_sequence + guard.release)."""
+    core = InferenceCore(ServerConfig(**cfg_over))
+    rec = Recorder(core)
+    convs = [Conv(sc) for sc in scenarios]
+    sessions = {i: SessionHandle(session_id=f"sess-{i}", guard=core.pool.acquire("session"))
+                for i in session_convs}
+    snaps = []
+    for t in range(max(sc.turn_count for sc in scenarios)):
+        for i, conv in enumerate(convs):
+            if t >= conv.sc.turn_count:
+                continue
+            toks, pieces = conv.prompt(core, t)
+            h = rec.submit(f"s{i}", toks, pieces, conv.sc.max_tokens, conv.sc.tools,
+                           f"{conv.sc.name}-c{i}-t{t}", session=sessions.get(i))
+            rec.run_until_done([h])
+            conv.after(t, h.result)
+            snaps.append(core_snapshot(core))
+    for i in sorted(sessions):
+        core.kv.release_sequence(sessions[i].guard.seq)
+        sessions[i].guard.release()
+    snaps.append(core_snapshot(core))
+    return {"name": name, "config": cfg_over, "mode": "sessions",
+            "sessions": [sessions[i].session_id for i in sorted(sessions)],
+            "requests": rec.finish_records(), "snapshots": snaps}
+
+
 def trace_waves(name, cfg_over, scenarios):
     """Turn-synchronous waves: turn t of every session submitted together (C5)."""
     core = InferenceCore(ServerConfig(**cfg_over))
@@ -445,12 +481,20 @@ def gen_traces():
                          [deep_c4("c4s", 8, pieces=200)]),
         trace_sequential("c4", {"spec_max_lookahead": 4, "capacity_cells": 262144},
                          [deep_c4("c4", 35)]),
+        trace_sessions("sessions", {"spec_max_lookahead": 4, "radix_enabled": False},
+                       [agentic_6turn("se1"), agentic_6turn("se2")], session_convs=(0, 1)),
+        trace_sessions("sessions_radix", {"spec_max_lookahead": 4},
+                       [agentic_6turn("sr1"), agentic_6turn("sr2"), agentic_6turn("sr1")],
+                       session_convs=(0,)),
         trace_waves("c5_small", {"pool_transient": 8, "capacity_cells": 65536},
                     [agentic_6turn(f"c5s{i}") for i in range(8)]),
         trace_waves("c5", {"pool_transient": 256, "capacity_cells": 1 << 19},
                     [agentic_6turn(f"c5s{i}") for i in range(256)]),
     ]
+    only = [a for a in sys.argv[2:]] if len(sys.argv) > 2 and sys.argv[1] == "traces" else None
     for tr in traces:
+        if only and tr["name"] not in only:
+            continue
         n = len(tr["requests"])
         last = tr["requests"][-1]
         print(f"{tr['name']}: {n} requests, last n_t={last['expect']['n_t']}")

@@ -27,7 +27,9 @@ def _device_invariants(core):
 
 @pytest.mark.parametrize("name,batched", [("c1", False), ("c2", False), ("c2_nospec", False),
                                           ("c3", False), ("c4_small", False), ("c5_small", False),
-                                          ("c2", True), ("c3", True), ("c5_small", True)])
+                                          ("c2", True), ("c3", True), ("c5_small", True),
+                                          ("sessions", False), ("sessions_radix", False),
+                                          ("sessions", True)])
 def test_trace_parity_gpu(cuda, name, batched):
     tr = load_trace(name)
     core = InferenceCore(core_config_for(tr, model="tiny", batched_forward=batched))

@@ -11,7 +11,8 @@ from oracle_engine import OracleEngine
 from paper_2605_26289_b200.scheduler import InferenceCore, SchedulerConfig, chunk_for, spec_cap
 from paper_2605_26289_b200.workload import core_config_for, load_trace, mismatches, replay
 
-TRACES = ["c1", "c2", "c2_nospec", "c3", "c3_nogroup", "c4_small", "c5_small"]
+TRACES = ["c1", "c2", "c2_nospec", "c3", "c3_nogroup", "c4_small", "c5_small", "sessions",
+          "sessions_radix"]
 
 
 @pytest.mark.parametrize("batched", [False, True])
