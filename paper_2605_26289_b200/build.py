@@ -25,7 +25,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-re
 
 SOURCES = ["policy.cu", "kvmeta.cu", "layers.cu", "attn_split.cu", "attn_decode.cu", "attn_decode_tc.cu",
            "attn_prefill_sm100.cu",
-           "gemm_skinny.cu", "gemm_tc.cu", "tma.cu",
+           "gemm_skinny.cu", "gemm_tc.cu", "gemm_lt.cu", "tma.cu",
            "runtime.cu"]
 
 
@@ -55,7 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L/usr/local/cuda/lib64", "-lcublas", "-lcudart",
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L/usr/local/cuda/lib64", "-lcublas", "-lcublasLt", "-lcudart",
            "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

@@ -1,0 +1,26 @@
+"""cuBLASLt heuristic candidates vs the cublasGemmEx default on the 8B
+projections at prefill / batched row counts (ds_debug_lt_sweep; 4 rotating
+weight copies > L2).  Usage: bench_lt.py [T ...]"""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2605_26289_b200._lib import lib
+
+L = lib()
+f = L.ds_debug_lt_sweep
+P = ctypes.c_void_p
+f.argtypes = [P, P, ctypes.c_int, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+              ctypes.c_int, P]
+dev = torch.device("cuda", 0)
+s = torch.cuda.current_stream().cuda_stream
+for T in [int(x) for x in (sys.argv[1:] or ["150"])]:
+    for name, N, K, f32 in (("qkv", 6144, 4096, 0), ("o", 4096, 4096, 1),
+                            ("gate_up", 28672, 4096, 0), ("down", 4096, 14336, 1)):
+        X = torch.randn(T, K, device=dev).bfloat16()
+        Ws = [(0.02 * torch.randn(N, K, device=dev)).bfloat16() for _ in range(4)]
+        arr = (P * 4)(*[w.data_ptr() for w in Ws])
+        Y = torch.zeros(T, N, device=dev, dtype=torch.float32 if f32 else torch.bfloat16)
+        print(f"== T={T} {name}", file=sys.stderr, flush=True)
+        rc = f(X.data_ptr(), arr, 4, Y.data_ptr(), T, N, K, f32, 20, s)
+        assert rc == 0, rc
+        del Ws
