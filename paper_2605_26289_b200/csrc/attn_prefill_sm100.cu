@@ -53,6 +53,10 @@ constexpr int kSmemBar = kSmemV + kVStages * 2 * kKHalf;  // 112 KB: two CTAs pe
 constexpr int kSmemBytes = kSmemBar + 128;
 constexpr int kTmemCols = 256;  // S0/P0 [0,64) S1/P1 [64,128) O [128,256)
 constexpr int kMaxSplits = 64;
+#ifndef DS_K6_POLY
+#define DS_K6_POLY 0
+#endif
+constexpr int kPolyPeriod = DS_K6_POLY;  // see the softmax loop
 constexpr int kMaxPartialCtas = 8 * 148;  // bounds the split-partial workspace
 
 // 16-byte chunk c (0..15 over d) of row r in a tile of `rows` rows, SW128
@@ -297,12 +301,18 @@ __global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
       const float mref = new_ref == -INFINITY ? 0.f : new_ref;
       float spart[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial sums
       uint32_t pk[kBN / 2];
-      // (a share of the exponentials on an FMA-pipe polynomial was measured
-      // slower: MUFU is not the limit here)
+      // every kPolyPeriod-th pair of exponentials on the FMA pipe (0 = all on
+      // the MUFU, the default: offloading 1/8, 1/4, 1/2 measured 2.4%, 6%,
+      // 15% slower at delta=881 over 31.5k keys - the MUFU is not the limit,
+      // the per-tile softmax dependency chain is)
 #pragma unroll
       for (int i = 0; i < kBN; i += 2) {
-        const float p0 = fast_exp2(fmaf(__uint_as_float(sv[i]), scale_log2, -mref));
-        const float p1 = fast_exp2(fmaf(__uint_as_float(sv[i + 1]), scale_log2, -mref));
+        const bool poly = kPolyPeriod > 0 && (i / 2) % (kPolyPeriod > 0 ? kPolyPeriod : 1) ==
+                                                 (kPolyPeriod > 0 ? kPolyPeriod - 1 : 0);
+        const float x0 = fmaf(__uint_as_float(sv[i]), scale_log2, -mref);
+        const float x1 = fmaf(__uint_as_float(sv[i + 1]), scale_log2, -mref);
+        const float p0 = poly ? poly_exp2(x0) : fast_exp2(x0);
+        const float p1 = poly ? poly_exp2(x1) : fast_exp2(x1);
         spart[(i / 2) & 3] += p0 + p1;
         pk[i / 2] = pack_bf16(p0, p1);
       }

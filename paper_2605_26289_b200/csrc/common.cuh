@@ -104,6 +104,21 @@ DS_DEVICE float fast_exp2(float x) {
   return y;
 }
 
+// 2^x on the FMA/ALU pipes (offloads the MUFU): x = n + f with n = rint(x)
+// (1.5 * 2^23 shifter), f in [-0.5, 0.5], 2^f by a degree-3 polynomial
+// (relative error < 5e-4, under the bf16 rounding of P), then n added to the
+// exponent field.  x is clamped at -126 (masked scores: -inf -> ~0).
+DS_DEVICE float poly_exp2(float x) {
+  x = fmaxf(x, -126.f);
+  const float r = __fadd_rn(x, 12582912.f);
+  const float f = __fsub_rn(x, __fsub_rn(r, 12582912.f));
+  float p = fmaf(f, 0.0555041087f, 0.2402265070f);
+  p = fmaf(p, f, 0.6931471806f);
+  p = fmaf(p, f, 1.0f);
+  const int n = __float_as_int(r) - 0x4B400000;
+  return __int_as_float(__float_as_int(p) + (n << 23));
+}
+
 }  // namespace ds
 
 // ---------------------------------------------------------------------------

@@ -16,4 +16,6 @@ pr.enable()
 core.reset_state(); replay(core, tr)
 pr.disable()
 print(f"wall {time.perf_counter() - t0:.2f} s, device {core.engine.device_seconds():.2f} s")
-st = pstats.Stats(pr); st.sort_stats("tottime").print_stats(22)
+st = pstats.Stats(pr)
+for key in (sys.argv[1:] or ["tottime"]):
+    st.sort_stats(key).print_stats(45)
