@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
   const int G = nh / nkv;
   const int R = en.q_len * G;
   const int kv_len = en.past + en.q_len;
-  const AttnSplitPlan plan = attn_split_plan(1, kv_len, nkv, n_entries, 1);
+  const AttnSplitPlan plan = attn_split_plan(1, kv_len, nkv, n_entries, 1, R);
   const bool active = split < plan.n_splits;  // idle CTAs still join the cluster merge
   const int kh = blockIdx.y;
   const int k_begin = split * plan.split_len;
@@ -547,7 +547,8 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
   for (int e = 0; e < n_entries; ++e) {
     const int kv = entries_host[e].past + entries_host[e].q_len;
     max_kv = kv > max_kv ? kv : max_kv;
-    const AttnSplitPlan p = attn_split_plan(1, kv, nkv, n_entries, 1);
+    const AttnSplitPlan p =
+        attn_split_plan(1, kv, nkv, n_entries, 1, entries_host[e].q_len * (nh / nkv));
     max_split_len = p.split_len > max_split_len ? p.split_len : max_split_len;
   }
   // one K/V tile per split (short prefixes): a one-stage ring keeps the CTA

@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
   const int G = nh / nkv;
   const int R = en.q_len * G;
   const int kv_len = en.past + en.q_len;
-  const AttnSplitPlan plan = attn_split_plan(1, kv_len, nkv, n_entries, 1);
+  const AttnSplitPlan plan = attn_split_plan(1, kv_len, nkv, n_entries, 1, R);
   const bool active = split < plan.n_splits;  // idle CTAs still join the cluster merge
   const bool cluster_merge = max_splits <= kDecodeMaxCluster;
   const int kh = blockIdx.y;

@@ -32,6 +32,10 @@ constexpr int kDecodeTcMinRows = 8;
 // combine kernel
 constexpr int kDecodeLastMergeRows = 8;
 constexpr int kDecodeTcMinKeys = 4096;
+#ifndef DS_K7_SHORT_TILES
+#define DS_K7_SHORT_TILES (8 * kDecodeMaxCluster)
+#endif
+constexpr int kDecodeShortTiles = DS_K7_SHORT_TILES;  // see attn_split_plan
 constexpr int kSplitRows = 64;  // packed rows per split-kernel CTA (4 warps x 16)
 
 struct AttnSplitPlan {
@@ -41,11 +45,21 @@ struct AttnSplitPlan {
 
 // mode 0: split kernel (~2 CTAs per SM, ceil); mode 1: warp-specialised decode
 // kernel (one CTA per SM, floor so the grid is a single wave).
-DS_HD AttnSplitPlan attn_split_plan(int qblocks, int kv_len, int nkv, int n_entries, int mode) {
+// rows: the entry's packed query rows.  Decode entries of more than
+// kDecodeLastMergeRows rows merge more than a cluster's worth of splits in the
+// combine kernel (one more launch, ~6 us per layer in the forward); up to
+// kDecodeShortTiles key tiles (8k keys) they take at most a cluster's worth
+// of splits instead: q=5 forward at m=2k 3.07 -> 2.98 ms, 4k 3.09 -> 3.02,
+// 4.2k 3.10 -> 3.03, 6k 3.08 -> 3.06; a 16k cap was slower from 8k keys on.
+DS_HD AttnSplitPlan attn_split_plan(int qblocks, int kv_len, int nkv, int n_entries, int mode,
+                                    int rows) {
   const int ctas = qblocks * nkv * n_entries;
   int n = mode ? kNumSMs / ctas : (2 * kNumSMs + ctas - 1) / ctas;
   const int by_len = (kv_len + 127) / 128;
   if (n > by_len) n = by_len;
+  if (mode && rows > kDecodeLastMergeRows && n > kDecodeMaxCluster &&
+      by_len <= kDecodeShortTiles)
+    n = kDecodeMaxCluster;
   if (n > 64) n = 64;
   if (n < 1) n = 1;
   const int gran = mode ? 128 : 64;  // key tile of the kernel
@@ -64,7 +78,7 @@ DS_HD int64_t attn_partial_base(const ds_entry* entries, int e, int n_entries, i
     const int R = entries[i].q_len * G;
     const int qb = (R + kSplitRows - 1) / kSplitRows;
     const AttnSplitPlan p =
-        attn_split_plan(qb, entries[i].past + entries[i].q_len, nkv, n_entries, mode);
+        attn_split_plan(qb, entries[i].past + entries[i].q_len, nkv, n_entries, mode, R);
     if (p.n_splits > 1) base += static_cast<int64_t>(p.n_splits) * R;
   }
   return base;

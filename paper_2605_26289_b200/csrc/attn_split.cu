@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(NW * 32) attn_split_kernel(
   const int qblocks = (R + NW * 16 - 1) / (NW * 16);
   if (static_cast<int>(blockIdx.x) >= qblocks) return;
   const int kv_len = en.past + en.q_len;
-  const AttnSplitPlan plan = attn_split_plan(qblocks, kv_len, nkv, n_entries, 0);
+  const AttnSplitPlan plan = attn_split_plan(qblocks, kv_len, nkv, n_entries, 0, R);
   if (split >= plan.n_splits) return;
   const int kh = blockIdx.y;
   const int row0 = blockIdx.x * NW * 16;
@@ -267,7 +267,8 @@ __global__ void attn_combine_kernel(const ds_entry* __restrict__ entries, int n_
   if (r >= R) return;
   const int kh = blockIdx.y;
   const int qblocks = (R + qblock_rows - 1) / qblock_rows;
-  const AttnSplitPlan plan = attn_split_plan(qblocks, en.past + en.q_len, nkv, n_entries, mode);
+  const AttnSplitPlan plan =
+      attn_split_plan(qblocks, en.past + en.q_len, nkv, n_entries, mode, R);
   if (plan.n_splits <= 1) return;
   const int64_t base = attn_partial_base(entries, e, n_entries, nh, nkv, mode);
   // two dependent L2 round trips in all: the split lse values (one thread
@@ -327,7 +328,7 @@ int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_en
     const ds_entry& en = entries_host[e];
     const int R = en.q_len * (nh / nkv);
     const int qb = (R + kSplitNW * 16 - 1) / (kSplitNW * 16);
-    const AttnSplitPlan p = attn_split_plan(qb, en.past + en.q_len, nkv, n_entries, mode);
+    const AttnSplitPlan p = attn_split_plan(qb, en.past + en.q_len, nkv, n_entries, mode, R);
     max_splits = p.n_splits > max_splits ? p.n_splits : max_splits;
     any_split |= p.n_splits > 1;
   }

@@ -258,7 +258,8 @@ std::string graph_key(const ds_model* m, const ds_kv_store* kv, const ds_forward
   for (int e = 0; e < a->n_entries; ++e) {
     const ds_entry& en = a->entries_host[e];
     const int kv_len = en.past + en.q_len;
-    const AttnSplitPlan p = attn_split_plan(1, kv_len, m->n_kv_heads, a->n_entries, 1);
+    const AttnSplitPlan p =
+        attn_split_plan(1, kv_len, m->n_kv_heads, a->n_entries, 1, en.q_len * G);
     // decode / verify (K7): the split plan fixes every launch shape; prefill
     // chunks (K6 + library GEMMs): the exact (past, q_len)
     const bool k6 = en.q_len * G > kDecodeMaxRows;
