@@ -431,7 +431,13 @@ static int prefill_splits(int ctas, int max_tiles) {
   int one = 0;
   for (int s = 1; s <= kMaxSplits && static_cast<long>(ctas) * s <= slots; ++s)
     if (s == 1 || max_tiles / s >= 8) one = s;
-  if (one > 0 && static_cast<double>(ctas) * one >= 0.85 * slots) return one;
+  // ... as long as a split's key range of every head stays L2-resident while
+  // all query blocks stream it (<= 96 tiles: 8 heads x 6k keys x 512 B =
+  // 25 MB): one split over a 32k prefix has every CTA stream the whole 134 MB
+  // from HBM (C4 prefill 22 -> 38 ms per chunk when delta >= 1009 took it)
+  if (one > 0 && static_cast<double>(ctas) * one >= 0.85 * slots &&
+      (max_tiles + one - 1) / one <= 96)
+    return one;
   int best = 1;
   double best_eff = 0.0;
   for (int s = 1; s <= kMaxSplits; ++s) {

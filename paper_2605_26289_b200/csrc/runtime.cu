@@ -276,9 +276,12 @@ int ds_model_forward(const ds_model* m, const ds_kv_store* kv, const ds_forward_
   if (!m || !kv || !a || a->n_rows <= 0 || a->n_entries <= 0 || a->n_out <= 0) return DS_EINVAL;
   cudaStream_t stream = (cudaStream_t)stream_;
   static const bool graphs = !(getenv("DS_GRAPHS") && atoi(getenv("DS_GRAPHS")) == 0);
-  // single-entry forwards: decode / verify (<= 32 rows) and prefill chunks
-  // (DS_GRAPHS=2: decode / verify only)
-  static const bool graph_prefill = !(getenv("DS_GRAPHS") && atoi(getenv("DS_GRAPHS")) == 2);
+  // single-entry decode / verify forwards (<= 32 rows; the key is the split
+  // plan, which repeats across prefix lengths).  DS_GRAPHS=3 also captures
+  // prefill chunks, keyed by their exact (past, q_len): a real workload
+  // rarely repeats one, so the capture + instantiate (~10 ms) lands on the
+  // critical path (C4 prefill 691 -> 1077 ms per step) - A/B only.
+  static const bool graph_prefill = getenv("DS_GRAPHS") && atoi(getenv("DS_GRAPHS")) == 3;
   if (graphs && a->n_entries == 1 && (a->n_rows <= 32 || graph_prefill)) {
     static thread_local std::unordered_map<std::string, GraphEntry> cache;
     if (cache.size() > 512) {  // bound: drop everything (rare - signatures repeat)
