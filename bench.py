@@ -384,15 +384,15 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
     elapsed, gpu_s = stats.tolist()
     launches = eng.gpu_launches - launches0
-    if rank != 0:
-        return
-    if args.workload.startswith("c5"):
+    if args.workload.startswith("c5"):  # every rank joins (sessions are sharded)
         local = torch.tensor([len(recs)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(local)
         total_turns = float(local.item())
     else:
         total_turns = nturns * args.steps * world
+    if rank != 0:
+        return
     warm = [r.latency_ms for r in recs if r.result.cached_prompt_tokens > 0] or \
         [r.latency_ms for r in recs]
     prefill_tok = sum(r.result.prefill_tokens for r in recs)
@@ -449,12 +449,14 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "forward_roofline": fwd_roof,
         "clocks": clk.summary(),
     }
-    if not args.no_micro:
+    # per-GPU extras (kernel micro-benchmarks, prefix curve, CPU baseline) at
+    # N=1 only: under torchrun the other ranks have already finished
+    if not args.no_micro and world == 1:
         line["kernels"] = kernel_micro(torch, dev, peaks)
         from paper_2605_26289_b200.curve import prefix_curve
 
         line["prefix_curve"] = prefix_curve(model=args.model, weights=eng.w)
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:
         ref = reference_turns(args.workload, 2)
         n, aff, model = cpu_info()
         line["cpu_baseline"] = {
