@@ -10,21 +10,31 @@
 namespace ds {
 
 // Called by all `nthreads` merge threads (tid < nthreads) of every CTA in the
-// cluster, between two cluster_sync_all(); `bar_id` names a barrier over those
-// threads.  cw: [>= R][kDecodeMaxCluster] scratch for the split weights.
+// cluster, between two cluster_sync_all().  One remote round trip per output
+// float4: each thread issues the row's split lse values and its split O
+// columns (float4) together, then forms the split weights 2^(lse_p - max) /
+// sum in split order (the same arithmetic as a per-row weight pass, without
+// its barrier and second round trip).  cw and bar_id are unused (kept for the
+// callers' layout).
 DS_DEVICE void decode_cluster_merge(const float* cval, const float* clse, float* cw, int R,
                                     int n_splits, int cluster, int tid, int nthreads, int bar_id,
                                     const ds_entry& en, int nh, int kh, int G,
                                     __nv_bfloat16* __restrict__ out) {
-  constexpr int kD = 128;
+  constexpr int kD = 128, kD4 = kD / 4;
+  (void)cw;
+  (void)bar_id;
   const uint32_t rank = cluster_ctarank();
-  // per-row split weights 2^(lse_p - max) / sum, in split order; all remote
-  // loads are issued before any is consumed (DSMEM round trips overlap)
-  for (int i = tid; i < R; i += nthreads) {
+  for (int idx = static_cast<int>(rank) * nthreads + tid; idx < R * kD4;
+       idx += cluster * nthreads) {
+    const int r = idx / kD4, d4 = idx - r * kD4;
+    const uint32_t a = smem_u32(cval + r * kD + 4 * d4), al = smem_u32(clse + r);
+    float4 v[kDecodeMaxCluster];
     float lv[kDecodeMaxCluster];
 #pragma unroll
-    for (int p = 0; p < kDecodeMaxCluster; ++p)
-      lv[p] = p < n_splits ? dsmem_ld_f32(dsmem_map(smem_u32(clse + i), p)) : -INFINITY;
+    for (int p = 0; p < kDecodeMaxCluster; ++p) {
+      v[p] = p < n_splits ? dsmem_ld_f32x4(dsmem_map(a, p)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      lv[p] = p < n_splits ? dsmem_ld_f32(dsmem_map(al, p)) : -INFINITY;
+    }
     float lmax = -INFINITY;
 #pragma unroll
     for (int p = 0; p < kDecodeMaxCluster; ++p) lmax = fmaxf(lmax, lv[p]);
@@ -35,23 +45,19 @@ DS_DEVICE void decode_cluster_merge(const float* cval, const float* clse, float*
       wsum += lv[p];
     }
     const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int p = 0; p < kDecodeMaxCluster; ++p) cw[i * kDecodeMaxCluster + p] = lv[p] * inv;
-  }
-  named_bar_sync(bar_id, nthreads);
-  for (int idx = static_cast<int>(rank) * nthreads + tid; idx < R * kD; idx += cluster * nthreads) {
-    const int r = idx / kD, d = idx - r * kD;
-    const uint32_t a = smem_u32(cval + r * kD + d);
-    float v[kDecodeMaxCluster];
-#pragma unroll
-    for (int p = 0; p < kDecodeMaxCluster; ++p)
-      v[p] = p < n_splits ? dsmem_ld_f32(dsmem_map(a, p)) : 0.f;
-    float acc = 0.f;
-#pragma unroll
-    for (int p = 0; p < kDecodeMaxCluster; ++p) acc += cw[r * kDecodeMaxCluster + p] * v[p];
+    for (int p = 0; p < kDecodeMaxCluster; ++p) {
+      const float w = lv[p] * inv;
+      acc.x += w * v[p].x;
+      acc.y += w * v[p].y;
+      acc.z += w * v[p].z;
+      acc.w += w * v[p].w;
+    }
     const int ti = r / G, gi = r - ti * G;
-    out[static_cast<int64_t>(en.q_start + ti) * nh * kD + (kh * G + gi) * kD + d] =
-        __float2bfloat16_rn(acc);
+    __nv_bfloat16* dst =
+        out + static_cast<int64_t>(en.q_start + ti) * nh * kD + (kh * G + gi) * kD + 4 * d4;
+    *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
   }
 }
 
