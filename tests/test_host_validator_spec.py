@@ -102,3 +102,26 @@ def test_acceptance_ema_matches_reference():
             rs.update_acceptance(b, rs.SpecOutcome(proposed=k, accepted=acc))
             assert a.ema == b.ema
             assert 0.0 <= a.ema <= 1.0
+
+
+def test_spec_cap_and_chunk_for_match_reference():
+    """Planner helpers (SURVEY 8a a11 chunk_for, a19 spec_cap) over random
+    configs, decoder counts, acceptance EMAs and prefill counts."""
+    _ref()
+    from deltaserve import scheduler as rsch
+
+    from paper_2605_26289_b200 import scheduler as osch
+
+    rng = random.Random(11)
+    for _ in range(3000):
+        cmin = rng.choice([16, 64, 128])
+        fair = rng.choice([cmin, 256, 1024])
+        cmax = rng.choice([fair, 2048, 4096])
+        kw = dict(n_batch=rng.choice([cmax, 4096, 8192]), chunk_min=cmin, fair_chunk=fair,
+                  chunk_max=cmax, spec_base_cap=rng.choice([4, 16, 32]),
+                  spec_d0=rng.choice([1, 2, 4, 8]), spec_floor_cap=rng.choice([1, 2]))
+        a, b = osch.SchedulerConfig(**kw), rsch.SchedulerConfig(**kw)
+        n, lat = rng.randrange(0, 300), rng.random() < 0.5
+        assert osch.chunk_for(a, n, lat) == rsch.chunk_for(b, n, lat)
+        d, ema = rng.randrange(0, 600), rng.random()
+        assert osch.spec_cap(d, ema, a) == rsch.spec_cap(d, ema, b)
