@@ -56,6 +56,9 @@ constexpr int kMaxSplits = 64;
 #ifndef DS_K6_POLY
 #define DS_K6_POLY 0
 #endif
+#ifndef DS_K6_F32X2  // packed FFMA2 / FADD2 in the softmax (0: scalar, the poly A/B path)
+#define DS_K6_F32X2 1
+#endif
 constexpr int kPolyPeriod = DS_K6_POLY;  // see the softmax loop
 constexpr int kMaxPartialCtas = 8 * 148;  // bounds the split-partial workspace
 
@@ -305,6 +308,33 @@ __global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
       // the MUFU, the default: offloading 1/8, 1/4, 1/2 measured 2.4%, 6%,
       // 15% slower at delta=881 over 31.5k keys - the MUFU is not the limit,
       // the per-tile softmax dependency chain is)
+#if DS_K6_F32X2
+      // packed FFMA2 / FADD2 (sm_100): the scale-subtract and the row sums two
+      // columns per instruction - 5 instead of 7 per column pair; K6 at
+      // delta=881 over 31.5k keys 459 -> 447 us (1.00 -> 1.03 PFLOP/s)
+      uint64_t acc2[2] = {0ull, 0ull};
+      uint64_t sc2, mr2;
+      asm("mov.b64 %0, {%1, %1};" : "=l"(sc2) : "f"(scale_log2));
+      asm("mov.b64 %0, {%1, %1};" : "=l"(mr2) : "f"(-mref));
+#pragma unroll
+      for (int i = 0; i < kBN; i += 2) {
+        uint64_t sx, x2;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(sx) : "r"(sv[i]), "r"(sv[i + 1]));
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(x2) : "l"(sx), "l"(sc2), "l"(mr2));
+        float x0, x1;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(x0), "=f"(x1) : "l"(x2));
+        const float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
+        uint64_t pp;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(pp) : "f"(p0), "f"(p1));
+        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc2[(i / 2) & 1]) : "l"(pp));
+        pk[i / 2] = pack_bf16(p0, p1);
+      }
+      float a0, a1, a2, a3;
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc2[0]));
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(a2), "=f"(a3) : "l"(acc2[1]));
+      (void)spart;
+      const float sum = (a0 + a1) + (a2 + a3);
+#else
 #pragma unroll
       for (int i = 0; i < kBN; i += 2) {
         const bool poly = kPolyPeriod > 0 && (i / 2) % (kPolyPeriod > 0 ? kPolyPeriod : 1) ==
@@ -317,6 +347,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
         pk[i / 2] = pack_bf16(p0, p1);
       }
       const float sum = (spart[0] + spart[1]) + (spart[2] + spart[3]);
+#endif
       tc::st32(trow + sb * kBN, pk);  // P_j over its own S columns
       // PV_{j-1} done (O stable) before an O correction and before PV_j is issued
       if (jj > 0) {
