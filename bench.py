@@ -340,7 +340,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     from paper_2605_26289_b200.scheduler import InferenceCore
-    from paper_2605_26289_b200.workload import core_config_for, load_trace, replay
+    from paper_2605_26289_b200.workload import core_config_for, load_trace, mismatches, replay
 
     peaks = _peaks()
     tr = load_trace(args.workload)
@@ -384,6 +384,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
     elapsed, gpu_s = stats.tolist()
     launches = eng.gpu_launches - launches0
+    # parity gate on the measured run itself: every turn's result fields equal
+    # the reference InferenceCore's recorded results for the same trace
+    bad = mismatches(recs)
+    if bad:
+        raise SystemExit(f"bench: {len(bad)} parity mismatches vs the reference trace: {bad[:3]}")
     if args.workload.startswith("c5"):  # every rank joins (sessions are sharded)
         local = torch.tensor([len(recs)], dtype=torch.float64, device=dev)
         if world > 1:
@@ -442,6 +447,12 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             "device": round(1000 * gpu_s / args.steps, 3),
             "wall": round(1000 * elapsed / args.steps, 3)},
         "gpu_launches": launches,
+        "parity": {"turns": len(recs), "mismatches": len(bad),
+                   "against": f"reference InferenceCore results recorded for trace "
+                              f"{args.workload} (tests/golden/traces)"},
+        "value_basis": "turns / device time of every launch sequence in the step (page-table "
+                       "and history metadata kernels, K1 proposals, forwards), CUDA events on "
+                       "the launching stream; e2e = turns / wall clock through InferenceCore",
         "e2e": {"value": round(total_turns / elapsed, 3), "unit": UNIT,
                 "h2d_bytes_per_step": int(eng.h2d_bytes / args.steps),
                 "d2h_bytes_per_step": int(eng.d2h_bytes / args.steps)},
@@ -481,8 +492,21 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--batched", action="store_true", help="one forward per plan (multi-session)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
+    if world != args.gpus and args.impl != "reference":
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; using {world}", file=sys.stderr)
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
         run_reference_arm(args, rank, world)

@@ -108,6 +108,15 @@ int ds_hist_write(const int32_t* src, const int32_t* segs, int n_segs, int32_t* 
 int ds_kv_copy_cells(void* k_pool, void* v_pool, int layers, int n_kv_heads, int64_t head_stride,
                      int head_dim, const int32_t* pairs, int n, ds_stream_t stream);
 
+/* Prefix migration payload (multi-GPU): pack the K and V rows of
+ * n cells (all layers) into buf [L][2][nkv][n][hd] bf16 (unpack = 0), or
+ * scatter a received buffer into the cells (unpack = 1).  The reference is
+ * single-GPU; the receiving side replaces the re-prefill a
+ * radix miss would cost (scheduler.py:422-480 _admit). */
+int ds_kv_pack_cells(void* k_pool, void* v_pool, int layers, int n_kv_heads, int64_t head_stride,
+                     int head_dim, const int32_t* cells, int n, void* buf, int unpack,
+                     ds_stream_t stream);
+
 /* Derived refcount (popcount(member) + trie_ref) and occupancy (cells with
  * refcount > 0) - the device view of kvcache.py:91-100, 185-187. */
 int ds_kv_refcount(const uint32_t* member, int mask_words, const int32_t* trie_ref,

@@ -108,6 +108,7 @@ def lib() -> ctypes.CDLL:
         "ds_hist_write": (c_i32, [P, P, c_i32, P, c_i64, P]),
         "ds_kv_copy_cells": (c_i32, [P, P, c_i32, c_i32, c_i64, c_i32, P, c_i32, P]),
         "ds_kv_refcount": (c_i32, [P, c_i32, P, c_i64, P, P, P]),
+        "ds_kv_pack_cells": (c_i32, [P, P, c_i32, c_i32, c_i64, c_i32, P, c_i32, P, c_i32, P]),
         "ds_forward_workspace_bytes": (ctypes.c_size_t, [P, c_i32, c_i32, c_i32]),
         "ds_model_forward": (c_i32, [P, P, P, P]),
         "ds_rope_kv_store": (c_i32, [P, c_i32, P, P, P, c_i64, c_i32, c_i32, c_i32, P, P, P, P,

@@ -23,9 +23,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")] + os.environ.get("DS_NVCC_EXTRA", "").split()
 
-SOURCES = ["policy.cu", "kvmeta.cu", "layers.cu", "attn_split.cu", "attn_decode.cu", "attn_decode_tc.cu",
-           "attn_prefill_sm100.cu",
-           "gemm_skinny.cu", "gemm_tc.cu", "gemm_lt.cu", "tma.cu",
+SOURCES = ["policy.cu", "kvmeta.cu", "layers.cu", "attn_dispatch.cu", "attn_decode.cu",
+           "attn_decode_tc.cu", "attn_prefill_sm100.cu", "gemm_skinny.cu", "gemm_tc.cu", "tma.cu",
            "runtime.cu"]
 
 

@@ -91,7 +91,6 @@ class CoreConfig:
     token_policy: str = "copy"        # "copy" (reference rule, bit-exact) | "argmax"
     seed: int = 0                     # random-init weights
     batched_forward: bool = False     # one varlen forward per plan (scheduler.py:652-660)
-    attn_impl: int = 0                # 0 auto, 1 split-KV mma kernel, 2 tcgen05 prefill
     extra: dict = field(default_factory=dict)
 
     @property

@@ -57,7 +57,10 @@ constexpr int kMaxSplits = 64;
 #define DS_K6_POLY 0
 #endif
 #ifndef DS_K6_F32X2  // packed FFMA2 / FADD2 in the softmax (0: scalar, the poly A/B path)
-#define DS_K6_F32X2 1
+#define DS_K6_F32X2 (DS_K6_POLY == 0)
+#endif
+#if DS_K6_F32X2 && DS_K6_POLY
+#error "DS_K6_POLY (FMA-pipe exponentials) is implemented on the scalar softmax: set DS_K6_F32X2=0"
 #endif
 constexpr int kPolyPeriod = DS_K6_POLY;  // see the softmax loop
 constexpr int kMaxPartialCtas = 8 * 148;  // bounds the split-partial workspace

@@ -101,9 +101,46 @@ __global__ void kv_copy_cells_kernel(__nv_bfloat16* k_pool, __nv_bfloat16* v_poo
   }
 }
 
+// Prefix migration payload (dist.py): the K and V rows of n cells, all
+// layers, packed as buf[L][2][nkv][n][hd] - one contiguous message per
+// migrated prefix.  unpack = 1 scatters a received buffer straight into the
+// freshly allocated cells (head-major pool [L][nkv][head_stride][hd]).
+__global__ void kv_pack_cells_kernel(__nv_bfloat16* k_pool, __nv_bfloat16* v_pool, int nkv,
+                                     int64_t head_stride, int hd, const int32_t* cells, int n,
+                                     __nv_bfloat16* buf, int unpack) {
+  const int i = blockIdx.x, l = blockIdx.y;
+  const int64_t cell = cells[i];
+  const int per_head = hd / 8;
+  const int64_t layer = static_cast<int64_t>(l) * nkv * head_stride * hd;
+  for (int j = threadIdx.x; j < 2 * nkv * per_head; j += blockDim.x) {
+    const int kv = j / (nkv * per_head);
+    const int rem = j - kv * nkv * per_head;
+    const int h = rem / per_head, c = rem - h * per_head;
+    __nv_bfloat16* pool = kv ? v_pool : k_pool;
+    uint4* p = reinterpret_cast<uint4*>(pool + layer + (h * head_stride + cell) * hd) + c;
+    uint4* b = reinterpret_cast<uint4*>(
+                   buf + ((((static_cast<int64_t>(l) * 2 + kv) * nkv + h) * n + i) * hd)) + c;
+    if (unpack)
+      *p = *b;
+    else
+      *b = *p;
+  }
+}
+
 }  // namespace ds
 
 extern "C" {
+
+int ds_kv_pack_cells(void* k_pool, void* v_pool, int layers, int n_kv_heads, int64_t head_stride,
+                     int head_dim, const int32_t* cells, int n, void* buf, int unpack,
+                     ds_stream_t stream) {
+  if (n < 0 || head_dim % 8 || layers <= 0 || n_kv_heads <= 0) return DS_EINVAL;
+  if (n == 0) return DS_OK;
+  ds::kv_pack_cells_kernel<<<dim3(n, layers), 256, 0, (cudaStream_t)stream>>>(
+      static_cast<__nv_bfloat16*>(k_pool), static_cast<__nv_bfloat16*>(v_pool), n_kv_heads,
+      head_stride, head_dim, cells, n, static_cast<__nv_bfloat16*>(buf), unpack);
+  return (int)cudaGetLastError();
+}
 
 int ds_kv_copy_cells(void* k_pool, void* v_pool, int layers, int n_kv_heads, int64_t head_stride,
                      int head_dim, const int32_t* pairs, int n, ds_stream_t stream) {

@@ -256,7 +256,9 @@ class GpuEngine:
     def reset_counters(self) -> None:
         self.h2d_bytes = 0
         self.d2h_bytes = 0
-        self._fwd = {"prefill": [0, 0.0, 0, 0], "decode": [0, 0.0, 0, 0]}  # n, s, rows, kv
+        # n, device seconds, rows, kv; "propose" = the K1 launches outside forwards
+        self._fwd = {"prefill": [0, 0.0, 0, 0], "decode": [0, 0.0, 0, 0],
+                     "propose": [0, 0.0, 0, 0]}
 
     def device_seconds(self) -> float:
         return sum(v[1] for v in self._fwd.values())
@@ -448,9 +450,9 @@ class GpuEngine:
         self.h2d_bytes += 4 * st.n
         stream = torch.cuda.current_stream()
         sp = stream.cuda_stream
+        self._ev[0].record(stream)  # device time includes the metadata kernels
         self._apply_metadata(*meta, sp)
         res = self.res_dev
-        self._ev[0].record(stream)
         # decode / verify only: the next proposal rides in the same launch
         nd = self.fused_drafts and all(r.kind != _lib.ENTRY_PREFILL and not r.scratch
                                        for r in reqs)
@@ -532,6 +534,7 @@ class GpuEngine:
         self.h2d_bytes += 4 * st.n
         stream = torch.cuda.current_stream()
         sp = stream.cuda_stream
+        self._ev[0].record(stream)  # device time includes the metadata kernels
         self._apply_metadata(*meta, sp)
         res = self.res_dev
         nd = self.fused_drafts
@@ -552,7 +555,6 @@ class GpuEngine:
         fa.logits_out = int(self.keep_logits)
         fa.next_window = self.cfg.spec_buffer if nd else 0
         fa.next_cap = self.nd_cap if nd else 0
-        self._ev[0].record(stream)
         check(lib().ds_model_forward(self._model_ref, self._kv_ref, self._fargs_ref, sp),
               "ds_model_forward")
         self.gpu_launches += self.launches_per_forward([r])
@@ -645,6 +647,7 @@ class GpuEngine:
         self.h2d_bytes += 4 * st.n
         stream = torch.cuda.current_stream()
         sp = stream.cuda_stream
+        self._ev[0].record(stream)
         self._apply_metadata(*meta, sp)
         k1 = self.k1_dev
         need = 3 * n + n * max_draft
@@ -658,13 +661,59 @@ class GpuEngine:
                                             st.dptr(o_cap), max_draft, e_p, l_p, d_p, dl_p, sp),
               "ds_longest_suffix_match")
         self.gpu_launches += 1
+        self._ev[1].record(stream)
         self.k1_host[:need].copy_(k1[:need], non_blocking=True)
         self.d2h_bytes += 4 * need
         stream.synchronize()
+        f = self._fwd["propose"]
+        f[0] += 1
+        f[1] += self._ev[0].elapsed_time(self._ev[1]) / 1000.0
         h = self.k1_host.numpy()
         dl = h[2 * n: 3 * n]
         d = h[3 * n: 3 * n + n * max_draft].reshape(n, max_draft)
         return [d[i, : dl[i]].tolist() for i in range(n)]
+
+    # -- prefix migration payload (dist.py) ------------------------------------------
+
+    def _cells_dev(self, cells) -> torch.Tensor:
+        return torch.as_tensor(np.asarray(cells, dtype=np.int32)).to(self.device,
+                                                                    non_blocking=False)
+
+    def pack_cells(self, cells) -> torch.Tensor:
+        """K/V rows of `cells` (all layers) as one [L][2][nkv][n][hd] bf16 buffer
+        (ds_kv_pack_cells); the message a prefix migration sends."""
+        s = self.shape
+        n = len(cells)
+        buf = torch.empty((s.layers, 2, s.n_kv_heads, n, s.head_dim), dtype=torch.bfloat16,
+                          device=self.device)
+        self.flush()  # pending row copies land before the rows are read
+        cd = self._cells_dev(cells)
+        stream = torch.cuda.current_stream().cuda_stream
+        check(lib().ds_kv_pack_cells(self.k_pool.data_ptr(), self.v_pool.data_ptr(), s.layers,
+                                     s.n_kv_heads, self.head_stride, s.head_dim, cd.data_ptr(), n,
+                                     buf.data_ptr(), 0, stream), "ds_kv_pack_cells")
+        self.gpu_launches += 1
+        return buf
+
+    def unpack_cells(self, cells, buf: torch.Tensor) -> None:
+        """Scatter a received [L][2][nkv][n][hd] buffer into `cells`."""
+        s = self.shape
+        n = len(cells)
+        if tuple(buf.shape) != (s.layers, 2, s.n_kv_heads, n, s.head_dim) or \
+                buf.dtype != torch.bfloat16 or not buf.is_contiguous():
+            raise ValueError(f"migration payload shape {tuple(buf.shape)} does not match "
+                             f"{n} cells")
+        cd = self._cells_dev(cells)
+        stream = torch.cuda.current_stream().cuda_stream
+        check(lib().ds_kv_pack_cells(self.k_pool.data_ptr(), self.v_pool.data_ptr(), s.layers,
+                                     s.n_kv_heads, self.head_stride, s.head_dim, cd.data_ptr(), n,
+                                     buf.data_ptr(), 1, stream), "ds_kv_pack_cells")
+        self.gpu_launches += 1
+
+    def payload_buffer(self, n: int) -> torch.Tensor:
+        s = self.shape
+        return torch.empty((s.layers, 2, s.n_kv_heads, n, s.head_dim), dtype=torch.bfloat16,
+                           device=self.device)
 
     # -- diagnostics -------------------------------------------------------------------
 

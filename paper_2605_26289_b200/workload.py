@@ -38,6 +38,7 @@ class TraceRequest:
     tools: frozenset
     expect: dict
     session: str | None = None  # session id (session path) or None (transient + radix)
+    fail_after: int | None = None  # injected fault after this many tokens (acceptance c11)
 
 
 def load_trace(name: str) -> dict:
@@ -52,7 +53,8 @@ def load_trace(name: str) -> dict:
         pieces = pp[: r["common"]] + r["pieces"]
         last[r["stream"]] = (toks, pieces)
         reqs.append(TraceRequest(r["id"], r["wave"], r["stream"], toks, pieces, r["max_tokens"],
-                                 frozenset(r["tools"]), r.get("expect", {}), r.get("session")))
+                                 frozenset(r["tools"]), r.get("expect", {}), r.get("session"),
+                                 r.get("fail_after")))
     tr["reqs"] = reqs
     return tr
 
@@ -69,6 +71,7 @@ class TurnRecord:
     req: TraceRequest
     result: object
     latency_ms: float
+    handle_error: Exception | None = None
 
 
 def replay(core, trace: dict, wave_limit: int | None = None, max_iters: int = 200_000,
@@ -91,7 +94,8 @@ def replay(core, trace: dict, wave_limit: int | None = None, max_iters: int = 20
             req = GenerationRequest(request_id=r.id + rid_suffix, prompt_tokens=list(r.tokens),
                                     prompt_pieces=list(r.pieces), max_tokens=r.max_tokens,
                                     temperature=0.0, seed=prompt_seed(r.tokens),
-                                    declared_tools=r.tools, guard=guard, session=session)
+                                    declared_tools=r.tools, guard=guard, session=session,
+                                    fail_after_tokens=r.fail_after)
             h = RequestHandle(req)
             core.submit(h)
             handles.append((r, h))
@@ -111,9 +115,11 @@ def replay(core, trace: dict, wave_limit: int | None = None, max_iters: int = 20
             if it > max_iters:
                 raise RuntimeError("wave did not complete")
         for r, h in handles:
-            if h.error is not None:
+            if h.error is not None and not (r.fail_after is not None
+                                            and type(h.error).__name__ == "InjectedFault"):
                 raise h.error
-            records.append(TurnRecord(r, h.result, (h.completed_at - h.submitted_at) * 1000.0))
+            records.append(TurnRecord(r, h.result, (h.completed_at - h.submitted_at) * 1000.0,
+                                      h.error))
     if wave_limit is None:
         for sid in sorted(sessions):
             core.close_session(sessions[sid])
@@ -125,6 +131,11 @@ def mismatches(records: list[TurnRecord]) -> list[str]:
     bad = []
     for rec in records:
         exp = rec.req.expect
+        if "failed" in exp or rec.result is None:
+            err = rec.handle_error
+            if "failed" not in exp or err is None or type(err).__name__ != exp["failed"]:
+                bad.append(f"{rec.req.id}: failed {err!r}, expected {exp.get('failed')}")
+            continue
         for f in RESULT_FIELDS:
             got = getattr(rec.result, f)
             if f in exp and got != exp[f]:

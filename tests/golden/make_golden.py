@@ -458,6 +458,65 @@ def trace_waves(name, cfg_over, scenarios):
             "requests": rec.finish_records(), "snapshots": snaps}
 
 
+def trace_failures(name, cfg_over, total=1000, seed=3, vocab_cap=30000):
+    """Acceptance c11 (tests/test_acceptance.py:314-341): 1000 requests in waves
+    of 10, ~10% with an injected fault after 1-3 tokens (InjectedFault ->
+    _fail_slot, scheduler.py:630-634, 853-867).  Same rng call sequence as the
+    reference test; prompt ids are folded into the vocabulary
+    (`% vocab_cap`) so a real embedding table can serve them.  Every request's
+    outcome (result fields, or failed) plus the pool / KV / radix state after
+    each wave are recorded."""
+    core = InferenceCore(ServerConfig(**cfg_over))
+    rng = random.Random(seed)
+    reqs, snaps, done, failures = [], [], 0, 0
+    wave_no = 0
+    while done < total:
+        wave = []
+        for _ in range(min(10, total - done)):
+            inject = rng.random() < 0.10
+            fail_after = rng.randint(1, 3) if inject else None
+            failures += bool(inject)
+            base = (rng.randint(1, 1_000_000) * 30) % vocab_cap
+            toks = [(base + i) % vocab_cap for i in range(rng.randint(4, 24))]
+            rid = f"s{done + len(wave)}"
+            max_tokens = rng.randint(1, 6)
+            guard = core.pool.acquire("transient", timeout=1.0)
+            req = GenerationRequest(request_id=rid, prompt_tokens=list(toks),
+                                    prompt_pieces=[f" w{t}" for t in toks], max_tokens=max_tokens,
+                                    temperature=0.0, seed=prompt_seed(toks), guard=guard,
+                                    fail_after_tokens=fail_after)
+            h = RequestHandle(req)
+            core.submit(h)
+            wave.append(h)
+            reqs.append((h, {"id": rid, "wave": wave_no, "stream": rid, "common": 0,
+                             "tokens": toks, "pieces": [f" w{t}" for t in toks],
+                             "max_tokens": max_tokens, "tools": [], "fail_after": fail_after}))
+        pending = list(wave)
+        while pending:
+            core.step()
+            pending = [h for h in pending if not h.wait(timeout=0)]
+        done += len(wave)
+        wave_no += 1
+        snap = core_snapshot(core)
+        snap["pool"] = core.pool.free_counts()
+        snaps.append(snap)
+    assert failures > total // 20  # the ~10% injection actually happened
+    for snap in snaps[:-1]:  # the full radix dump only at the end (fixture size)
+        snap.pop("radix_dump")
+    assert core.pool.free_counts() == {"transient": 12, "session": 4}
+    assert core.kv.occupancy == core.radix.total_cells
+    out = []
+    for h, rec in reqs:
+        if h.error is not None:
+            rec["expect"] = {"failed": type(h.error).__name__}
+        else:
+            rec["expect"] = {f: getattr(h.result, f) for f in RESULT_FIELDS}
+            rec["expect"]["finalize"] = h.result.finalize.kind
+        out.append(rec)
+    return {"name": name, "config": cfg_over, "mode": "waves", "requests": out,
+            "snapshots": snaps, "failures": failures}
+
+
 def deep_c4(salt, turns, pieces=820):
     sc = deep_workflow(salt, turns)
     sc.tool_results = [turn_tool_result(salt, t, pieces=pieces) for t in range(turns)]
@@ -490,6 +549,9 @@ def gen_traces():
                     [agentic_6turn(f"c5s{i}") for i in range(8)]),
         trace_waves("c5", {"pool_transient": 256, "capacity_cells": 1 << 19},
                     [agentic_6turn(f"c5s{i}") for i in range(256)]),
+        trace_failures("c11", {}),
+        # the same under KV pressure: evictions and deferrals between faults
+        trace_failures("c11_tight", {"capacity_cells": 256}, total=400, seed=11),
     ]
     only = [a for a in sys.argv[2:]] if len(sys.argv) > 2 and sys.argv[1] == "traces" else None
     for tr in traces:
@@ -497,7 +559,7 @@ def gen_traces():
             continue
         n = len(tr["requests"])
         last = tr["requests"][-1]
-        print(f"{tr['name']}: {n} requests, last n_t={last['expect']['n_t']}")
+        print(f"{tr['name']}: {n} requests, last n_t={last['expect'].get('n_t')}")
         dump(f"traces/{tr['name']}.json.gz", tr, gz=True)
 
 

@@ -1,13 +1,14 @@
 """Multi-GPU host logic on CPU (gloo, world_size 2): session routing, the prefix
-directory, and prefix migration between two cores - the migrated prefix must
-produce the same radix hit the reference core produces locally (C3: the
-second agent restores the 224-token shared tool-schema prefix)."""
+directory, and ADMISSION-TIME prefix migration between two cores.  Rank 1's
+admission of agent B's first C3 turn finds rank 0's announced tool-schema
+prefix, migrates the cells past its own (empty) match and must reproduce the
+radix hit the reference core produces locally (224 cached tokens) and the
+reference result fields."""
 from __future__ import annotations
 
 import os
 import socket
 
-import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -27,28 +28,63 @@ def test_route_is_reference_fnv32():
     assert min(counts) > 60  # roughly balanced
 
 
-def test_pack_unpack_roundtrip():
-    k = torch.randn(L, NKV, 64, HD)
-    v = torch.randn(L, NKV, 64, HD)
-    cells = [3, 9, 10, 40]
-    buf = D.pack_cells(k, v, cells)
-    assert buf.shape == (L, 2, NKV, 4, HD)
-    k2, v2 = torch.zeros_like(k), torch.zeros_like(v)
-    D.unpack_cells(k2, v2, [0, 1, 2, 3], buf)
-    assert torch.equal(k2[:, :, :4], k[:, :, cells]) and torch.equal(v2[:, :, :4], v[:, :, cells])
+def test_directory_best_remote():
+    d = D.PrefixDirectory()
+    toks = list(range(100, 400))
+    d.publish(1, toks[:50] + [7, 7, 7])
+    d.publish(1, toks[:120])
+    d.publish(0, toks[:200] + [1, 2])
+    d.publish(2, toks[:60] + [9] * 300)  # partial overlap: 60 tokens in common
+    assert d.best_remote(toks, rank=0, limit=299) == (1, 120)  # own prefixes skipped
+    assert d.best_remote(toks, rank=2, limit=299) == (0, 200)
+    assert d.best_remote(toks, rank=2, limit=150) == (0, 150)
+    assert d.best_remote([1] + toks[1:], rank=2, limit=299) == (-1, 0)
+    t = D.TokenTrie()
+    for seq in ([1, 2, 3, 4], [1, 2, 5], [1, 2, 3, 9, 9], [6]):
+        t.insert(seq)
+    assert [t.longest(x) for x in ([1, 2, 3, 4, 5], [1, 2, 5, 5], [1, 2, 3, 9], [6, 1], [2])] \
+        == [4, 3, 4, 1, 0]
 
 
-def _make_core():
+def _make_core(cap=CAP):
     from oracle_engine import OracleEngine
     from paper_2605_26289_b200.scheduler import InferenceCore
     from paper_2605_26289_b200.workload import core_config_for, load_trace
 
+    class PoolEngine(OracleEngine):
+        """Test engine with a CPU K/V pool (the GPU engine packs / scatters
+        with ds_kv_pack_cells)."""
+
+        def __init__(self, *a):
+            super().__init__(*a)
+            self.k_pool = torch.zeros(L, NKV, cap, HD)
+            self.v_pool = torch.zeros(L, NKV, cap, HD)
+
+        def pack_cells(self, cells):
+            idx = torch.as_tensor(list(cells), dtype=torch.long)
+            return torch.stack([self.k_pool[:, :, idx], self.v_pool[:, :, idx]], 1).contiguous()
+
+        def payload_buffer(self, n):
+            return torch.empty(L, 2, NKV, n, HD)
+
+        def unpack_cells(self, cells, buf):
+            idx = torch.as_tensor(list(cells), dtype=torch.long)
+            self.k_pool[:, :, idx] = buf[:, 0]
+            self.v_pool[:, :, idx] = buf[:, 1]
+
     tr = load_trace("c3")
-    cfg = core_config_for(tr, model="tiny", capacity_cells=CAP)
-    eng = OracleEngine(cfg.vocab, cfg.copy_min_match)
-    eng.k_pool = torch.zeros(L, NKV, CAP, HD)
-    eng.v_pool = torch.zeros(L, NKV, CAP, HD)
-    return InferenceCore(cfg, engine=eng), tr
+    cfg = core_config_for(tr, model="tiny", capacity_cells=cap)
+    return InferenceCore(cfg, engine=PoolEngine(cfg.vocab, cfg.copy_min_match)), tr
+
+
+def _wait_announced(mig, n=1):
+    import time
+
+    t0 = time.monotonic()
+    while len(mig.directory.tries) < n:
+        mig.poll()
+        assert time.monotonic() - t0 < 60
+        time.sleep(0.001)
 
 
 def _worker(rank, port, q):
@@ -56,43 +92,67 @@ def _worker(rank, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=2)
     try:
-        from paper_2605_26289_b200.workload import replay, waves
+        from paper_2605_26289_b200.workload import mismatches, replay, waves
 
         core, tr = _make_core()
+        mig = D.PrefixMigrator(core)
+        closer = mig
         w = waves(tr)
         first_a, first_b = w[0][0], w[1][0]  # agent A turn 0, agent B turn 0
-        shared = 224  # reference C3: B's first turn restores 224 cached tokens
-        prefix = first_b.tokens[:shared]
+        eng = core.engine
         if rank == 0:
-            replay(core, {"reqs": [first_a]})  # A's turn commits the schema prefix
-            cells = D.export_prefix(core, prefix)
-            assert len(cells) == shared
-            eng = core.engine
             for c in range(CAP):  # deterministic per-cell payload
                 eng.k_pool[:, :, c, :] = c
                 eng.v_pool[:, :, c, :] = -c
+            replay(core, {"reqs": [first_a]})  # A's turn commits + announces its prefix
+            cells = [c for s, n in core.radix.longest_prefix(first_b.tokens).runs
+                     for c in range(s, s + n)]
             dist.send_object_list([cells], dst=1)
+            mig.close()  # serves rank 1's request until rank 1 says goodbye
+            q.put(("served", mig.stats["served"], mig.stats["cells_out"]))
         else:
             src_cells = [None]
             dist.recv_object_list(src_cells, src=0)
-        directory = D.PrefixDirectory()
-        if rank == 0:
-            directory.publish_local(0, [(cpu.fnv1a64_tokens(prefix), shared)])
-        directory.sync()
-        owner = directory.owner(cpu.fnv1a64_tokens(prefix))
-        assert owner is not None and owner.rank == 0 and owner.length == shared
-        nbytes = D.migrate_prefix(core, core, prefix, 0, 1)
-        assert nbytes == L * 2 * NKV * shared * HD * 4
-        if rank == 1:
-            got = D.export_prefix(core, prefix)
-            assert len(got) == shared
-            eng = core.engine
-            exp = torch.tensor(src_cells[0], dtype=torch.float32)
+            _wait_announced(mig)
+            recs = replay(core, {"reqs": [first_b]})  # admission migrates, then aliases
+            assert mismatches(recs) == []
+            got = [c for s, n in core.radix.longest_prefix(first_b.tokens).runs
+                   for c in range(s, s + n)][:224]
+            exp = torch.tensor(src_cells[0][:224], dtype=torch.float32)
             assert torch.equal(eng.k_pool[0, 0, got, 0], exp)
             assert torch.equal(eng.v_pool[1, 1, got, 3], -exp)
-            recs = replay(core, {"reqs": [first_b]})
+            stats = dict(mig.stats)
             q.put(("hit", recs[0].result.cached_prompt_tokens,
-                   first_b.expect["cached_prompt_tokens"]))
+                   first_b.expect["cached_prompt_tokens"], stats["fetches"],
+                   core.metrics.counters().get("migrated_prefixes", 0)))
+    finally:
+        closer.close(timeout_s=60)  # goodbye even on failure: the peer stops waiting
+        dist.destroy_process_group()
+
+
+def _cross_worker(rank, port, q):
+    """Both ranks ask each other for a prefix at the same time: each waits for
+    its reply while serving the peer's request (no deadlock)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        from paper_2605_26289_b200.workload import load_trace, replay, waves
+
+        core, tr = _make_core()
+        mig = D.PrefixMigrator(core)
+        c2 = load_trace("c2")["reqs"]
+        c3 = waves(tr)
+        # rank 0 holds the C2 conversation's first turn, rank 1 C3 agent A's;
+        # then each admits a turn (C3 agent A turn 1, C2 turn 1) whose prefix only
+        # the OTHER rank holds
+        mine, theirs = (c2[0], c3[3][0]) if rank == 0 else (c3[0][0], c2[1])
+        replay(core, {"reqs": [mine]})  # commit + announce
+        _wait_announced(mig, 1)
+        recs = replay(core, {"reqs": [theirs]})  # both fetch at once, serving each other
+        mig.close()  # keeps serving until the peer is done too
+        q.put((rank, recs[0].result.cached_prompt_tokens, theirs.expect["cached_prompt_tokens"],
+               mig.stats["fetches"], mig.stats["served"]))
     finally:
         dist.destroy_process_group()
 
@@ -105,15 +165,32 @@ def _free_port():
     return port
 
 
-def test_prefix_migration_two_ranks():
+def _run(target):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=target, args=(r, port, q)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
-        p.join(timeout=240)
+        p.join(timeout=180)
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
-    tag, got, expected = q.get()
-    assert tag == "hit" and got == expected == 224
+    return [q.get() for _ in range(2)]
+
+
+def test_admission_triggers_prefix_migration():
+    out = dict((r[0], r[1:]) for r in _run(_worker))
+    got, expected, fetches, migrated = out["hit"]
+    assert got == expected == 224
+    assert fetches == 1 and migrated == 1
+    served, cells_out = out["served"]
+    assert served == 1 and cells_out >= 224
+
+
+def test_concurrent_requests_do_not_deadlock():
+    out = sorted(_run(_cross_worker))
+    for rank, cached, expected, fetches, served in out:
+        # >= 1: a rank may also fetch the 220 tokens C2 and C3 share for its own
+        # first request, depending on when the peer's announcement lands
+        assert fetches >= 1 and served >= 1
+        assert cached == expected > 200  # the reference's local radix hit, migrated

@@ -29,7 +29,15 @@ def _device_invariants(core):
                                           ("c3", False), ("c4_small", False), ("c5_small", False),
                                           ("c2", True), ("c3", True), ("c5_small", True),
                                           ("sessions", False), ("sessions_radix", False),
-                                          ("sessions", True)])
+                                          ("sessions", True),
+                                          # full BASELINE C4 (32,370-token prefix: split-KV
+                                          # through the whole path) and C5 (256 sessions,
+                                          # radix evictions on the device page tables)
+                                          ("c4", False), ("c4", True), ("c5", False),
+                                          ("c5", True),
+                                          # acceptance c11: injected faults -> _fail_slot
+                                          ("c11", False), ("c11", True),
+                                          ("c11_tight", False), ("c11_tight", True)])
 def test_trace_parity_gpu(cuda, name, batched):
     tr = load_trace(name)
     core = InferenceCore(core_config_for(tr, model="tiny", batched_forward=batched))
@@ -38,7 +46,34 @@ def test_trace_parity_gpu(cuda, name, batched):
     final = tr["snapshots"][-1]
     assert core.engine.ledger.snapshot() == final["ledger"]
     assert core.radix.dump() == final["radix_dump"]
+    if name == "c5":  # the device page tables went through radix evictions
+        assert core.radix.evicted_cells_total > 0
+    if "pool" in final:  # c11: zero leaked sequence ids or cells after the faults
+        assert core.pool.free_counts() == final["pool"]
+        assert core.kv.occupancy == core.radix.total_cells == final["radix_cells"]
+        assert not core._slots and not core._pending
+        assert sum(1 for r in recs if r.handle_error is not None) > 20
     _device_invariants(core)
+
+
+def test_batched_capacity_precheck_gpu(cuda):
+    """KV pressure (session-held cells): batched plans fall back to the
+    reference's check-then-forward order; results equal the sequential run
+    and the device page tables / refcounts equal the host allocator's."""
+    from test_host_scheduler import _pressure_run
+
+    from paper_2605_26289_b200.engine import GpuEngine
+
+    def gpu(cfg):
+        return None  # InferenceCore builds its GpuEngine
+
+    seq_out, seq_snap, _, c0 = _pressure_run(False, engine_factory=gpu)
+    _device_invariants(c0)
+    bat_out, bat_snap, tight, c1 = _pressure_run(True, engine_factory=gpu)
+    _device_invariants(c1)
+    assert tight > 0 and seq_snap[3] > 0
+    assert bat_out == seq_out and bat_snap == seq_snap
+    assert isinstance(c1.engine, GpuEngine)
 
 
 @pytest.mark.parametrize("name", ["c2", "c4_small"])

@@ -12,7 +12,7 @@ from paper_2605_26289_b200.scheduler import InferenceCore, SchedulerConfig, chun
 from paper_2605_26289_b200.workload import core_config_for, load_trace, mismatches, replay
 
 TRACES = ["c1", "c2", "c2_nospec", "c3", "c3_nogroup", "c4_small", "c5_small", "sessions",
-          "sessions_radix"]
+          "sessions_radix", "c4", "c5", "c11", "c11_tight"]
 
 
 @pytest.mark.parametrize("batched", [False, True])
@@ -29,6 +29,11 @@ def test_trace_parity_host(name, batched):
     assert core.radix.total_cells == final["radix_cells"]
     assert core.radix.dump() == final["radix_dump"]
     assert core.iterations == final["iterations"]
+    if "pool" in final:  # acceptance c11: zero leaked ids / cells after injected faults
+        assert core.pool.free_counts() == final["pool"]
+        assert core.kv.occupancy == core.radix.total_cells
+        assert not core._slots and not core._pending
+        assert sum(1 for r in recs if r.handle_error is not None) > 20
 
 
 CFG = SchedulerConfig()
@@ -57,3 +62,75 @@ def test_temperature_rejected():
     h = RequestHandle(GenerationRequest("t", [1, 2, 3], [" a"] * 3, 4, 0.7, 0, guard=g))
     with pytest.raises(ValueError):
         core.submit(h)
+
+
+def _pressure_run(batched: bool, engine_factory=None):
+    """Session KV (held between turns, outside the admission charge) squeezes
+    the free pool so decode/verify entries must evict radix leaves or defer."""
+    from paper_2605_26289_b200 import scheduler as S
+    from paper_2605_26289_b200.config import CoreConfig
+    from paper_2605_26289_b200.kernels import prompt_seed
+    from paper_2605_26289_b200.scheduler import GenerationRequest, RequestHandle
+    import random
+
+    cfg = CoreConfig(model="tiny", capacity_cells=256, spec_max_lookahead=4, pool_transient=12,
+                     batched_forward=batched)
+    core = InferenceCore(cfg, engine=(engine_factory or (
+        lambda c: OracleEngine(c.vocab, c.copy_min_match)))(cfg))
+    tight = {"n": 0}
+    orig = S.InferenceCore._run_decode_entry
+
+    def counting(self, entry, events):
+        tight["n"] += 1
+        return orig(self, entry, events)
+
+    S.InferenceCore._run_decode_entry = counting
+    rng = random.Random(5)
+    sessions = [core.open_session(f"s{i}") for i in range(2)]
+    out = []
+    try:
+        for rnd in range(12):
+            hs = []
+            for i, sess in enumerate(sessions):  # sessions grow by ~20 tokens a turn
+                toks = list(sess.tokens) + [rng.randrange(50) for _ in range(20)]
+                req = GenerationRequest(f"s{i}-{rnd}", toks, [f" w{t}" for t in toks], 6, 0.0,
+                                        prompt_seed(toks), session=sess)
+                hs.append(RequestHandle(req))
+            for w in range(6):  # repetitive transient prompts: copy policy + long drafts
+                base = [rng.randrange(6) for _ in range(6)]
+                toks = (base * 5)[: 12 + rng.randrange(12)]
+                req = GenerationRequest(f"t{rnd}-{w}", toks, [f" w{t}" for t in toks], 10, 0.0,
+                                        prompt_seed(toks), guard=core.pool.acquire("transient"))
+                hs.append(RequestHandle(req))
+            for h in hs:
+                core.submit(h)
+            for _ in range(10_000):
+                if all(h.wait(timeout=0) for h in hs):
+                    break
+                core.step()
+            for h in hs:
+                assert h.error is None, h.error
+                r = h.result
+                out.append((r.request_id, r.generated, r.decode_passes, r.spec_accepted,
+                            r.cached_prompt_tokens))
+            for i, sess in enumerate(sessions):
+                if rnd % 3 == 2:  # reset the sessions now and then
+                    core.close_session(sess)
+                    sessions[i] = core.open_session(f"s{i}")
+    finally:
+        S.InferenceCore._run_decode_entry = orig
+    snap = (core.engine.ledger.snapshot(), core.radix.dump(), core.kv.occupancy,
+            core.radix.evicted_cells_total)
+    return out, snap, tight["n"], core
+
+
+def test_batched_capacity_precheck_matches_sequential():
+    """Batched plans check capacity BEFORE the forward (scheduler.py:740/761
+    order); under KV pressure they fall back to entry-by-entry execution and
+    must produce exactly the sequential (reference-order) results."""
+    seq_out, seq_snap, _, _ = _pressure_run(False)
+    bat_out, bat_snap, tight, _ = _pressure_run(True)
+    assert tight > 0  # the pre-check fired
+    assert seq_snap[3] > 0  # radix evictions happened
+    assert bat_out == seq_out
+    assert bat_snap == seq_snap

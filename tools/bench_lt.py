@@ -3,10 +3,18 @@ projections at prefill / batched row counts (ds_debug_lt_sweep; 4 rotating
 weight copies > L2).  Usage: bench_lt.py [T ...]"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import subprocess
 import torch
-from paper_2605_26289_b200._lib import lib
 
-L = lib()
+# measurement-only: tools/gemm_lt.cu is built into its own library here (it is
+# not part of the product libdeltaserve_b200.so)
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "libgemm_lt.so")
+subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a",
+                       "-O2", "-shared", "-Xcompiler", "-fPIC",
+                       "-I" + os.path.join(os.path.dirname(HERE), "include"),
+                       os.path.join(HERE, "gemm_lt.cu"), "-o", SO, "-lcublasLt", "-lcublas"])
+L = ctypes.CDLL(SO)
 f = L.ds_debug_lt_sweep
 P = ctypes.c_void_p
 f.argtypes = [P, P, ctypes.c_int, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
