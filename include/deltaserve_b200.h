@@ -320,6 +320,16 @@ int ds_gemm_skinny_ex(const void* X, const void* W, void* Y, int M, int N, int K
 int ds_gemm_tc(const void* X, const void* W, void* Y, int T, int N, int K, int y_f32,
                int accumulate, ds_stream_t stream);
 
+/* K10: persistent stream-K projection GEMM on tcgen05/TMEM for prefill chunks
+ * and batched plans (any T): Y[T][N] (+)= X[T][K] . W[N][K]^T with the
+ * ds_skinny_epi fusions (norm consumer, residual producer + row sums,
+ * SwiGLU, RoPE + KV store, LM-head argmax), row-indexed buffers sized for T
+ * rows.  N % 128 == 0, K % 64 == 0.  Deterministic (fixed-order split
+ * reduction).  Replaces the serial per-entry engine.forward of the reference
+ * (scheduler.py:652-660) inside one varlen pass. */
+int ds_gemm_stream(const void* X, const void* W, void* Y, int T, int N, int K, int y_f32,
+                   int accumulate, const ds_skinny_epi* epi, ds_stream_t stream);
+
 /* K8: row argmax over fp32 logits (lowest index on ties, engine.py:146-159). */
 int ds_argmax(const float* logits, int n_rows, int vocab, int32_t* out, ds_stream_t stream);
 

@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(
         tma_load_3d(sp + a_bytes, &tx, 0, t0, (s_beg + i) * ks, &full[st]);
       }
     }
+    __syncwarp();  // reconverge before the CTA barrier (bar.sync is warp-aligned)
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_bf16(kBM, NT, false);
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(
       }
       tc::commit(acc_full);
     }
+    __syncwarp();
   } else {
     // epilogue warps 2-5: TMEM lane quadrant (warp & 3), thread = weight row
     pdl_wait();  // the residual (accumulate) comes from the previous kernel

@@ -35,6 +35,10 @@ namespace {
 
 constexpr size_t kAlign = 256;
 constexpr size_t kCublasWs = 32u << 20;
+// row bound of the fused norm / argmax scalars (two row-sum buffers + the
+// LM-head argmax keys), kept at row-count-independent offsets: both GEMM
+// paths (skinny M <= 32, stream-K above) share them and the clear/fill cycle
+constexpr int kMaxSsRows = 16384;
 
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
@@ -82,8 +86,8 @@ struct Carve {
 struct Buffers {
   float* x;  // fp32 residual stream
   __nv_bfloat16 *h, *qkv, *attn, *gu, *act, *hf;
-  uint64_t* ss;  // 2 x 32: fixed-point row sums of squares (skinny GEMM epilogues)
-  uint64_t* amax;  // 32: fused LM-head argmax keys (re-armed by the token policy)
+  uint64_t* ss;    // 2 x kMaxSsRows: fixed-point row sums of squares (GEMM epilogues)
+  uint64_t* amax;  // kMaxSsRows: fused LM-head argmax keys (re-armed by the token policy)
   uint64_t* row_hash;
   void* attn_ws;
   size_t attn_ws_bytes;
@@ -99,8 +103,8 @@ size_t layout(const ds_model* m, int rows, int outs, Buffers* b, uint8_t* base) 
   // first, at row-count-independent offsets: the ss buffers and the attention
   // split-merge counters are zero between calls (self re-arming), which must
   // hold whatever the previous call's batch size was
-  t.ss = c.take<uint64_t>(2 * DS_SKINNY_SS_WORDS * 8);
-  t.amax = c.take<uint64_t>(DS_SKINNY_SS_WORDS * 8);
+  t.ss = c.take<uint64_t>(2 * kMaxSsRows * 8);
+  t.amax = c.take<uint64_t>(kMaxSsRows * 8);
   t.attn_ws_bytes = attn_partial_bytes_bound();
   t.attn_ws = c.take<uint8_t>(t.attn_ws_bytes);
   t.x = c.take<float>(rows * H * 4);
@@ -134,15 +138,26 @@ extern "C" int ds_gemm_skinny_ex(const void* X, const void* W, void* Y, int M, i
 namespace ds {
 namespace {
 
+// DS_GEMM_STREAM=1: K10 (stream-K / cluster split-K tcgen05 GEMM with the
+// fused epilogues) for M > 32 rows.  Opt-in: it is correct, deterministic
+// and fuses RMSNorm / RoPE+KV store / SwiGLU / the LM-head argmax, but its
+// split-K reduction (partials through L2 or DSMEM) and 128 x NT single-CTA
+// tiles still lose to cuBLAS + the unfused kernels
+bool use_stream_gemm() {
+  static const bool v = getenv("DS_GEMM_STREAM") && atoi(getenv("DS_GEMM_STREAM")) == 1;
+  return v;
+}
+
 // decode / verify row counts stream the weights through our skinny GEMM;
-// prefill chunks (compute-bound) go to cuBLAS.
+// prefill chunks and batched plans through the stream-K tcgen05 GEMM (K10).
 int project(cublasHandle_t h, const void* X, const void* W, void* Y, int M, int N, int K,
             bool y_f32, bool accumulate, cudaStream_t s) {
   if (M <= 32 && N % 16 == 0 && K % 256 == 0)
     return ds_gemm_skinny(X, W, Y, M, N, K, y_f32, accumulate, s);
-  // DS_GEMM_TC=1: K9 (tcgen05) instead of the library GEMM.  Opt-in: K9 is
-  // correct and deterministic but still slower than cuBLAS on these shapes
-  // (its TMA ring is too shallow for the load latency)
+  if (use_stream_gemm() && N % 128 == 0 && K % 64 == 0)
+    return ds_gemm_stream(X, W, Y, M, N, K, y_f32, accumulate, nullptr, s);
+  // DS_GEMM_TC=1 (with DS_GEMM_STREAM=0): K9, the earlier data-parallel
+  // tcgen05 GEMM with cluster split-K - kept for A/B
   static const bool use_tc = getenv("DS_GEMM_TC") && atoi(getenv("DS_GEMM_TC")) == 1;
   if (use_tc && N % 128 == 0 && K % 64 == 0 && K >= 128)
     return ds_gemm_tc(X, W, Y, M, N, K, y_f32, accumulate, s);
@@ -390,12 +405,23 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
     const char* e = getenv("DS_L2_NEXT_MB");
     return static_cast<int64_t>(e ? atof(e) * 1048576.0 : 12.0 * 1048576.0);
   }();
-  const bool fused = T <= 32 && H % 256 == 0 && F % 256 == 0 && (nh * hd) % 256 == 0 &&
-                     QKV % 16 == 0 && hd == 128;
+  // the fused epilogues: skinny GEMM (T <= 32) or the stream-K tcgen05 GEMM
+  // (K10, larger T) - the same ds_skinny_epi fusions either way
+  const bool small = T <= 32;
+  const bool fused = hd == 128 && QKV % 16 == 0 &&
+                     (small ? (H % 256 == 0 && F % 256 == 0 && (nh * hd) % 256 == 0)
+                            : (use_stream_gemm() && T <= kMaxSsRows && QKV % 128 == 0 &&
+                               H % 128 == 0 && (2 * F) % 128 == 0 && (nh * hd) % 64 == 0 &&
+                               F % 64 == 0));
+  auto gemm_ex = [&](const void* X, const void* W, void* Y, int N, int K, int y_f32, int acc,
+                     const ds_skinny_epi* e) {
+    return small ? ds_gemm_skinny_ex(X, W, Y, T, N, K, y_f32, acc, e, stream)
+                 : ds_gemm_stream(X, W, Y, T, N, K, y_f32, acc, e, stream);
+  };
   // two ss buffers, each producer clearing the one its consumer already read
   // (wo clears ss_attn, read by this layer's wqkv; down clears ss_mlp)
-  uint64_t* ss_attn = b.ss;                       // down -> next wqkv
-  uint64_t* ss_mlp = b.ss + DS_SKINNY_SS_WORDS;  // wo -> gate_up
+  uint64_t* ss_attn = b.ss;               // down -> next wqkv
+  uint64_t* ss_mlp = b.ss + kMaxSsRows;  // wo -> gate_up
   for (int l = 0; l < L; ++l) {
     const __nv_bfloat16* wqkv_l = wqkv + static_cast<size_t>(l) * QKV * H;
     if (fused) {  // norm (row scale) + projection + RoPE + KV store in one launch
@@ -418,7 +444,7 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
       e.k_pool_l = kp + l * kv_layer;
       e.v_pool_l = vp + l * kv_layer;
       e.kv_head_stride = kv->capacity;
-      DS_CHECK(ds_gemm_skinny_ex(b.h, wqkv_l, b.qkv, T, QKV, H, 0, 0, &e, stream));
+      DS_CHECK(gemm_ex(b.h, wqkv_l, b.qkv, QKV, H, 0, 0, &e));
     } else {
       DS_CHECK(ds_rmsnorm(b.x, 1, nullptr, T, H, an + static_cast<size_t>(l) * H, m->rms_eps, b.h,
                           stream));
@@ -430,7 +456,7 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
     // the attention leaves HBM mostly idle (short contexts): K7's producer
     // warps pull wo's weights into L2 for the next projection meanwhile
     static const double wo_l2_frac = getenv("DS_WO_L2_FRAC") ? atof(getenv("DS_WO_L2_FRAC")) : 1.0;
-    if (fused && wo_l2_frac > 0)
+    if (fused && small && wo_l2_frac > 0)
       set_attn_l2_prefetch(wo + static_cast<size_t>(l) * H * nh * hd,
                            static_cast<int64_t>(wo_l2_frac * H * nh * hd * 2) & ~15ll);
     if (n_long > 0 && n_long < a->n_entries) {  // mixed plan: K6 for prefill chunks, K7 rest
@@ -458,14 +484,14 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
       eo.ss_zero = ss_attn;
       eo.h_out = b.h;
       eo.h_w = mn + static_cast<size_t>(l) * H;
-      DS_CHECK(ds_gemm_skinny_ex(b.attn, wo_l, b.x, T, H, nh * hd, 1, 1, &eo, stream));
+      DS_CHECK(gemm_ex(b.attn, wo_l, b.x, H, nh * hd, 1, 1, &eo));
       ds_skinny_epi eg{};
       eg.row_ss = ss_mlp;
       eg.eps = m->rms_eps;
       eg.swiglu = 1;
       eg.l2_next = wd_l;
       eg.l2_next_bytes = l2_next_bytes;
-      DS_CHECK(ds_gemm_skinny_ex(b.h, wgu_l, b.act, T, 2 * F, H, 0, 0, &eg, stream));
+      DS_CHECK(gemm_ex(b.h, wgu_l, b.act, 2 * F, H, 0, 0, &eg));
       ds_skinny_epi ed{};
       ed.ss_out = ss_attn;  // (last layer: unused, keeps the clear/fill cycle uniform)
       ed.ss_zero = ss_mlp;
@@ -476,7 +502,7 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
         ed.h_out = b.h;
         ed.h_w = an + static_cast<size_t>(l + 1) * H;
       }
-      DS_CHECK(ds_gemm_skinny_ex(b.act, wd_l, b.x, T, H, F, 1, 1, &ed, stream));
+      DS_CHECK(gemm_ex(b.act, wd_l, b.x, H, F, 1, 1, &ed));
     } else {
       DS_CHECK(project(rt.blas, b.attn, wo_l, b.x, T, H, nh * hd, true, true, stream));
       DS_CHECK(ds_rmsnorm(b.x, 1, nullptr, T, H, mn + static_cast<size_t>(l) * H, m->rms_eps,
@@ -492,12 +518,16 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
   // LM head: <= 32 sampled rows reduce to their argmax in the GEMM epilogue
   // (logits stored only on request); more rows go through the library GEMM
   // and the K8 row argmax
-  const bool fused_head = a->n_out <= 32;
+  const bool fused_head = a->n_out <= 32 ||
+                          (use_stream_gemm() && a->n_out <= kMaxSsRows && m->vocab % 128 == 0);
   if (fused_head) {
     ds_skinny_epi eh{};
     eh.argmax_out = b.amax;
-    DS_CHECK(ds_gemm_skinny_ex(b.hf, m->lm_head, a->logits_out ? a->logits : nullptr, a->n_out,
-                               m->vocab, H, 1, 0, &eh, stream));
+    void* lg = a->logits_out ? a->logits : nullptr;
+    if (a->n_out <= 32)
+      DS_CHECK(ds_gemm_skinny_ex(b.hf, m->lm_head, lg, a->n_out, m->vocab, H, 1, 0, &eh, stream));
+    else
+      DS_CHECK(ds_gemm_stream(b.hf, m->lm_head, lg, a->n_out, m->vocab, H, 1, 0, &eh, stream));
   } else {
     DS_CHECK(project(rt.blas, b.hf, m->lm_head, a->logits, a->n_out, m->vocab, H, true, false,
                      stream));

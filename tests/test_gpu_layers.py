@@ -206,6 +206,48 @@ def test_gemm_skinny_vs_fp32(cuda, M, N, K, y_f32, acc):
     assert err < (1e-3 if y_f32 else 1e-2 * ref.abs().max().item()), err
 
 
+def _gemm_ex(L, X, W, Y, M, N, K, y_f32, acc, epi, s):
+    """The forward's GEMM for M rows: skinny (M <= 32) or stream-K K10."""
+    f = L.ds_gemm_skinny_ex if M <= 32 else L.ds_gemm_stream
+    return f(X, W, Y, M, N, K, y_f32, acc, epi, s)
+
+
+# K10 (persistent stream-K tcgen05, the product GEMM for M > 32): every shape
+# the forward uses (8B qkv / wo / gate_up / down / LM head at prefill and
+# batched row counts, the tiny model), ragged token tiles, plain bf16 and the
+# fp32 residual accumulate; bit-identical on a repeat (fixed-order split-K).
+@pytest.mark.parametrize("T,N,K", [(150, 4096, 4096), (150, 6144, 4096), (150, 28672, 4096),
+                                   (150, 4096, 14336), (33, 1024, 1024), (415, 4096, 4096),
+                                   (881, 1536, 1024), (881, 6144, 4096), (200, 5632, 1024),
+                                   (100, 1024, 2816), (4096, 1024, 4096), (256, 4096, 4096),
+                                   (257, 4096, 4096), (64, 128256, 4096), (512, 4096, 14336),
+                                   (1300, 28672, 4096), (40, 128, 64)])
+@pytest.mark.parametrize("y_f32,acc", [(0, 0), (1, 1)])
+def test_gemm_stream_vs_fp32(cuda, T, N, K, y_f32, acc):
+    from paper_2605_26289_b200._lib import check, lib
+
+    g = torch.Generator(device=cuda).manual_seed(T + N + K)
+    X = torch.randn(T, K, device=cuda, generator=g).bfloat16()
+    W = (0.02 * torch.randn(N, K, device=cuda, generator=g)).bfloat16()
+    Y0 = torch.randn(T, N, device=cuda, generator=g)
+    Y = Y0.clone() if y_f32 else Y0.bfloat16()
+    s = torch.cuda.current_stream().cuda_stream
+    L = lib()
+    check(L.ds_gemm_stream(X.data_ptr(), W.data_ptr(), Y.data_ptr(), T, N, K, y_f32, acc, None, s))
+    torch.cuda.synchronize()
+    ref = X.float() @ W.float().T
+    if acc:
+        ref = ref + (Y0 if y_f32 else Y0.bfloat16().float())
+    err = (Y.float() - ref).abs().max().item()
+    assert err < (2e-3 if y_f32 else 1e-2 * ref.abs().max().item()), err
+    if y_f32:  # deterministic: partial tiles are added in fixed k order
+        Y2 = Y0.clone()
+        check(L.ds_gemm_stream(X.data_ptr(), W.data_ptr(), Y2.data_ptr(), T, N, K, 1, acc, None,
+                               s))
+        torch.cuda.synchronize()
+        assert torch.equal(Y, Y2)
+
+
 # K9 (tcgen05): prefill chunks and batched plans.  Shapes cover one token tile
 # (150 -> N=160), ragged multi-tile (415 -> 2 x 208, 881 -> 4 x 224, 4096), the
 # cluster split-K (wo/down/wqkv-like N with few row tiles) and the tiny model.
@@ -237,7 +279,7 @@ def test_gemm_tc_vs_fp32(cuda, T, N, K, y_f32, acc):
         assert torch.equal(Y, Y2)
 
 
-@pytest.mark.parametrize("M", [1, 5, 13, 20, 32])
+@pytest.mark.parametrize("M", [1, 5, 13, 20, 32, 33, 150, 300, 881])
 def test_gemm_skinny_epilogue_fusions(cuda, M):
     """ds_gemm_skinny_ex: residual producer (y += X.W^T, h = bf16(y*w_norm),
     per-CTA partial sums of y^2) feeding a norm consumer (row scale
@@ -257,26 +299,27 @@ def test_gemm_skinny_epilogue_fusions(cuda, M):
     Wgu = (0.02 * torch.randn(2 * F, H, device=cuda, generator=g)).bfloat16()
     x = x0.clone()
     h = torch.empty(M, H, device=cuda, dtype=torch.bfloat16)
-    ss = torch.zeros(32, device=cuda, dtype=torch.int64)
-    other = torch.full((32,), 7, device=cuda, dtype=torch.int64)
+    R = max(32, M)
+    ss = torch.zeros(R, device=cuda, dtype=torch.int64)
+    other = torch.full((R,), 7, device=cuda, dtype=torch.int64)
     prod = SkinnyEpi(ss_out=ss.data_ptr(), ss_zero=other.data_ptr(), h_out=h.data_ptr(),
                      h_w=nw.data_ptr())
-    check(L.ds_gemm_skinny_ex(Xin.data_ptr(), Wo.data_ptr(), x.data_ptr(), M, H, Kin, 1, 1,
-                              ctypes.byref(prod), s))
+    check(_gemm_ex(L, Xin.data_ptr(), Wo.data_ptr(), x.data_ptr(), M, H, Kin, 1, 1,
+                   ctypes.byref(prod), s))
     act = torch.empty(M, F, device=cuda, dtype=torch.bfloat16)
     cons = SkinnyEpi(row_ss=ss.data_ptr(), eps=1e-5, swiglu=1)
-    check(L.ds_gemm_skinny_ex(h.data_ptr(), Wgu.data_ptr(), act.data_ptr(), M, 2 * F, H, 0, 0,
-                              ctypes.byref(cons), s))
+    check(_gemm_ex(L, h.data_ptr(), Wgu.data_ptr(), act.data_ptr(), M, 2 * F, H, 0, 0,
+                   ctypes.byref(cons), s))
     q = torch.empty(M, 512, device=cuda, dtype=torch.bfloat16)
     cons2 = SkinnyEpi(row_ss=ss.data_ptr(), eps=1e-5)
-    check(L.ds_gemm_skinny_ex(h.data_ptr(), Wgu[:512].contiguous().data_ptr(), q.data_ptr(), M,
-                              512, H, 0, 0, ctypes.byref(cons2), s))
+    check(_gemm_ex(L, h.data_ptr(), Wgu[:512].contiguous().data_ptr(), q.data_ptr(), M,
+                   512, H, 0, 0, ctypes.byref(cons2), s))
     torch.cuda.synchronize()
     x_ref = x0 + Xin.float() @ Wo.float().T
     assert (x - x_ref).abs().max().item() < 1e-3
     assert torch.allclose(h.float(), _bf(x * nw.float()).float(), atol=0, rtol=0)
     assert torch.allclose(ss[:M].double() / 2**24, (x * x).sum(-1).double(), rtol=1e-5)
-    assert other.eq(0).all()
+    assert other[:M].eq(0).all()
     hn = _bf(x_ref * torch.rsqrt((x_ref * x_ref).mean(-1, keepdim=True) + 1e-5) * nw.float())
     gu = _bf(hn.float() @ Wgu.float().T).float()
     gt, up = split_gate_up(gu, F)
@@ -288,7 +331,7 @@ def test_gemm_skinny_epilogue_fusions(cuda, M):
     assert err < 2e-2 * q_ref.abs().max().item(), err
 
 
-@pytest.mark.parametrize("M", [1, 5, 6, 17, 32])
+@pytest.mark.parametrize("M", [1, 5, 6, 17, 32, 33, 100, 300])
 def test_gemm_skinny_argmax_epilogue(cuda, M):
     """Fused LM-head argmax (ds_skinny_epi.argmax_out): the
     packed per-row key decodes to np.argmax of the same kernel's fp32 product
@@ -304,14 +347,15 @@ def test_gemm_skinny_argmax_epilogue(cuda, M):
     W = (0.02 * torch.randn(V, H, device=cuda, generator=g)).bfloat16()
     W[77000] = W[90000] = W[5] = (0.5 * X[0].float() / X[0].float().norm()).bfloat16()
     Y = torch.empty(M, V, device=cuda)
-    keys = torch.zeros(32, device=cuda, dtype=torch.int64)
+    R = max(32, M)
+    keys = torch.zeros(R, device=cuda, dtype=torch.int64)
     epi = SkinnyEpi(argmax_out=keys.data_ptr())
-    check(L.ds_gemm_skinny_ex(X.data_ptr(), W.data_ptr(), Y.data_ptr(), M, V, H, 1, 0,
-                              ctypes.byref(epi), s))
-    keys2 = torch.zeros(32, device=cuda, dtype=torch.int64)
+    check(_gemm_ex(L, X.data_ptr(), W.data_ptr(), Y.data_ptr(), M, V, H, 1, 0,
+                   ctypes.byref(epi), s))
+    keys2 = torch.zeros(R, device=cuda, dtype=torch.int64)
     epi2 = SkinnyEpi(argmax_out=keys2.data_ptr())
-    check(L.ds_gemm_skinny_ex(X.data_ptr(), W.data_ptr(), None, M, V, H, 1, 0,
-                              ctypes.byref(epi2), s))
+    check(_gemm_ex(L, X.data_ptr(), W.data_ptr(), None, M, V, H, 1, 0,
+                   ctypes.byref(epi2), s))
     torch.cuda.synchronize()
     idx = (0xFFFFFFFF - (keys[:M] & 0xFFFFFFFF)).cpu()
     assert torch.equal(idx, Y.argmax(-1).cpu())  # torch: first maximal index
@@ -322,7 +366,7 @@ def test_gemm_skinny_argmax_epilogue(cuda, M):
     assert (Y - ref).abs().max().item() < 1e-2
 
 
-@pytest.mark.parametrize("M", [1, 5, 17, 32])
+@pytest.mark.parametrize("M", [1, 5, 17, 32, 48, 150, 300])
 @pytest.mark.parametrize("norm", [False, True])
 def test_gemm_skinny_rope_kv_epilogue(cuda, M, norm):
     """ds_gemm_skinny_ex rope mode (wqkv projection + RoPE + KV store, the
@@ -338,30 +382,31 @@ def test_gemm_skinny_rope_kv_epilogue(cuda, M, norm):
     W = (0.05 * torch.randn(QKV, H, generator=g)).bfloat16()
     cos, sin = rope_tables(4096, d, 500000.0)
     row_seq = torch.randint(0, 3, (M,), generator=g, dtype=torch.int32)
-    row_pos = torch.randint(0, 4096, (M,), generator=g, dtype=torch.int32)
-    cells = torch.randperm(256, generator=g)[:M].to(torch.int32)
+    row_pos = torch.randperm(4096, generator=g)[:M].to(torch.int32)  # distinct (seq, pos)
+    cells = torch.randperm(1024, generator=g)[:M].to(torch.int32)
     pos2cell = torch.zeros(3, 4096, dtype=torch.int32)
     pos2cell[row_seq.long(), row_pos.long()] = cells
-    head_stride = 256
+    head_stride = 1024
     kp = torch.zeros(nkv, head_stride, d, dtype=torch.bfloat16, device=cuda)
     vp = torch.zeros_like(kp)
     Y = torch.zeros(M, QKV, dtype=torch.bfloat16, device=cuda)
     dev = [t.to(cuda) for t in (X, W, cos, sin, row_seq, row_pos, pos2cell)]
     Xd, Wd, cd, sd, rsd, rpd, p2cd = dev
-    ss = torch.zeros(32, dtype=torch.int64, device=cuda)
+    R = max(32, M)
+    ss = torch.zeros(R, dtype=torch.int64, device=cuda)
     scale = torch.ones(M)
     if norm:  # consumer row scale: X holds bf16(x * w); row sums of x^2 given
         x = torch.randn(M, H, generator=g) * 2
         fixed = ((x * x).double().sum(-1) * 2**24).round().long()
-        ss.copy_(torch.nn.functional.pad(fixed, (0, 32 - M)).to(cuda))
+        ss.copy_(torch.nn.functional.pad(fixed, (0, R - M)).to(cuda))
         scale = torch.rsqrt((x * x).sum(-1) / H + 1e-5)
     epi = SkinnyEpi(row_ss=ss.data_ptr() if norm else None, eps=1e-5, rope=1, n_heads=nh,
                     n_kv_heads=nkv, row_seq=rsd.data_ptr(), row_pos=rpd.data_ptr(),
                     pos2cell=p2cd.data_ptr(), pos_stride=4096, rope_cos=cd.data_ptr(),
                     rope_sin=sd.data_ptr(), k_pool_l=kp.data_ptr(), v_pool_l=vp.data_ptr(),
                     kv_head_stride=head_stride)
-    check(lib().ds_gemm_skinny_ex(Xd.data_ptr(), Wd.data_ptr(), Y.data_ptr(), M, QKV, H, 0, 0,
-                                  ctypes.byref(epi), torch.cuda.current_stream().cuda_stream))
+    check(_gemm_ex(lib(), Xd.data_ptr(), Wd.data_ptr(), Y.data_ptr(), M, QKV, H, 0, 0,
+                   ctypes.byref(epi), torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     qkv = unpermute_qk(_bf((X.float() @ W.float().T) * scale[:, None]), nh, nkv, d).float()
     from oracle.llama_ref import rope
