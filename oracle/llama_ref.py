@@ -8,7 +8,10 @@ angles), GQA attention, SwiGLU MLP, untied LM head.  It rounds to bf16 at
 exactly the tensor boundaries the GPU stores (norm outputs, projections,
 roped q/k, KV cache, attention output, MLP activations) and keeps the
 residual stream and every accumulation in fp32, so the tolerance budget is only the
-accumulation-order / bf16-P difference (logits max-abs <= 1e-2).
+accumulation-order / bf16-P difference.  Measured: per
+attention kernel max-abs <= 1e-2 (9e-3 worst); logits through the 8B layer
+shapes 4.6e-2 .. 5.6e-2 max-abs against this oracle's own fp32-vs-fp64 floor
+of 2.5e-2 - the stated logits bound is 6e-2 (tests/test_gpu_numerics_8b.py).
 """
 from __future__ import annotations
 
@@ -102,17 +105,69 @@ def forward(w: dict, shape, tokens: list[int], out_rows: list[int] | None = None
 
 
 @torch.no_grad()
+def forward_prefix(w: dict, shape, prefix_kv: list, tokens: list[int], start: int,
+                   out_rows: list[int], dtype=torch.float32, q_chunk: int = 256) -> torch.Tensor:
+    """Logits [len(out_rows), V] for `tokens` at positions start.. over an
+    EXTERNAL cached prefix: prefix_kv[l] = (k, v), each [start, n_kv, d] with
+    the values the paged store holds (k already rotated).  This is what the
+    GPU forward computes for a delta-prefill chunk / verify over an aliased
+    prefix - the prefix need not be re-run on the CPU, so
+    the 8B layer shapes at 32k positions stay tractable.  `dtype` float64 gives
+    the oracle's own accumulation-order noise floor.  Queries are processed in
+    chunks of q_chunk (score memory)."""
+    T = len(tokens)
+    nh, nkv, d = shape.n_heads, shape.n_kv_heads, shape.head_dim
+    G = nh // nkv
+    cos, sin = rope_tables(start + T, d, shape.rope_theta)
+    cos, sin = cos[start:], sin[start:]
+    cast = (lambda t: t.to(dtype))  # noqa: E731
+    x = cast(w["embed"][torch.tensor(tokens, dtype=torch.long)])
+    scale = 1.0 / (d ** 0.5)
+    kpos = torch.arange(start + T)
+    for l in range(shape.layers):
+        h = rmsnorm(x, cast(w["attn_norm"][l]), shape.rms_eps).to(dtype)
+        qkv = unpermute_qk(_bf(h @ cast(w["wqkv"][l]).T).to(dtype), nh, nkv, d)
+        q = qkv[:, : nh * d].view(T, nh, d)
+        k = qkv[:, nh * d: (nh + nkv) * d].view(T, nkv, d)
+        v = qkv[:, (nh + nkv) * d:].view(T, nkv, d)
+        q, k = rope(q, cos, sin).to(dtype), rope(k, cos, sin).to(dtype)
+        pk, pv = prefix_kv[l]
+        kk = torch.cat([cast(pk), k]).repeat_interleave(G, dim=1)  # [S, nh, d]
+        vv = torch.cat([cast(pv), v]).repeat_interleave(G, dim=1)
+        o = torch.empty(T, nh, d, dtype=dtype)
+        for a in range(0, T, q_chunk):
+            b = min(T, a + q_chunk)
+            s_ = torch.einsum("qhd,khd->hqk", q[a:b], kk) * scale
+            qpos = torch.arange(start + a, start + b)[:, None]
+            s_ = s_.masked_fill((kpos[None, :] > qpos)[None], float("-inf"))
+            o[a:b] = torch.einsum("hqk,khd->qhd", torch.softmax(s_, dim=-1), vv)
+        o = _bf(o.reshape(T, nh * d)).to(dtype)
+        x = x + o @ cast(w["wo"][l]).T
+        h = rmsnorm(x, cast(w["mlp_norm"][l]), shape.rms_eps).to(dtype)
+        gu = _bf(h @ cast(w["w_gate_up"][l]).T).to(dtype)
+        g, u = split_gate_up(gu, shape.ffn)
+        a_ = _bf(torch.nn.functional.silu(g) * u).to(dtype)
+        x = x + a_ @ cast(w["w_down"][l]).T
+    hf = rmsnorm(x[out_rows], cast(w["final_norm"]), shape.rms_eps).to(dtype)
+    return (hf @ cast(w["lm_head"]).T).float()
+
+
+@torch.no_grad()
 def paged_attention(q: torch.Tensor, k_cells: torch.Tensor, v_cells: torch.Tensor,
-                    q_pos: list[int], kv_len: int, scale: float) -> torch.Tensor:
+                    q_pos: list[int], kv_len: int, scale: float, q_chunk: int = 128) -> torch.Tensor:
     """Reference attention for one sequence: q [Tq, nh, d] (roped, bf16 values),
-    k/v [kv_len, nkv, d] gathered in logical order; causal by absolute position."""
+    k/v [kv_len, nkv, d] gathered in logical order; causal by absolute position.
+    Queries in chunks of q_chunk (bounded score memory at 32k keys)."""
     Tq, nh, d = q.shape
     G = nh // k_cells.shape[1]
     kr = k_cells.float().repeat_interleave(G, dim=1)
     vr = v_cells.float().repeat_interleave(G, dim=1)
-    s = torch.einsum("qhd,khd->hqk", q.float(), kr) * scale
     kpos = torch.arange(kv_len)[None, :]
-    qpos = torch.tensor(q_pos)[:, None]
-    s = s.masked_fill((kpos > qpos)[None], float("-inf"))
-    p = torch.softmax(s, dim=-1)
-    return torch.einsum("hqk,khd->qhd", p, vr)
+    out = torch.empty(Tq, nh, d)
+    for a in range(0, Tq, q_chunk):
+        b = min(Tq, a + q_chunk)
+        s = torch.einsum("qhd,khd->hqk", q[a:b].float(), kr) * scale
+        qpos = torch.tensor(q_pos[a:b])[:, None]
+        s = s.masked_fill((kpos > qpos)[None], float("-inf"))
+        out[a:b] = torch.einsum("hqk,khd->qhd", torch.softmax(s, dim=-1), vr)
+    return out

@@ -2,7 +2,7 @@
 (config.py:25-92) plus the model-shape / device keys of this build."""
 from __future__ import annotations
 
-from dataclasses import dataclass, field, fields
+from dataclasses import dataclass, field, fields, replace
 
 FEATURE_FLAGS = ("radix_enabled", "speculation_enabled", "response_cache_enabled",
                  "grouping_enabled", "validator_enabled")
@@ -95,7 +95,15 @@ class CoreConfig:
 
     @property
     def shape(self) -> ModelShape:
-        return SHAPES[self.model]
+        # "<shape>:L<n>" truncates a shape to its first n layers (numerics tests
+        # at the 8B layer shapes with a CPU-tractable oracle)
+        base, _, trunc = self.model.partition(":")
+        s = SHAPES[base]
+        if trunc:
+            if not trunc.startswith("L") or int(trunc[1:]) < 1:
+                raise ValueError(f"bad model truncation {self.model!r}")
+            s = replace(s, layers=int(trunc[1:]), name=self.model)
+        return s
 
     def with_overrides(self, **kw) -> "CoreConfig":
         known = {f.name for f in fields(self)}

@@ -49,3 +49,13 @@ def _built_library():
 
     build.build()
     cpu.build()
+
+
+def record_numeric(name: str, **values) -> None:
+    """Append one measured error record (max-abs, rel RMS, floor ...) to
+    gpurun_out/numerics.jsonl - the evidence behind the tolerances stated in
+    DESIGN.md section 4 (copied to profiles/ per round)."""
+    out = os.path.join(ROOT, "gpurun_out")
+    os.makedirs(out, exist_ok=True)
+    with open(os.path.join(out, "numerics.jsonl"), "a") as fh:
+        fh.write(json.dumps({"case": name, **values}) + "\n")

@@ -112,6 +112,20 @@ def test_attention_tcgen05_prefill_vs_fp32(cuda, past, q_len, contiguous):
     _attention_case(cuda, past, q_len, contiguous, impl=2)
 
 
+# per-kernel attention tolerance (bf16 Q/K/V in, fp32 softmax and accumulate,
+# P rounded to bf16 for the PV product, bf16 O out): measured max-abs at
+# N(0,1) inputs is recorded per case (gpurun_out/numerics.jsonl ->
+# profiles/round2/numerics.md); the bound is 1e-2
+ATTN_TOL = 1e-2
+
+
+# the BASELINE reference points on the 8B head shape: K6 at the C4 last turn
+# (31,489 cached + 881 new) and K7 verify q = 5 over 32k keys
+@pytest.mark.parametrize("past,q_len,impl", [(31489, 881, 2), (32768, 5, 1), (32768, 1, 1)])
+def test_attention_bench_points(cuda, past, q_len, impl):
+    _attention_case(cuda, past, q_len, True, impl)
+
+
 def _attention_case(cuda, past, q_len, contiguous, impl, nh=32, nkv=8):
     from paper_2605_26289_b200._lib import check, lib
 
@@ -141,7 +155,11 @@ def _attention_case(cuda, past, q_len, contiguous, impl, nh=32, nkv=8):
         torch.cuda.synchronize()
         got = out.cpu().float().view(q_len, nh, d)
         err = (got - ref).abs().max().item()
-        assert err < 2e-2, err
+        assert err < ATTN_TOL, err
+    from conftest import record_numeric
+
+    record_numeric(f"attention impl={impl} past={past} q={q_len} heads={nh}/{nkv} "
+                   f"contiguous={contiguous}", max_abs=err, ref_max=ref.abs().max().item())
 
 
 def test_rope_kv_store(cuda):
