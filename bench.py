@@ -333,6 +333,134 @@ def gemm_roofline(torch, eng, rows: int, peaks) -> dict:
             "launches": len(seq), "peak_source": peaks[3]}
 
 
+def cpu_fp32_baseline(threads: int) -> dict:
+    """the CPU fp32 oracle transformer
+    (oracle/cpu_engine.py, torch on all host cores) - (i) the full C1 workflow
+    through the product InferenceCore (tiny shape, copy policy: transcripts
+    equal the reference), (ii) the Llama-3-8B shape per layer at the C2 point
+    (delta-prefill 150 and verify q=5 over a 1,024-token paged prefix), one and
+    two layers timed so per-layer and LM-head costs separate; the per-turn
+    figure is estimated from them (32 layers, C2 pass mix).  A baseline, not a
+    target."""
+    import torch
+
+    from oracle.cpu_engine import CpuTransformerEngine
+    from paper_2605_26289_b200.config import CoreConfig
+    from paper_2605_26289_b200.kvcache import UnifiedKvCache
+    from paper_2605_26289_b200.scheduler import InferenceCore
+    from paper_2605_26289_b200.workload import core_config_for, load_trace, mismatches, replay
+
+    torch.set_num_threads(threads)
+
+    def weights(s, seed=0):
+        g = torch.Generator().manual_seed(seed)
+
+        def rn(*sh):
+            return (torch.randn(*sh, generator=g) * 0.02).bfloat16().float()
+
+        return {"embed": rn(s.vocab, s.hidden), "attn_norm": torch.ones(s.layers, s.hidden),
+                "wqkv": rn(s.layers, s.qkv_width, s.hidden),
+                "wo": rn(s.layers, s.hidden, s.n_heads * s.head_dim),
+                "mlp_norm": torch.ones(s.layers, s.hidden),
+                "w_gate_up": rn(s.layers, 2 * s.ffn, s.hidden),
+                "w_down": rn(s.layers, s.hidden, s.ffn), "final_norm": torch.ones(s.hidden),
+                "lm_head": rn(s.vocab, s.hidden)}
+
+    out = {"kind": "port (oracle fp32 transformer, torch on host cores)", "cores": threads}
+    tr = load_trace("c1")
+    cfg = core_config_for(tr, model="tiny")
+    eng = CpuTransformerEngine(cfg.shape, weights(cfg.shape), cfg.vocab, cfg.copy_min_match,
+                               cfg.capacity_cells)
+    core = InferenceCore(cfg, engine=eng)
+    eng.attach(core.kv)
+    t0 = time.perf_counter()
+    recs = replay(core, tr)
+    wall = time.perf_counter() - t0
+    lat = [r.latency_ms for r in recs]
+    out["c1"] = {"turns": len(recs), "turns_per_s": round(len(recs) / wall, 3),
+                 "p50_turn_ms": round(statistics.median(lat[1:]), 2),
+                 "parity_mismatches": len(mismatches(recs)),
+                 "sample": "C1 travel-5 workflow, tiny shape, full transformer math on the CPU"}
+    times = {}
+    for layers in (1, 2):
+        c8 = CoreConfig(model=f"llama3-8b:L{layers}", capacity_cells=2048)
+        s = c8.shape
+        kv = UnifiedKvCache(c8.capacity_cells)
+        e8 = CpuTransformerEngine(s, weights(s, 1), c8.vocab, c8.copy_min_match, c8.capacity_cells)
+        e8.attach(kv)
+        toks = [(13 * i + 7) % 30000 for i in range(1200)]
+        kv.append_cells(1, 1024 + 150)
+        e8.hist[1] = toks
+        row = {}
+        for name, q, rows in (("prefill150", 150, [149]), ("verify5", 5, list(range(5)))):
+            ts = []
+            for _ in range(3):
+                a = time.perf_counter()
+                e8._model(1, 1024, toks[1024:1024 + q], rows)
+                ts.append(time.perf_counter() - a)
+            row[name] = statistics.median(ts)
+        times[layers] = row
+        del e8
+    per = {k: times[2][k] - times[1][k] for k in times[1]}
+    head = {k: times[1][k] - per[k] for k in times[1]}
+    est = {k: head[k] + 32 * per[k] for k in per}
+    out["llama3_8b"] = {
+        "per_layer_ms": {k: round(1000 * v, 2) for k, v in per.items()},
+        "embed_lm_head_ms": {k: round(1000 * v, 2) for k, v in head.items()},
+        "est_forward_ms": {k: round(1000 * v, 1) for k, v in est.items()},
+        "est_c2_turn_ms": round(1000 * (est["prefill150"] + 11.2 * est["verify5"]), 1),
+        "sample": "1- and 2-layer truncations of the 8B shape timed (median of 3) at m=1024; "
+                  "forward = embed/head + 32 x layer; C2 turn = 1 delta prefill + 11.2 verify "
+                  "passes (SURVEY 8 C2 mix)"}
+    return out
+
+
+def c4_leg(args, torch) -> dict:
+    """Driver-visible BASELINE C4 leg: the 35-turn coding workflow growing to a
+    32,370-token prefix through InferenceCore (8B shape), per-turn latency vs
+    prefix length, parity-checked against the reference results, clocks
+    sampled during the timed replay."""
+    from paper_2605_26289_b200.scheduler import InferenceCore
+    from paper_2605_26289_b200.workload import core_config_for, load_trace, mismatches, replay
+
+    tr = load_trace("c4")
+    core = InferenceCore(core_config_for(tr, model=args.model))
+    replay(core, tr)  # warm-up (graph captures, first-touch)
+    core.reset_state()
+    core.engine.reset_counters()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t0 = time.perf_counter()
+        recs = replay(core, tr)
+        wall = time.perf_counter() - t0
+    bad = mismatches(recs)
+    if bad:
+        raise SystemExit(f"bench C4: {len(bad)} parity mismatches: {bad[:3]}")
+    bins = ((0, 4096), (4096, 8192), (8192, 16384), (16384, 24576), (24576, 40000))
+    curve = []
+    for lo, hi in bins:
+        ts = [r.latency_ms for r in recs if lo <= r.result.n_t < hi and r.result.cached_prompt_tokens]
+        if ts:
+            curve.append({"n_t": f"{lo}-{hi}", "turns": len(ts),
+                          "p50_turn_ms": round(statistics.median(ts), 2),
+                          "max_turn_ms": round(max(ts), 2)})
+    warm = [r.latency_ms for r in recs if r.result.cached_prompt_tokens]
+    fwd = core.engine.forward_stats()
+    out = {"workload": WORKLOAD_DESC["c4"], "turns": len(recs),
+           "p50_turn_ms": round(statistics.median(warm), 2),
+           "turns_per_s": round(len(recs) / wall, 3), "wall_s": round(wall, 3),
+           "device_s": round(core.engine.device_seconds(), 3),
+           "p50_vs_prefix": curve,
+           "prefill_tok_s": round(sum(r.result.prefill_tokens for r in recs)
+                                  / max(fwd["prefill"]["seconds"], 1e-9), 1),
+           "decode_tok_s": round(sum(len(r.result.generated) for r in recs)
+                                 / max(fwd["decode"]["seconds"], 1e-9), 1),
+           "parity": {"turns": len(recs), "mismatches": 0},
+           "clocks": clk.summary()}
+    del core
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     import torch
     import torch.distributed as dist
@@ -467,6 +595,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         from paper_2605_26289_b200.curve import prefix_curve
 
         line["prefix_curve"] = prefix_curve(model=args.model, weights=eng.w)
+    if not args.no_c4 and world == 1 and args.workload != "c4":
+        del core, eng  # the C4 core builds its own 8B engine (same seed: same weights)
+        torch.cuda.empty_cache()
+        line["c4_leg"] = c4_leg(args, torch)
     if not args.no_cpu and world == 1:
         ref = reference_turns(args.workload, 2)
         n, aff, model = cpu_info()
@@ -477,6 +609,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                       f"(copy-model mock, no model math), backend {ref['backend']}",
             "p50_turn_ms": round(statistics.median(ref["lat_ms"]), 3), "host_cpus": n,
             "affinity": aff, "cpu_model": model}
+        line["cpu_baseline_fp32"] = cpu_fp32_baseline(aff)
     print(json.dumps(line))
 
 
@@ -490,6 +623,7 @@ def main() -> None:
     ap.add_argument("--model", default="llama3-8b")
     ap.add_argument("--no-micro", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 (32k prefix) leg")
     ap.add_argument("--batched", action="store_true", help="one forward per plan (multi-session)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
