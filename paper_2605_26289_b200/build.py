@@ -48,7 +48,38 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
+HOST_SRC = os.path.join(HERE, "csrc_host", "hostcore.cpp")
+
+
+def host_lib_path() -> str:
+    import sysconfig
+
+    return os.path.join(HERE, "_hostcore" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_host(force: bool = False) -> str:
+    """The native host core (radix trie + cell allocator, pybind11) - g++,
+    in-tree next to the CUDA library."""
+    import sysconfig
+
+    import pybind11
+
+    out = host_lib_path()
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(HOST_SRC):
+        return out
+    tmp = out + ".tmp"
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-fvisibility=hidden",
+           "-I" + pybind11.get_include(), "-I" + sysconfig.get_paths()["include"], HOST_SRC,
+           "-o", tmp]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"g++ failed for hostcore.cpp:\n{res.stderr}")
+    os.replace(tmp, out)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_host(force)
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _deps_mtime():
         return LIB
     os.makedirs(BUILD, exist_ok=True)

@@ -341,9 +341,11 @@ class GpuEngine:
             segs_off = self.stage.add(segs)
             n_segs = len(segs)
             self._pending_hist = []
-        ops = self.kv.take_ops() + (extra_ops or [])
-        if ops:
-            ops_off = self.stage.add(np.asarray(ops, dtype=np.int32))
+        ops = np.asarray(self.kv.take_ops(), dtype=np.int32).reshape(-1, 5)
+        if extra_ops:
+            ops = np.concatenate([ops, np.asarray(extra_ops, dtype=np.int32).reshape(-1, 5)])
+        if len(ops):
+            ops_off = self.stage.add(ops)
             n_ops = len(ops)
         return segs_off, n_segs, ops_off, n_ops, cp_off, n_cp
 

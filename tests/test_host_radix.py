@@ -3,7 +3,8 @@ from __future__ import annotations
 
 from conftest import load_golden
 from paper_2605_26289_b200.kvcache import CapacityExhausted, UnifiedKvCache
-from paper_2605_26289_b200.radix import BudgetExceeded, RadixTrie
+from paper_2605_26289_b200.kvcache import PyUnifiedKvCache
+from paper_2605_26289_b200.radix import BudgetExceeded, PyRadixTrie, RadixTrie
 
 
 def test_golden_radix_sequences():
@@ -41,8 +42,10 @@ def test_golden_radix_sequences():
 
 
 def test_eviction_tie_break_lower_first_token():
-    kv = UnifiedKvCache(4096)
-    trie = RadixTrie(kv, 2048)
+    # pokes node internals: the Python restatement; the native core is held to
+    # it by the differential fuzz (test_host_native.py)
+    kv = PyUnifiedKvCache(4096)
+    trie = PyRadixTrie(kv, 2048)
     kv.append_cells(1, 4)
     trie.save([5, 5], 1, 0)
     trie.save([3, 3], 1, 2)
