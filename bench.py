@@ -115,10 +115,13 @@ def reference_turns(trace_name: str, repeats: int) -> dict:
             hs = []
             t0 = time.perf_counter()
             for r in wave:
+                toks, pieces = r.tokens, r.pieces
+                if r.messages is not None:  # the reference's own front end (render + tokenize)
+                    _, toks, pieces = core.prepare_prompt(r.messages, r.tool_defs)
                 g = core.pool.acquire("transient", timeout=1.0)
                 h = RequestHandle(GenerationRequest(
-                    request_id=r.id, prompt_tokens=list(r.tokens), prompt_pieces=list(r.pieces),
-                    max_tokens=r.max_tokens, temperature=0.0, seed=prompt_seed(r.tokens),
+                    request_id=r.id, prompt_tokens=list(toks), prompt_pieces=list(pieces),
+                    max_tokens=r.max_tokens, temperature=0.0, seed=prompt_seed(toks),
                     declared_tools=r.tools, guard=g))
                 core.submit(h)
                 hs.append(h)
@@ -488,7 +491,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
 
     def one_step():
         core.reset_state()
-        return replay(core, tr)
+        # chat traces enter through the host front end (render + tokenize caches)
+        return replay(core, tr, via_chat=True)
 
     for _ in range(args.warmup):
         one_step()
@@ -562,7 +566,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                    "max_tokens_per_session": max(r.n_t for r in [x.result for x in recs]),
                    "parallelism": f"session-sharded x{world} (one process per GPU)",
                    "token_policy": cfg.token_policy, "batched_forward": cfg.batched_forward,
-                   "l2": "weights 16 GB >> 126 MB L2 each forward (no flush needed)"},
+                   "l2": "weights 16 GB >> 126 MB L2 each forward (no flush needed)",
+                   "turn_input": "chat messages -> render + tokenize (host caches, "
+                                 "prepare_prompt) -> submit; latency from the messages"},
         "p50_turn_ms": round(statistics.median(warm), 3),
         "turn_ms_all": [round(r.latency_ms, 2) for r in recs[: min(nturns, 12)]],
         "prefill_tok_s": round(prefill_tok / max(fwd["prefill"]["seconds"], 1e-9), 1),

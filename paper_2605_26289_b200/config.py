@@ -77,6 +77,10 @@ class CoreConfig:
 
     validator_grace_pieces: int = 2
 
+    response_cache_entries: int = 1024
+    render_cache_entries: int = 256
+    tokenize_cache_entries: int = 64
+
     radix_enabled: bool = True
     speculation_enabled: bool = True
     response_cache_enabled: bool = True

@@ -627,7 +627,33 @@ class RadixCore {
 
 }  // namespace
 
+// FNV-1a 64 over UTF-8 bytes (reference _native.pyx fnv1a64_bytes)
+uint64_t fnv1a64(const char* p, size_t n) {
+  uint64_t h = 0xCBF29CE484222325ull;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= static_cast<uint8_t>(p[i]);
+    h *= 0x100000001B3ull;
+  }
+  return h;
+}
+
 PYBIND11_MODULE(_hostcore, m) {
+  m.def("fnv1a64_bytes", [](const py::bytes& b) {
+    const std::string s = b;
+    return fnv1a64(s.data(), s.size());
+  });
+  // tokenizer piece ids: fnv1a64(utf-8 piece) mod modulus (engine.py:228-230)
+  m.def("piece_ids", [](const py::list& pieces, uint64_t modulus) {
+    std::vector<int64_t> out;
+    out.reserve(pieces.size());
+    for (auto h : pieces) {
+      Py_ssize_t n = 0;
+      const char* p = PyUnicode_AsUTF8AndSize(h.ptr(), &n);
+      if (!p) throw py::error_already_set();
+      out.push_back(static_cast<int64_t>(fnv1a64(p, static_cast<size_t>(n)) % modulus));
+    }
+    return out;
+  });
   m.doc() = "deltaserve B200 native host core: cell allocator / page tables and radix trie";
   m.def("set_exceptions", [](py::object cap, py::object donor, py::object budget) {
     g_capacity_exc = cap;

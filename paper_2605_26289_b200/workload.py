@@ -39,6 +39,9 @@ class TraceRequest:
     expect: dict
     session: str | None = None  # session id (session path) or None (transient + radix)
     fail_after: int | None = None  # injected fault after this many tokens (acceptance c11)
+    messages: list | None = None   # chat input the prompt was rendered from (chat traces)
+    tool_defs: list | None = None
+    cache_stats: dict | None = None  # reference render / tokenize cache counters after it
 
 
 def load_trace(name: str) -> dict:
@@ -54,7 +57,8 @@ def load_trace(name: str) -> dict:
         last[r["stream"]] = (toks, pieces)
         reqs.append(TraceRequest(r["id"], r["wave"], r["stream"], toks, pieces, r["max_tokens"],
                                  frozenset(r["tools"]), r.get("expect", {}), r.get("session"),
-                                 r.get("fail_after")))
+                                 r.get("fail_after"), r.get("messages"), r.get("tool_defs"),
+                                 r.get("cache_stats")))
     tr["reqs"] = reqs
     return tr
 
@@ -74,12 +78,22 @@ class TurnRecord:
     handle_error: Exception | None = None
 
 
+class ChatMismatch(AssertionError):
+    """prepare_prompt did not reproduce the reference's tokens / pieces."""
+
+
 def replay(core, trace: dict, wave_limit: int | None = None, max_iters: int = 200_000,
-           rid_suffix: str = "") -> list[TurnRecord]:
+           rid_suffix: str = "", via_chat: bool = False) -> list[TurnRecord]:
     """Submit each wave's requests together and step the core until they finish.
     Session traces (mode "sessions") bind one session per id first
     (`InferenceCore.open_session`, POST /v1/sessions) and delete them all after
-    the last wave (`close_session`, DELETE /v1/sessions/{id})."""
+    the last wave (`close_session`, DELETE /v1/sessions/{id}).
+
+    via_chat: requests that carry their chat messages go through the host
+    front end first - render + tokenize with the render / tokenize caches
+    (InferenceCore.prepare_prompt, reference scheduler.py:340-346) - and the
+    turn latency starts before it; the produced ids / pieces must equal the
+    reference's recorded prompt."""
     from .scheduler import GenerationRequest, RequestHandle
 
     records: list[TurnRecord] = []
@@ -90,13 +104,20 @@ def replay(core, trace: dict, wave_limit: int | None = None, max_iters: int = 20
         handles = []
         for r in wave:
             session = sessions[r.session] if r.session is not None else None
+            t_start = time.monotonic()
+            tokens, pieces = r.tokens, r.pieces
+            if via_chat and r.messages is not None:
+                _, tokens, pieces = core.prepare_prompt(r.messages, r.tool_defs)
+                if tokens != r.tokens or pieces != r.pieces:
+                    raise ChatMismatch(f"{r.id}: front end produced a different prompt")
             guard = None if session is not None else core.pool.acquire("transient", timeout=1.0)
-            req = GenerationRequest(request_id=r.id + rid_suffix, prompt_tokens=list(r.tokens),
-                                    prompt_pieces=list(r.pieces), max_tokens=r.max_tokens,
-                                    temperature=0.0, seed=prompt_seed(r.tokens),
+            req = GenerationRequest(request_id=r.id + rid_suffix, prompt_tokens=list(tokens),
+                                    prompt_pieces=list(pieces), max_tokens=r.max_tokens,
+                                    temperature=0.0, seed=prompt_seed(tokens),
                                     declared_tools=r.tools, guard=guard, session=session,
                                     fail_after_tokens=r.fail_after)
             h = RequestHandle(req)
+            h.submitted_at = t_start  # the turn starts at its chat input
             core.submit(h)
             handles.append((r, h))
         pending = [h for _, h in handles]

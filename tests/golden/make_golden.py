@@ -299,6 +299,8 @@ class Recorder:
         self.requests = []
         self.last_prompt = {}  # stream key -> (tokens, pieces) for delta coding
         self.wave = 0  # requests of one wave are submitted together, then run to completion
+        self.chat = None  # (messages, tools) of the next submit, when recording chat input
+        self.record_chat = False
 
     def submit(self, stream, tokens, pieces, max_tokens, tools, rid, session=None):
         # a session request holds no transient guard (server.py:300-318)
@@ -319,6 +321,14 @@ class Recorder:
                "pieces": pieces[c:], "max_tokens": max_tokens, "tools": sorted(declared)}
         if session is not None:
             rec["session"] = session.session_id
+        if self.record_chat and self.chat is not None:
+            # the chat input the prompt was rendered + tokenized from
+            # (scheduler.py:340-346), plus the caches' counters after it
+            rec["messages"] = json.loads(json.dumps(self.chat[0]))
+            rec["tool_defs"] = self.chat[1]
+            rec["cache_stats"] = {"render": self.core.render_cache.stats(),
+                                  "tokenize": self.core.tokenize_cache.stats()}
+            self.chat = None
         self.requests.append((h, rec))
         return h
 
@@ -356,9 +366,11 @@ class Conv:
         self.sc = sc
         self.messages = [{"role": "system", "content": sc.system}]
 
-    def prompt(self, core, t):
+    def prompt(self, core, t, rec=None):
         self.messages.append({"role": "user", "content": self.sc.user_texts[t]})
         _, toks, pieces = core.prepare_prompt(self.messages, self.sc.tools)
+        if rec is not None:
+            rec.chat = (list(self.messages), self.sc.tools)
         return toks, pieces
 
     def after(self, t, result):
@@ -373,11 +385,14 @@ def core_snapshot(core):
             "iterations": core.iterations}
 
 
-def trace_sequential(name, cfg_over, scenarios, interleave=True, bursts=()):
+def trace_sequential(name, cfg_over, scenarios, interleave=True, bursts=(), chat=False):
     """Conversations turn by turn (interleaved A1 B1 C1 A2 ...), each turn run to
-    completion; then optional bursts of concurrent single-turn requests."""
+    completion; then optional bursts of concurrent single-turn requests.
+    chat=True also records each request's chat messages / tools and the
+    render / tokenize cache counters (host front-end parity)."""
     core = InferenceCore(ServerConfig(**cfg_over))
     rec = Recorder(core)
+    rec.record_chat = chat
     convs = [Conv(sc) for sc in scenarios]
     turns = max(sc.turn_count for sc in scenarios)
     order = ([(t, i) for t in range(turns) for i in range(len(convs))] if interleave
@@ -387,7 +402,7 @@ def trace_sequential(name, cfg_over, scenarios, interleave=True, bursts=()):
         conv = convs[i]
         if t >= conv.sc.turn_count:
             continue
-        toks, pieces = conv.prompt(core, t)
+        toks, pieces = conv.prompt(core, t, rec)
         h = rec.submit(f"s{i}", toks, pieces, conv.sc.max_tokens, conv.sc.tools,
                        f"{conv.sc.name}-t{t}")
         rec.run_until_done([h])
@@ -399,6 +414,7 @@ def trace_sequential(name, cfg_over, scenarios, interleave=True, bursts=()):
         for w, text in enumerate(texts):
             msgs = [{"role": "system", "content": system}, {"role": "user", "content": text}]
             _, toks, pieces = core.prepare_prompt(msgs, tools)
+            rec.chat = (msgs, tools)
             handles.append(rec.submit(f"b{w}", toks, pieces, 80, tools, f"burst-{bsalt}-{w}"))
         rec.run_until_done(handles)
         snaps.append(core_snapshot(core))
@@ -527,12 +543,12 @@ def deep_c4(salt, turns, pieces=820):
 def gen_traces():
     c2 = agentic_6turn("c2")
     traces = [
-        trace_sequential("c1", {}, [agent_scenario("travel", "c1")]),
-        trace_sequential("c2", {"spec_max_lookahead": 4}, [c2]),
+        trace_sequential("c1", {}, [agent_scenario("travel", "c1")], chat=True),
+        trace_sequential("c2", {"spec_max_lookahead": 4}, [c2], chat=True),
         trace_sequential("c2_nospec", {"spec_max_lookahead": 4, "speculation_enabled": False}, [c2]),
         trace_sequential("c3", {"pool_transient": 16},
                          [deep_workflow(s, 5) for s in ("c3a", "c3b", "c3c")],
-                         bursts=[("c3burst", 16)]),
+                         bursts=[("c3burst", 16)], chat=True),
         trace_sequential("c3_nogroup", {"pool_transient": 16, "grouping_enabled": False},
                          [deep_workflow(s, 5) for s in ("c3a", "c3b", "c3c")],
                          bursts=[("c3burst", 16)]),

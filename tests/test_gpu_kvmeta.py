@@ -17,9 +17,10 @@ pytestmark = pytest.mark.gpu
 def _apply(cuda, ops, pos2cell, member, trie, n_seqs):
     from paper_2605_26289_b200._lib import check, lib
 
-    if not ops:
+    ops = np.asarray(ops, dtype=np.int32).reshape(-1, 5)
+    if not len(ops):
         return
-    o = torch.tensor(np.asarray(ops, dtype=np.int32)).to(cuda)
+    o = torch.tensor(ops).to(cuda)
     check(lib().ds_kv_apply(o.data_ptr(), len(ops), pos2cell.data_ptr(), pos2cell.shape[1],
                             n_seqs, member.data_ptr(), member.shape[1], trie.data_ptr(),
                             torch.cuda.current_stream().cuda_stream))
