@@ -28,5 +28,12 @@ python tools/profile_forward.py llama3-8b 1000 5 > $OUT/forward_critical_path.tx
 python tools/timeline.py llama3-8b 1000 5 > $OUT/timeline_verify_m1000.txt 2>&1
 python tools/timeline.py llama3-8b 1000 5 edges >> $OUT/timeline_verify_m1000.txt 2>&1
 python tools/timeline.py llama3-8b 1000 150 > $OUT/timeline_prefill_m1000.txt 2>&1
+# the C5 batched forward (256 sessions, one varlen forward per plan): launch list
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 20000 -c 2500 --csv \
+  --log-file $OUT/launches_c5.csv python bench.py --workload c5 --steps 1 --warmup 1 --no-cpu \
+  --no-micro > $OUT/launches_c5_bench.log 2>&1
+# K10 (opt-in stream-K GEMM) on the prefill qkv shape, for the record
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:gemm_cluster -s 2 -c 1 \
+  -o $OUT/ncu_k10_cluster python tools/one_gemm.py 150 6144 4096 4 > /dev/null 2>&1
 python tools/fwd_time.py llama3-8b 1000:5 2048:5 8192:5 32768:5 1000:1 32768:1 1000:150 > $OUT/fwd_time.txt 2>&1
 ls -la $OUT
