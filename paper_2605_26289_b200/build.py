@@ -79,7 +79,8 @@ def build_host(force: bool = False) -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    build_host(force)
+    if not os.environ.get("DS_LIB_OUT"):  # variant builds: the CUDA library only
+        build_host(force)
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _deps_mtime():
         return LIB
     os.makedirs(BUILD, exist_ok=True)

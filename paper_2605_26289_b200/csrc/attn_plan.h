@@ -36,6 +36,12 @@ constexpr int kDecodeTcMinKeys = 4096;
 #define DS_K7_SHORT_TILES (8 * kDecodeMaxCluster)
 #endif
 constexpr int kDecodeShortTiles = DS_K7_SHORT_TILES;  // see attn_split_plan
+#ifndef DS_K7_SHORT_SPLITS  // split cap for R > 8 rows over <= kDecodeShortTiles key tiles
+#define DS_K7_SHORT_SPLITS kDecodeMaxCluster
+#endif
+#ifndef DS_K7_SHORT_SPLITS_SMALL  // the same cap for R <= 8 rows (A/B; default: none)
+#define DS_K7_SHORT_SPLITS_SMALL 64
+#endif
 constexpr int kSplitRows = 64;  // packed rows per split-kernel CTA (4 warps x 16)
 
 struct AttnSplitPlan {
@@ -57,9 +63,12 @@ DS_HD AttnSplitPlan attn_split_plan(int qblocks, int kv_len, int nkv, int n_entr
   int n = mode ? kNumSMs / ctas : (2 * kNumSMs + ctas - 1) / ctas;
   const int by_len = (kv_len + 127) / 128;
   if (n > by_len) n = by_len;
-  if (mode && rows > kDecodeLastMergeRows && n > kDecodeMaxCluster &&
+  if (mode && rows > kDecodeLastMergeRows && n > DS_K7_SHORT_SPLITS &&
       by_len <= kDecodeShortTiles)
-    n = kDecodeMaxCluster;
+    n = DS_K7_SHORT_SPLITS;
+  if (mode && rows <= kDecodeLastMergeRows && n > DS_K7_SHORT_SPLITS_SMALL &&
+      by_len <= kDecodeShortTiles)
+    n = DS_K7_SHORT_SPLITS_SMALL;
   if (n > 64) n = 64;
   if (n < 1) n = 1;
   const int gran = mode ? 128 : 64;  // key tile of the kernel

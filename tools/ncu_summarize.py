@@ -56,7 +56,8 @@ def main(tag: str) -> None:
     md = [f"# ncu summaries ({tag})\n",
           "Captured with `tools/profile_round.sh` under gpurun on one B200 "
           "(`ncu --set full --clock-control none`); numbers per launch.\n"]
-    for name in ("ncu_gemm_ring", "ncu_k7_decode", "ncu_k7_decode_q1", "ncu_k6_prefill"):
+    for name in ("ncu_gemm_ring", "ncu_k7_decode", "ncu_k7_decode_q1", "ncu_k6_prefill",
+                 "ncu_k10_cluster"):
         rep = os.path.join(OUT, name + ".ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -76,9 +77,13 @@ def main(tag: str) -> None:
             txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
                                  capture_output=True, text=True).stdout
             fh.write(txt)
-    # launch list -> per-kernel share of GPU time in the bench step
-    lpath = os.path.join(OUT, "launches.csv")
-    if os.path.exists(lpath):
+    # launch lists -> per-kernel share of GPU time in the bench step
+    for lname, title in (("launches.csv", "bench.py --steps 1 (C2), steady state"),
+                         ("launches_c5.csv", "bench.py --workload c5 --steps 1 (256 sessions, "
+                                             "batched plans)")):
+        lpath = os.path.join(OUT, lname)
+        if not os.path.exists(lpath):
+            continue
         lines = open(lpath).read().splitlines()
         start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
         rd = csv.DictReader(lines[start:])
@@ -96,15 +101,15 @@ def main(tag: str) -> None:
             tot[k] += v
             cnt[k] += 1
         T = sum(tot.values())
-        md.append("\n## launch list share (bench.py --steps 1, steady state, cold-cache serialised)\n")
+        md.append(f"\n## launch list share ({title}; cold-cache serialised)\n")
         md.append("| kernel | launches | total us | share |")
         md.append("|---|---|---|---|")
         share = {}
         for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
             md.append(f"| {k} | {cnt[k]} | {v:.1f} | {v / T * 100:.1f}% |")
             share[k] = v / T
-        summary["launch_share"] = share
-        with open(os.path.join(dst, "launches.csv"), "w") as fh:
+        summary["launch_share" if lname == "launches.csv" else "launch_share_c5"] = share
+        with open(os.path.join(dst, lname), "w") as fh:
             fh.write(open(lpath).read())
     g = summary.get("ncu_gemm_ring")
     if g:
