@@ -637,7 +637,42 @@ uint64_t fnv1a64(const char* p, size_t n) {
   return h;
 }
 
+// FNV-1a over the 4-byte little-endian serialisation of tokens[start:end]
+// (reference _native.pyx:36-59: uint32 reinterpretation), straight from a
+// Python list (no int32 array conversion) or any int32-convertible buffer
+template <typename H, H kPrime>
+H fnv_tokens(py::handle seq, py::ssize_t start, py::ssize_t end, H h) {
+  auto step = [&](uint32_t u) {
+    for (int b = 0; b < 4; ++b) {
+      h ^= static_cast<uint8_t>(u >> (8 * b));
+      h *= kPrime;
+    }
+  };
+  if (PyList_Check(seq.ptr())) {
+    const py::ssize_t n = PyList_GET_SIZE(seq.ptr());
+    if (end > n) end = n;
+    for (py::ssize_t i = start; i < end; ++i) {
+      const long v = PyLong_AsLong(PyList_GET_ITEM(seq.ptr(), i));
+      if (v == -1 && PyErr_Occurred()) throw py::error_already_set();
+      step(static_cast<uint32_t>(static_cast<int32_t>(v)));
+    }
+    return h;
+  }
+  auto a = py::array_t<int32_t, py::array::c_style | py::array::forcecast>::ensure(seq);
+  if (!a) throw py::type_error("tokens must be a list or an int32-convertible array");
+  const int32_t* d = a.data();
+  if (end > a.size()) end = a.size();
+  for (py::ssize_t i = start; i < end; ++i) step(static_cast<uint32_t>(d[i]));
+  return h;
+}
+
 PYBIND11_MODULE(_hostcore, m) {
+  m.def("fnv1a64_tokens", [](py::handle seq, py::ssize_t start, py::ssize_t end, uint64_t state) {
+    return fnv_tokens<uint64_t, 0x100000001B3ull>(seq, start, end, state);
+  });
+  m.def("fnv1a32_tokens", [](py::handle seq, py::ssize_t start, py::ssize_t end, uint32_t state) {
+    return fnv_tokens<uint32_t, 0x01000193u>(seq, start, end, state);
+  });
   m.def("fnv1a64_bytes", [](const py::bytes& b) {
     const std::string s = b;
     return fnv1a64(s.data(), s.size());

@@ -26,7 +26,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import _lib
+from . import _hostcore, _lib
 from ._lib import check, lib
 from .config import CoreConfig
 from .kernels import FNV64_OFFSET, _as_i32, host_fnv1a64_tokens
@@ -308,7 +308,7 @@ class GpuEngine:
         if ln > past:
             ln, st = 0, FNV64_OFFSET
         if past > ln:
-            st = host_fnv1a64_tokens(tokens[ln:past], st)
+            st = _hostcore.fnv1a64_tokens(tokens, ln, past, st)
         self._hash[seq] = (past, st)
         return st
 
@@ -392,41 +392,50 @@ class GpuEngine:
         G = self.shape.n_heads // self.shape.n_kv_heads
         order = sorted(range(n_e),
                        key=lambda i: 0 if len(reqs[i].batch) * G > DECODE_MAX_ROWS else 1)
+        # per-entry columns in one pass, then vectorised row arrays
+        rs = [reqs[ri] for ri in order]
+        qs = np.fromiter((len(r.batch) for r in rs), dtype=np.int64, count=n_e)
+        if n_e and qs.min() == 0:
+            raise ValueError("batch must be non-empty")
+        kinds = np.fromiter((r.kind for r in rs), dtype=np.int64, count=n_e)
+        pasts = np.fromiter((r.past for r in rs), dtype=np.int64, count=n_e)
+        seqs = np.fromiter((r.seq for r in rs), dtype=np.int64, count=n_e)
+        n_outs = np.where(kinds == _lib.ENTRY_VERIFY, qs, 1)
+        q_starts = np.concatenate(([0], np.cumsum(qs)[:-1]))
+        out_starts = np.concatenate(([0], np.cumsum(n_outs)[:-1]))
+        q_start, out_start = int(qs.sum()), int(n_outs.sum())
+        if q_start > self.max_rows or out_start > self.max_out:
+            raise ValueError("forward exceeds engine buffers")
         ents = np.zeros(n_e, dtype=_ENTRY_DT)
-        erows = []  # entry tuples, one structured-array assignment at the end
-        tok_l, seq_l, pos_l, out_l = [], [], [], []
-        q_start = out_start = 0
+        ents["seq"], ents["past"], ents["q_len"], ents["q_start"] = seqs, pasts, qs, q_starts
+        ents["kind"], ents["out_start"], ents["n_out"] = kinds, out_starts, n_outs
+        ents["n_draft"] = np.fromiter((r.n_draft for r in rs), dtype=np.int64, count=n_e)
+        ents["hash_in"] = np.fromiter((self._hash_in(r.seq, r.past, r.tokens) for r in rs),
+                                      dtype=np.uint64, count=n_e)
+        row_entry = np.repeat(np.arange(n_e), qs)
+        row_in = np.arange(q_start) - np.repeat(q_starts, qs)  # row index within its entry
+        tok_l = []
+        for r in rs:
+            tok_l.extend(r.batch)
+        toks = [np.asarray(tok_l, dtype=np.int32)]
+        rseq = [seqs[row_entry].astype(np.int32)]
+        rpos = [(pasts[row_entry] + row_in).astype(np.int32)]
+        # sampled rows: the last n_out rows of every entry
+        orow = [np.nonzero(row_in >= (qs - n_outs)[row_entry])[0].astype(np.int32)]
         scratch_ops, scratch_of, s_off = [], {}, 0
         for i, ri in enumerate(order):
-            r = reqs[ri]
-            q = len(r.batch)
-            if q == 0:
-                raise ValueError("batch must be non-empty")
-            n_out = q if r.kind == _lib.ENTRY_VERIFY else 1
-            erows.append((r.seq, r.past, q, q_start, r.kind, r.n_draft, out_start, n_out,
-                          self._hash_in(r.seq, r.past, r.tokens)))
-            tok_l.extend(r.batch)
-            seq_l.extend([r.seq] * q)
-            pos_l.extend(range(r.past, r.past + q))
-            out_l.extend(range(q_start + q - n_out, q_start + q))
+            r = rs[i]
             if r.scratch:
+                q = int(qs[i])
                 if s_off + q > self.n_scratch:
                     raise ValueError("scratch cells exhausted")
                 cell = self.capacity + s_off
                 scratch_ops.append((_lib.KV_MAP_SCRATCH, r.seq, r.past, cell, q))
                 scratch_of[ri] = list(range(cell, cell + q))
                 s_off += q
-            q_start += q
-            out_start += n_out
-            if count:
+        if count:
+            for q in qs.tolist():
                 self.ledger.count_forward(q)
-        if q_start > self.max_rows or out_start > self.max_out:
-            raise ValueError("forward exceeds engine buffers")
-        ents[:] = erows
-        toks = [np.asarray(tok_l, dtype=np.int32)]
-        rseq = [np.asarray(seq_l, dtype=np.int32)]
-        rpos = [np.asarray(pos_l, dtype=np.int32)]
-        orow = [np.asarray(out_l, dtype=np.int32)]
         st = self.stage
         st.reset()
         if q_start <= GRAPH_MAX_ROWS or n_e == 1:
@@ -478,24 +487,24 @@ class GpuEngine:
         f[0] += 1
         f[1] += self._ev[0].elapsed_time(self._ev[1]) / 1000.0
         f[2] += q_start
-        f[3] += sum(r.past + len(r.batch) for r in reqs)
+        f[3] += int(pasts.sum()) + q_start
         h = self.res_host.numpy()
         tok, src, acc = h[: self.max_out], h[self.max_out: 2 * self.max_out], h[2 * self.max_out:]
         if nd:  # cache the proposals for the token lists the scheduler will hold next
             o = self.nd_off
             dlen = h[o + 2 * n_e: o + 3 * n_e]
             drafts = h[o + 3 * n_e: o + 3 * n_e + n_e * self.nd_cap].reshape(n_e, self.nd_cap)
-            for i, ri in enumerate(order):
-                r = reqs[ri]
+            for i, r in enumerate(rs):
                 a = int(acc[i]) if r.kind == _lib.ENTRY_VERIFY else 0
                 self._draft_cache[r.seq] = (r.past + a + 2, drafts[i, : dlen[i]].tolist())
         out = [None] * n_e
-        for i, ri in enumerate(order):
-            r = reqs[ri]
-            o0, n_out = int(ents[i]["out_start"]), int(ents[i]["n_out"])
-            rows = [RowResult(int(tok[o0 + j]), None if src[o0 + j] < 0 else int(src[o0 + j]))
+        tok_all, src_all = tok[:out_start].tolist(), src[:out_start].tolist()
+        acc_all = acc[:n_e].tolist()
+        for i, (ri, o0, n_out) in enumerate(zip(order, out_starts.tolist(), n_outs.tolist())):
+            r = rs[i]
+            rows = [RowResult(tok_all[o0 + j], None if src_all[o0 + j] < 0 else src_all[o0 + j])
                     for j in range(n_out)]
-            res = VerifyResult(int(acc[i]), rows) if r.kind == _lib.ENTRY_VERIFY else rows[0]
+            res = VerifyResult(acc_all[i], rows) if r.kind == _lib.ENTRY_VERIFY else rows[0]
             if r.scratch:
                 res.scratch = scratch_of[ri]
             out[ri] = res

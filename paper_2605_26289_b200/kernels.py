@@ -20,6 +20,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from . import _hostcore
 from ._lib import check, lib, stream_ptr
 
 BACKEND = "cuda-sm100a"
@@ -166,15 +167,15 @@ def longest_suffix_match(ring, tail, min_len: int) -> tuple[int, int]:
 # ---------------------------------------------------------------------------
 
 def host_fnv1a64_tokens(tokens, state: int | None = None) -> int:
-    a = _as_i32(tokens)
-    return int(lib().ds_host_fnv1a64_tokens(a.ctypes.data, len(a),
-                                            FNV64_OFFSET if state is None else state))
+    """Host bookkeeping hash (native host core; same function as the library's
+    ds_host_fnv1a64_tokens, reference _native.pyx:47-59)."""
+    return _hostcore.fnv1a64_tokens(tokens, 0, len(tokens),
+                                    FNV64_OFFSET if state is None else state)
 
 
 def host_fnv1a32_tokens(tokens, state: int | None = None) -> int:
-    a = _as_i32(tokens)
-    return int(lib().ds_host_fnv1a32_tokens(a.ctypes.data, len(a),
-                                            FNV32_OFFSET if state is None else state))
+    return _hostcore.fnv1a32_tokens(tokens, 0, len(tokens),
+                                    FNV32_OFFSET if state is None else state)
 
 
 def prompt_seed(tokens) -> int:
