@@ -27,7 +27,9 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "agentic turns/s (per-turn p50 latency, delta-prefill & decode tok/s alongside)"
+METRIC = ("per-turn p50 latency and delta-prefill/decode tok/s vs prefix length (headline value: "
+          "C2 agentic turns/s; p50_turn_ms, prefill/decode tok/s, prefix_curve and the C4 "
+          "per-prefix-length leg on the same line)")
 UNIT = "turns/s"
 
 

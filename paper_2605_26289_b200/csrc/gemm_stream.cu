@@ -614,6 +614,139 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_stream_kernel(
   }
 }
 
+// ---- token-row epilogue (cluster mode): one warp = one token row of the
+// tile's 128 features, lane l = features 4l..4l+3 - every global access is a
+// contiguous 8- or 16-byte piece of a 256 / 512-byte row segment; the
+// gate/up and RoPE-pair partners (features f, f ^ 8) are lanes l, l ^ 2 ----
+DS_DEVICE void epilogue_tokrow(float4 y, const StreamArgs& a, const ds_skinny_epi& epi, int wt,
+                               int tk, int lane, const float* s_inv, const int* s_pos,
+                               const int64_t* s_cell) {
+  const int fl = 4 * lane, f = wt * kBM + fl;
+  const int t = tk;  // cluster mode: one token tile, t0 = 0
+  float v[4] = {y.x, y.y, y.z, y.w};
+  if (epi.row_ss) {
+    const float sc = s_inv[tk];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] *= sc;
+  }
+  auto st_bf4 = [](__nv_bfloat16* d, float a0, float a1, float a2, float a3) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(a0, a1), hi = __floats2bfloat162_rn(a2, a3);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&lo);
+    u.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(d) = u;
+  };
+  if (epi.rope) {
+    constexpr int kHd = 128, kHalf = 64;
+    const int qk_width = (epi.n_heads + epi.n_kv_heads) * kHd;
+    if (wt * kBM < qk_width) {
+      const int head = wt, c = fl;  // features within the head
+      const bool lo = (c & 15) < 8;
+      const int i0 = 8 * (c >> 4) + (c & 7);  // dims i0..i0+3 (or +64)
+      float x[4], p[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        x[k] = bf16r_(v[k]);  // the unfused path stores qkv in bf16
+        p[k] = __shfl_xor_sync(0xffffffffu, x[k], 2);
+      }
+      const int64_t tp = static_cast<int64_t>(s_pos[tk]) * kHalf + i0;
+      const float4 cs = *reinterpret_cast<const float4*>(epi.rope_cos + tp);
+      const float4 sn = *reinterpret_cast<const float4*>(epi.rope_sin + tp);
+      const float cc[4] = {cs.x, cs.y, cs.z, cs.w}, ss[4] = {sn.x, sn.y, sn.z, sn.w};
+      float o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[k] = lo ? x[k] * cc[k] - p[k] * ss[k] : x[k] * cc[k] + p[k] * ss[k];
+      __nv_bfloat16* row =
+          head < epi.n_heads
+              ? static_cast<__nv_bfloat16*>(a.Y) + static_cast<int64_t>(t) * a.N + head * kHd
+              : static_cast<__nv_bfloat16*>(epi.k_pool_l) +
+                    ((head - epi.n_heads) * epi.kv_head_stride + s_cell[tk]) * kHd;
+      st_bf4(row + (lo ? i0 : i0 + kHalf), o[0], o[1], o[2], o[3]);
+    } else {
+      const int fv = f - qk_width;
+      __nv_bfloat16* d = static_cast<__nv_bfloat16*>(epi.v_pool_l) +
+                         ((fv / kHd) * epi.kv_head_stride + s_cell[tk]) * kHd + fv % kHd;
+      st_bf4(d, v[0], v[1], v[2], v[3]);
+    }
+    return;
+  }
+  if (epi.swiglu) {
+    float u[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) u[k] = __shfl_xor_sync(0xffffffffu, v[k], 2);
+    if ((fl & 15) >= 8) return;  // up lanes
+    float o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float gg = bf16r_(v[k]), uu = bf16r_(u[k]);  // the unfused path stores gate|up in bf16
+      o[k] = gg / (1.f + expf(-gg)) * uu;
+    }
+    const int unit = wt * (kBM / 2) + (fl >> 4) * 8 + (fl & 7);
+    st_bf4(static_cast<__nv_bfloat16*>(a.Y) + static_cast<int64_t>(t) * (a.N / 2) + unit, o[0],
+           o[1], o[2], o[3]);
+    return;
+  }
+  const int64_t off = static_cast<int64_t>(t) * a.N + f;
+  if (epi.argmax_out) {
+    if (a.Y) *reinterpret_cast<float4*>(static_cast<float*>(a.Y) + off) = make_float4(v[0], v[1], v[2], v[3]);
+    unsigned long long k = argmax_key(v[0], f);
+#pragma unroll
+    for (int q = 1; q < 4; ++q) {
+      const unsigned long long kq = argmax_key(v[q], f + q);
+      k = kq > k ? kq : k;
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      const unsigned long long o = shfl_xor_u64(k, m);
+      k = o > k ? o : k;
+    }
+    if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(epi.argmax_out) + t, k);
+    return;
+  }
+  if (a.y_f32) {
+    float* yp = static_cast<float*>(a.Y) + off;
+    if (a.accumulate) {
+      const float4 old = *reinterpret_cast<const float4*>(yp);
+      v[0] += old.x;
+      v[1] += old.y;
+      v[2] += old.z;
+      v[3] += old.w;
+    }
+    *reinterpret_cast<float4*>(yp) = make_float4(v[0], v[1], v[2], v[3]);
+  } else {
+    __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(a.Y) + off;
+    if (a.accumulate) {
+      const uint2 uo = *reinterpret_cast<const uint2*>(yp);
+      const float2 p0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uo.x));
+      const float2 p1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uo.y));
+      v[0] += p0.x;
+      v[1] += p0.y;
+      v[2] += p1.x;
+      v[3] += p1.y;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = bf16r_(v[k]);
+    st_bf4(yp, v[0], v[1], v[2], v[3]);
+  }
+  if (epi.ss_out) {  // residual producer: next RMSNorm's weight multiply + row sums
+    if (epi.h_out && a.h_w) {
+      const uint2 hu = *reinterpret_cast<const uint2*>(a.h_w + f);
+      const float2 h0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hu.x));
+      const float2 h1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hu.y));
+      st_bf4(static_cast<__nv_bfloat16*>(epi.h_out) + off, v[0] * h0.x, v[1] * h0.y,
+             v[2] * h1.x, v[3] * h1.y);
+    }
+    long long q = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q += __float2ll_rn(v[k] * v[k] * kSsScale);
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) q += static_cast<long long>(shfl_xor_u64(q, m));
+    if (lane == 0)
+      atomicAdd(reinterpret_cast<unsigned long long*>(epi.ss_out) + t,
+                static_cast<unsigned long long>(q));
+  }
+}
+
 // ---- cluster split-K mode: one token tile (T <= 256) and fewer weight tiles
 // than SMs (qkv / wo / down at prefill-chunk sizes).  The S CTAs of a cluster
 // take S equal k ranges of ONE tile; each leaves its partial tile in its own
@@ -629,15 +762,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cluster_kernel(
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // SW128 atoms
   const int stage_bytes = kSlabA + a.NT * 128;
   uint8_t* tail = smem + a.stages * stage_bytes;
-  float* s_inv = reinterpret_cast<float*>(tail);
-  int* s_pos = reinterpret_cast<int*>(s_inv + kMaxNT);
-  int64_t* s_cell = reinterpret_cast<int64_t*>(s_pos + kMaxNT);
-  unsigned long long* s_amax = reinterpret_cast<unsigned long long*>(s_cell + kMaxNT);
-  float* stg_all = reinterpret_cast<float*>(s_amax + kMaxNT);  // [8 warps][32][kStg]
-  uint64_t* full = reinterpret_cast<uint64_t*>(stg_all + 8 * 32 * kStg);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tail);
   uint64_t* empty = full + a.stages;
   uint64_t* acc_full = empty + a.stages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  // epilogue-phase scalars live in the (then idle) ring after the partial tile
+  constexpr int kPT = kBM + 4;  // token-major partial row (features + pad)
+  const int ncols_ = (a.NT + 31) & ~31;
+  float* s_inv = reinterpret_cast<float*>(smem + ncols_ * kPT * 4);
+  int* s_pos = reinterpret_cast<int*>(s_inv + kMaxNT);
+  int64_t* s_cell = reinterpret_cast<int64_t*>(s_pos + kMaxNT);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = gridDim.x, split = blockIdx.x;  // cluster = the S splits of one tile
@@ -705,43 +839,41 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cluster_kernel(
     }
     __syncwarp();
   }
-  const int PSm = a.NT + 4;  // padded partial rows in shared memory (conflict-free v4)
+  // partial tiles token-major in shared memory: [NT tokens][kPT features]
+  // (padded row: the thread-per-feature writes and the warp-per-token reads
+  // are both bank-conflict free)
   const int ncols = (a.NT + 31) & ~31, nch = ncols / 32;
   const bool epi_warp = warp >= 2;
   const int quad = warp & 3, r = quad * 32 + lane, half = (warp - 2) >> 2;
-  const int ht = (threadIdx.x - 64) & 127;
-  float* stg = stg_all + (warp - 2) * 32 * kStg;
+  const int et = threadIdx.x - 64;  // 0..255
+  const int w8 = warp - 2;          // 0..7
+  float* part = reinterpret_cast<float*>(smem);
   if (epi_warp) {
     pdl_wait();
     mbar_wait(acc_full, 0);
     tc::fence_after();
     if (tr && threadIdx.x == 64) tr[3] = gtimer();
-    if (S > 1) {  // partial tile -> own shared memory (every MMA has completed: ring idle)
-      float* part = reinterpret_cast<float*>(smem) + r * PSm;
-      for (int c = half; c < nch; c += 2) {
-        float v[32];
-        tc::ld32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + c * 32, v);
+    // every MMA has completed: the ring is idle and holds the partial tile
+    for (int c = half; c < nch; c += 2) {
+      float v[32];
+      tc::ld32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + c * 32, v);
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (c * 32 + 4 * k < a.NT)
-            *reinterpret_cast<float4*>(part + c * 32 + 4 * k) =
-                make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-      }
+      for (int j = 0; j < 32; ++j) part[(c * 32 + j) * kPT + r] = v[j];
     }
   }
   if (tr && threadIdx.x == 64) tr[4] = gtimer();
-  if (S > 1) cluster_sync_all();  // every split's partial tile is in its shared memory
+  if (S > 1) {
+    cluster_sync_all();  // every split's partial tile is in its shared memory
+  } else {
+    __syncthreads();
+  }
   if (tr && threadIdx.x == 64) tr[5] = gtimer();
   if (epi_warp) {
-    const uint32_t my_part = smem_u32(smem) + static_cast<uint32_t>(r * PSm) * 4;
-    int k_mine = 0;
-    for (int c = (S > 1 ? split : 0); c < nch; c += S, ++k_mine) {
-      if ((k_mine & 1) != half) continue;
+    const uint32_t part_u = smem_u32(part);
+    for (int c = (S > 1 ? split : 0); c < nch; c += S) {  // chunk c -> split c mod S
       const int c0 = c * 32;
-      // per-token scalars of the chunk
-      if (ht < 32) {
-        const int tk = c0 + ht, t = tk;
-        s_amax[tk] = 0;
+      if (et < 32) {  // per-token scalars of the chunk
+        const int tk = c0 + et, t = tk;
         if (tk < a.NT && t < a.T) {
           if (epi.row_ss) {
             const unsigned long long rs =
@@ -758,38 +890,35 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cluster_kernel(
           if (epi.ss_zero && wt == 0) epi.ss_zero[t] = 0;
         }
       }
-      named_bar_sync(2 + half, 128);
-      if (tr && threadIdx.x == 64) tr[10] = gtimer();
-      float v[32];
-      if (S == 1) {
-        tc::ld32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + c0, v);
-      } else {
+      named_bar_sync(1, kEpiThreads);
+      // warp w8 reduces token rows c0 + w8 + 8i (i < 4): all S splits' rows
+      // loaded before the fixed-order sum (deterministic)
+      float4 acc[4];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = 0.f;
-        for (int q = 0; q < S; ++q) {  // fixed split order: deterministic
-          // unconditional: columns past NT read the padding / next row (ignored)
-          const uint32_t rq = dsmem_map(my_part + c0 * 4, q);
-          float4 x[8];
+      for (int i = 0; i < 4; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < S; ++q) {
+        float4 x[4];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) x[k] = dsmem_ld_f32x4(rq + 16 * k);
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t ad = part_u + static_cast<uint32_t>(((c0 + w8 + 8 * i) * kPT + 4 * lane) * 4);
+          x[i] = S > 1 ? dsmem_ld_f32x4(dsmem_map(ad, q))
+                       : *reinterpret_cast<const float4*>(smem + (ad - part_u));
+        }
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            v[4 * k] += x[k].x;
-            v[4 * k + 1] += x[k].y;
-            v[4 * k + 2] += x[k].z;
-            v[4 * k + 3] += x[k].w;
-          }
+        for (int i = 0; i < 4; ++i) {
+          acc[i].x += x[i].x;
+          acc[i].y += x[i].y;
+          acc[i].z += x[i].z;
+          acc[i].w += x[i].w;
         }
       }
-      if (tr && threadIdx.x == 64) tr[6] = gtimer() + static_cast<unsigned long long>(v[0] * 0.f);
-      epilogue_chunk(v, a, epi, wt, 0, c0, r, s_inv, s_pos, s_cell, s_amax, a.h_w, stg);
-      if (tr && threadIdx.x == 64) tr[8] = gtimer();
-      if (epi.argmax_out) {
-        named_bar_sync(2 + half, 128);
-        if (ht < 32 && c0 + ht < a.NT && c0 + ht < a.T)
-          atomicMax(reinterpret_cast<unsigned long long*>(epi.argmax_out) + c0 + ht,
-                    s_amax[c0 + ht]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int tk = c0 + w8 + 8 * i;
+        if (tk < a.NT && tk < a.T)  // warp-uniform
+          epilogue_tokrow(acc[i], a, epi, wt, tk, lane, s_inv, s_pos, s_cell);
       }
+      named_bar_sync(1, kEpiThreads);  // the chunk's scalars are no longer read
     }
   }
   if (tr && threadIdx.x == 64) tr[9] = gtimer();
@@ -955,14 +1084,42 @@ extern "C" int ds_gemm_stream(const void* X, const void* W, void* Y, int T, int 
             "stages=%d smem=%d\n", T, N, K, p.NT, p.n_tt, p.tiles,
             static_cast<long long>(p.total), p.P, p.stages, p.smem);
   // one token tile and fewer weight tiles than SMs: cluster split-K (the
-  // partials reduce through distributed shared memory)
+  // partials reduce through distributed shared memory).  The ring only has to
+  // hold the token-major partial tile at the end, so it could be ~110 KB and
+  // let two CTAs share an SM (DS_STREAM_CL_WIDE=0, A/B)
   static const int cl_env = getenv("DS_STREAM_CLUSTER") ? atoi(getenv("DS_STREAM_CLUSTER")) : 1;
-  int S = 0;
-  if (cl_env && p.n_tt == 1 && p.tiles < num_sms()) {
-    S = num_sms() / p.tiles;
-    if (S > 8) S = 8;
-    while (S > 1 && p.kt / S < 4) --S;
-    while (S > 1 && max_clusters(S, p.smem) < p.tiles) --S;
+  int S = 0, cl_stages = 0, cl_smem = 0;
+  // DS_STREAM_CL_BIG=1 (A/B): also one-token-tile shapes with up to two
+  // tiles per SM (gate_up at T <= 256: 224 tiles), unsplit, two shallow-ring
+  // CTAs per SM
+  static const int cl_big = getenv("DS_STREAM_CL_BIG") ? atoi(getenv("DS_STREAM_CL_BIG")) : 0;
+  const bool big = cl_big && p.n_tt == 1 && p.tiles >= num_sms() && p.tiles <= 2 * num_sms();
+  if (cl_env && p.n_tt == 1 && (p.tiles < num_sms() || big)) {
+    const int stage = kSlabA + p.NT * 128;
+    // partial tile + the epilogue scalars (s_inv, s_pos, s_cell) in the ring
+    const int64_t part = static_cast<int64_t>((p.NT + 31) & ~31) * (kBM + 4) * 4 +
+                         kMaxNT * (4 + 4 + 8);
+    const int fixed = 1024 + 256;  // alignment slack + barriers
+    cl_stages = static_cast<int>((part + stage - 1) / stage);
+    if (cl_stages < 3) cl_stages = 3;
+    cl_smem = fixed + cl_stages * stage;
+    // default: the deep ring of one CTA per SM - measured faster than two
+    // shallow-ring CTAs per SM (T=150: wo 15.9 vs 19.4 us, down 30.8 vs 39.2):
+    // the bytes in flight per SM matter more than overlapping the next
+    // kernel's prologue with this one's reduction
+    static const int cl_wide = getenv("DS_STREAM_CL_WIDE") ? atoi(getenv("DS_STREAM_CL_WIDE")) : 1;
+    if (cl_wide && !big) {
+      cl_stages = p.stages;
+      cl_smem = p.smem;
+    }
+    if (big) {
+      S = 1;
+    } else if (cl_smem <= kSmemMax) {
+      S = num_sms() / p.tiles;
+      if (S > 8) S = 8;
+      while (S > 1 && p.kt / S < 4) --S;
+      while (S > 1 && max_clusters(S, cl_smem) < p.tiles) --S;
+    }
   }
   StreamArgs a{};
   a.Y = Y;
@@ -998,11 +1155,13 @@ extern "C" int ds_gemm_stream(const void* X, const void* W, void* Y, int T, int 
       cl_attr = true;
     }
     if (getenv("DS_STREAM_VERBOSE"))
-      fprintf(stderr, "gemm_stream cluster mode: %d tiles x %d splits\n", p.tiles, S);
+      fprintf(stderr, "gemm_stream cluster mode: %d tiles x %d splits, %d stages, %d B smem\n",
+              p.tiles, S, cl_stages, cl_smem);
+    a.stages = cl_stages;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(S, p.tiles, 1);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = p.smem;
+    cfg.dynamicSmemBytes = cl_smem;
     cfg.stream = (cudaStream_t)stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
