@@ -130,7 +130,7 @@ def reference_turns(trace_name: str, repeats: int) -> dict:
             pend = list(hs)
             while pend:
                 core.step()
-                pend = [h for h in pend if not h.wait(timeout=0)]
+                pend = [h for h in pend if not h._event.is_set()]  # same poll as our arm
             dt = (time.perf_counter() - t0) * 1000.0
             for h in hs:
                 lat.append(dt)

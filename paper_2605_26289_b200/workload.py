@@ -128,7 +128,7 @@ def replay(core, trace: dict, wave_limit: int | None = None, max_iters: int = 20
             now = time.monotonic()
             still = []
             for h in pending:
-                if h.wait(timeout=0):
+                if h._event.is_set():  # non-blocking poll (wait(0) costs a lock round trip)
                     h.completed_at = h.completed_at or now
                 else:
                     still.append(h)
