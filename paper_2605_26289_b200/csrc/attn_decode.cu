@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     float* __restrict__ part_o, float* __restrict__ part_lse, int64_t head_stride,
     int* __restrict__ counters, const __grid_constant__ CUtensorMap tmk,
     const __grid_constant__ CUtensorMap tmv, const char* __restrict__ l2p, int64_t l2_bytes,
-    int last_merge, int n_stages, int early_trigger) {
+    int last_merge, int n_stages, int early_trigger, int one_pass) {
   K7_STAMP(6);
   const bool cluster_merge = max_splits <= kDecodeMaxCluster;  // launched with clusters
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -285,226 +285,400 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
         qpos[j][h] = rh < R ? en.past + rh / G : -1;
       }
     }
-    float o[8][NT][4];
-    float m_run[NT][2], l_run[NT][2];  // l_run: this lane's keys only (reduced at the end)
+    const int64_t base =
+        plan.n_splits > 1 && !cluster_merge ? attn_partial_base(entries, e, n_entries, nh, nkv, 1)
+                                            : 0;
+    if (one_pass) {
+      // ---- every tile of the split resident in the ring (short prefixes) ----
+      // One softmax pass: the warps' row maxima over all of the split's keys
+      // are exchanged first, so every warp's P is relative to the split's max;
+      // the P^T fragments are shared through shared memory and the PV product
+      // is split by head dimension (warp w: d rows [16w, 16w+16) over every
+      // key).  No per-warp O states exist, so there is no online rescaling and
+      // no 8-warp merge (the two-round merge was ~2.5 us of the ~8 us a
+      // one-tile launch spends after its dependency wait, tools/k7_trace.py).
+      float* mxs = cw;  // [8 warps][24 rows] row maxima (cw is free until the cluster merge)
+      const int kw = warp * kKeysPerWarp;
+      const int k_row = kw + (lane & 7) + ((lane >> 3) & 1) * 8, k_chunk = lane >> 4;
+      float s[kStages][NT][4];
+      float mx[NT][2];
   #pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      m_run[j][0] = m_run[j][1] = -INFINITY;
-      l_run[j][0] = l_run[j][1] = 0.f;
+      for (int j = 0; j < NT; ++j) mx[j][0] = mx[j][1] = -INFINITY;
   #pragma unroll
-      for (int i = 0; i < 8; ++i) o[i][j][0] = o[i][j][1] = o[i][j][2] = o[i][j][3] = 0.f;
-    }
-    const int kw = warp * kKeysPerWarp;
-    // per-lane ldmatrix rows: K (A, row-major) and V (A = V^T via .trans)
-    const int k_row = kw + (lane & 7) + ((lane >> 3) & 1) * 8, k_chunk = lane >> 4;
-    const int v_row = kw + (lane & 7) + ((lane >> 4) << 3), v_chunk = (lane >> 3) & 1;
-
-    for (int it = 0; it < ntiles; ++it) {
-      const int st = it % n_stages;
-      mbar_wait(&full[st], (it / n_stages) & 1);
-      if (it == 0) K7_STAMP(2);
-      const uint32_t ks_u = smem_u32(smem + st * kStageBytes), vs_u = ks_u + kHalfBytes;
-      float s[NT][4];
+      for (int it = 0; it < kStages; ++it) {
+        if (it >= ntiles) break;
+        mbar_wait(&full[it], 0);
+        if (it == 0) K7_STAMP(2);
+        const uint32_t ks_u = smem_u32(smem + it * kStageBytes);
   #pragma unroll
-      for (int j = 0; j < NT; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+        for (int j = 0; j < NT; ++j) s[it][j][0] = s[it][j][1] = s[it][j][2] = s[it][j][3] = 0.f;
   #pragma unroll
-      for (int kk = 0; kk < 8; kk += 2) {
-        uint32_t a0[4], a1[4];
-        ldsm_x4(a0[0], a0[1], a0[2], a0[3], ks_u + tswz(k_row, 2 * kk + k_chunk));
-        ldsm_x4(a1[0], a1[1], a1[2], a1[3], ks_u + tswz(k_row, 2 * kk + 2 + k_chunk));
+        for (int kk = 0; kk < 8; kk += 2) {
+          uint32_t a0[4], a1[4];
+          ldsm_x4(a0[0], a0[1], a0[2], a0[3], ks_u + tswz(k_row, 2 * kk + k_chunk));
+          ldsm_x4(a1[0], a1[1], a1[2], a1[3], ks_u + tswz(k_row, 2 * kk + 2 + k_chunk));
   #pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          uint32_t b[4];
-          if constexpr (kQSmem) {
-            ldsm_x4(b[0], b[1], b[2], b[3], smem_u32(qs) + qswz(8 * j + (lane & 7), 2 * kk + (lane >> 3)));
-          } else {
-            b[0] = qb[j][kk][0];
-            b[1] = qb[j][kk][1];
-            b[2] = qb[j][kk + 1][0];
-            b[3] = qb[j][kk + 1][1];
-          }
-          mma_bf16_16816(s[j], a0, b[0], b[1]);
-          mma_bf16_16816(s[j], a1, b[2], b[3]);
-        }
-      }
-      // s[j][q]: key kt + g (+8 for q >= 2), row 8j + 2t + (q & 1)
-      const int kt = k_begin + it * kTile + kw;
-      const bool need_mask = (kt + kKeysPerWarp > k_end) || (kt + kKeysPerWarp - 1 > en.past);
-      uint32_t pb[NT][2];
-  #pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        float mx[2] = {m_run[j][0], m_run[j][1]};
-  #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float v = s[j][q] * scale_log2;
-          if (need_mask) {
-            const int key = kt + g + ((q >> 1) << 3);
-            v = (key < k_end && key <= qpos[j][q & 1]) ? v : -INFINITY;
-          }
-          s[j][q] = v;
-          mx[q & 1] = fmaxf(mx[q & 1], v);
-        }
-        float alpha[2], mref[2];
-  #pragma unroll
-        for (int h = 0; h < 2; ++h) {  // row max over the warp's 16 keys (lanes sharing t)
-          mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 4));
-          mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 8));
-          mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 16));
-          mref[h] = mx[h] == -INFINITY ? 0.f : mx[h];
-          alpha[h] = fast_exp2(m_run[j][h] - mref[h]);
-          m_run[j][h] = mx[h];
-          l_run[j][h] *= alpha[h];
-        }
-        if (__any_sync(0xffffffffu, alpha[0] != 1.f || alpha[1] != 1.f)) {
-  #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            o[i][j][0] *= alpha[0];
-            o[i][j][1] *= alpha[1];
-            o[i][j][2] *= alpha[0];
-            o[i][j][3] *= alpha[1];
+          for (int j = 0; j < NT; ++j) {
+            uint32_t b[4];
+            if constexpr (kQSmem) {
+              ldsm_x4(b[0], b[1], b[2], b[3],
+                      smem_u32(qs) + qswz(8 * j + (lane & 7), 2 * kk + (lane >> 3)));
+            } else {
+              b[0] = qb[j][kk][0];
+              b[1] = qb[j][kk][1];
+              b[2] = qb[j][kk + 1][0];
+              b[3] = qb[j][kk + 1][1];
+            }
+            mma_bf16_16816(s[it][j], a0, b[0], b[1]);
+            mma_bf16_16816(s[it][j], a1, b[2], b[3]);
           }
         }
-        float p[4];
+        // s[it][j][q]: key kt + g (+8 for q >= 2), row 8j + 2t + (q & 1)
+        const int kt = k_begin + it * kTile + kw;
+        const bool need_mask = (kt + kKeysPerWarp > k_end) || (kt + kKeysPerWarp - 1 > en.past);
   #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          p[q] = fast_exp2(s[j][q] - mref[q & 1]);
-          l_run[j][q & 1] += p[q];
-        }
-        // (keys g | g+8, rows 2t, 2t+1) -> transposed: (keys 2t, 2t+1 | +8, row g)
-        pb[j][0] = movm_t(pack_bf16(p[0], p[1]));
-        pb[j][1] = movm_t(pack_bf16(p[2], p[3]));
-      }
+        for (int j = 0; j < NT; ++j)
   #pragma unroll
-      for (int i = 0; i < 8; ++i) {  // d rows [16i, 16i+16)
-        uint32_t a[4];
-        ldsm_x4_t(a[0], a[1], a[2], a[3], vs_u + tswz(v_row, 2 * i + v_chunk));
-  #pragma unroll
-        for (int j = 0; j < NT; ++j) mma_bf16_16816(o[i][j], a, pb[j][0], pb[j][1]);
-      }
-      // generic-proxy reads of the stage complete before the producer's TMA
-      // (async proxy) refills it (measured necessary in the skinny GEMM ring)
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
-    }
-    named_bar_sync(1, kConsumers * 32);  // all consumers done with the ring
-    K7_STAMP(3);
-
-    // ---- merge the 8 warps' states (ring memory is free now) ----
-    // Two rounds through a [4][24][132] buffer (fits the one-stage ring):
-    // warps 4-7 publish (m, l, O), warps 0-3 fold their partner's state into
-    // registers and publish the result; then per-row weights are computed once
-    // and every output element is a 4-term dot product (independent loads).
-    constexpr int kHalfW = kConsumers / 2;
-    float* osm = reinterpret_cast<float*>(smem);             // [4][24][132]
-    float* msm = osm + kHalfW * kMaxRows * kOsmStride;       // [4][24]
-    float* lsm = msm + kHalfW * kMaxRows;                    // [4][24]
-    float* wsm = lsm + kHalfW * kMaxRows;                    // [24][4] row weights
-    float* rlse = wsm + kMaxRows * kHalfW;                   // [24] row log2-sum-exp
-    const int slotw = warp & (kHalfW - 1);
-  #pragma unroll
-    for (int j = 0; j < NT; ++j)
-  #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float l = l_run[j][h];
-        l += __shfl_xor_sync(0xffffffffu, l, 4);
-        l += __shfl_xor_sync(0xffffffffu, l, 8);
-        l += __shfl_xor_sync(0xffffffffu, l, 16);
-        l_run[j][h] = l;  // the warp's row total
-      }
-    auto publish = [&]() {
-  #pragma unroll
-      for (int j = 0; j < NT; ++j) {
-  #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int r = 8 * j + 2 * t + h;
-          if (g == 0) {
-            msm[slotw * kMaxRows + r] = m_run[j][h];
-            lsm[slotw * kMaxRows + r] = l_run[j][h];
+          for (int q = 0; q < 4; ++q) {
+            float v = s[it][j][q] * scale_log2;
+            if (need_mask) {
+              const int key = kt + g + ((q >> 1) << 3);
+              v = (key < k_end && key <= qpos[j][q & 1]) ? v : -INFINITY;
+            }
+            s[it][j][q] = v;
+            mx[j][q & 1] = fmaxf(mx[j][q & 1], v);
           }
-        }
-  #pragma unroll
-        for (int i = 0; i < 8; ++i)
-  #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            osm[(slotw * kMaxRows + 8 * j + 2 * t + (q & 1)) * kOsmStride + 16 * i + g +
-                ((q >> 1) << 3)] = o[i][j][q];
       }
-    };
-    if (warp >= kHalfW) publish();
-    named_bar_sync(1, kConsumers * 32);
-    if (warp < kHalfW) {  // fold the partner warp (warp + 4): same fragment positions
+  #pragma unroll
+      for (int j = 0; j < NT; ++j)
+  #pragma unroll
+        for (int h = 0; h < 2; ++h) {  // the warp's row max (lanes sharing t)
+          float m = mx[j][h];
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+          if (g == 0) mxs[warp * kMaxRows + 8 * j + 2 * t + h] = m;
+        }
+      named_bar_sync(1, kConsumers * 32);  // maxima published; every warp is done with K
+      // the K halves of the stages are free now: each tile's P^T fragments go
+      // into its own K half, the row sums after stage 0's fragments
+      constexpr int kPbsBytes = kConsumers * 3 * 32 * 8;  // [8 warps][NT <= 3][32 lanes] uint2
+      float* lsm = reinterpret_cast<float*>(smem + kPbsBytes);  // [8][24]
+      float mref[NT][2];
   #pragma unroll
       for (int j = 0; j < NT; ++j)
   #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int r = 8 * j + 2 * t + h;
-          const float mb = msm[slotw * kMaxRows + r], lb = lsm[slotw * kMaxRows + r];
-          const float ma = m_run[j][h];
-          const float mm = fmaxf(ma, mb);
-          const float mref = mm == -INFINITY ? 0.f : mm;
-          const float sa = fast_exp2(ma - mref), sb = fast_exp2(mb - mref);
-          m_run[j][h] = mm;
-          l_run[j][h] = l_run[j][h] * sa + lb * sb;
+          float m = -INFINITY;
   #pragma unroll
-          for (int i = 0; i < 8; ++i)
-  #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if ((q & 1) == h) {
-                const float ob = osm[(slotw * kMaxRows + r) * kOsmStride + 16 * i + g +
-                                     ((q >> 1) << 3)];
-                o[i][j][q] = o[i][j][q] * sa + ob * sb;
-              }
+          for (int w = 0; w < kConsumers; ++w) m = fmaxf(m, mxs[w * kMaxRows + r]);
+          mref[j][h] = m == -INFINITY ? 0.f : m;
         }
-    }
-    named_bar_sync(1, kConsumers * 32);
-    if (warp < kHalfW) publish();
-    named_bar_sync(1, kConsumers * 32);
-    if (tid < R) {
-      float mv[kHalfW], lv[kHalfW];
+      float l[NT][2];
   #pragma unroll
-      for (int w = 0; w < kHalfW; ++w) {
-        mv[w] = msm[w * kMaxRows + tid];
-        lv[w] = lsm[w * kMaxRows + tid];
+      for (int j = 0; j < NT; ++j) l[j][0] = l[j][1] = 0.f;
+  #pragma unroll
+      for (int it = 0; it < kStages; ++it) {
+        if (it >= ntiles) break;
+        uint2* pbs = reinterpret_cast<uint2*>(smem + it * kStageBytes);
+  #pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          float p[4];
+  #pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            p[q] = fast_exp2(s[it][j][q] - mref[j][q & 1]);
+            l[j][q & 1] += p[q];
+          }
+          // (keys g | g+8, rows 2t, 2t+1) -> transposed: (keys 2t, 2t+1 | +8, row g)
+          pbs[(warp * NT + j) * 32 + lane] =
+              make_uint2(movm_t(pack_bf16(p[0], p[1])), movm_t(pack_bf16(p[2], p[3])));
+        }
       }
-      float mm = -INFINITY;
   #pragma unroll
-      for (int w = 0; w < kHalfW; ++w) mm = fmaxf(mm, mv[w]);
-      const float mref = mm == -INFINITY ? 0.f : mm;
-      float L = 0.f;
+      for (int j = 0; j < NT; ++j)
   #pragma unroll
-      for (int w = 0; w < kHalfW; ++w) {
-        mv[w] = fast_exp2(mv[w] - mref);
-        L += lv[w] * mv[w];
+        for (int h = 0; h < 2; ++h) {
+          float v = l[j][h];
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 16);
+          if (g == 0) lsm[warp * kMaxRows + 8 * j + 2 * t + h] = v;
+        }
+      named_bar_sync(1, kConsumers * 32);  // every warp's P^T and row sums published
+      float o[NT][4];
+  #pragma unroll
+      for (int j = 0; j < NT; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+      const int v_row = (lane & 7) + ((lane >> 4) << 3), v_chunk = (lane >> 3) & 1;
+  #pragma unroll
+      for (int it = 0; it < kStages; ++it) {
+        if (it >= ntiles) break;
+        const uint32_t vs_u = smem_u32(smem + it * kStageBytes) + kHalfBytes;
+        const uint2* pbs = reinterpret_cast<const uint2*>(smem + it * kStageBytes);
+  #pragma unroll
+        for (int kc = 0; kc < kConsumers; ++kc) {  // keys [16kc, 16kc+16) of the tile
+          uint32_t a[4];
+          ldsm_x4_t(a[0], a[1], a[2], a[3], vs_u + tswz(16 * kc + v_row, 2 * warp + v_chunk));
+  #pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const uint2 b2 = pbs[(kc * NT + j) * 32 + lane];
+            mma_bf16_16816(o[j], a, b2.x, b2.y);
+          }
+        }
       }
-      const float inv = L > 0.f ? 1.f / L : 0.f;
+      K7_STAMP(3);
+      // o[j][q]: d = 16w + g (+8 for q >= 2), row 8j + 2t + (q & 1)
   #pragma unroll
-      for (int w = 0; w < kHalfW; ++w) wsm[tid * kHalfW + w] = mv[w] * inv;
-      rlse[tid] = L > 0.f ? mm + __log2f(L) : -INFINITY;
-    }
-    named_bar_sync(1, kConsumers * 32);
-    const int64_t base =
-        plan.n_splits > 1 && !cluster_merge ? attn_partial_base(entries, e, n_entries, nh, nkv, 1)
-                                            : 0;
-    for (int idx = tid; idx < R * kD; idx += kConsumers * 32) {
-      const int r = idx / kD, d = idx - r * kD;
-      float ov[kHalfW];
+      for (int j = 0; j < NT; ++j) {
+        float inv[2], lse[2];
   #pragma unroll
-      for (int w = 0; w < kHalfW; ++w) ov[w] = osm[(w * kMaxRows + r) * kOsmStride + d];
-      float val = 0.f;
+        for (int h = 0; h < 2; ++h) {
+          const int r = 8 * j + 2 * t + h;
+          float L = 0.f;
   #pragma unroll
-      for (int w = 0; w < kHalfW; ++w) val += wsm[r * kHalfW + w] * ov[w];
-      if (plan.n_splits == 1) {  // no split: write the row directly
-        const int ti = r / G, gi = r - ti * G;
-        out[static_cast<int64_t>(en.q_start + ti) * nh * kD + (kh * G + gi) * kD + d] =
-            __float2bfloat16_rn(val);
-      } else if (cluster_merge) {  // this split's normalised rows -> its cluster buffer
-        cval[r * kD + d] = val;
-        if (d == 0) clse[r] = rlse[r];
-      } else {  // -> global partials
-        const int64_t slot = (base + static_cast<int64_t>(split) * R + r) * nkv + kh;
-        part_o[slot * kD + d] = val;
-        if (d == 0) part_lse[slot] = rlse[r];
+          for (int w = 0; w < kConsumers; ++w) L += lsm[w * kMaxRows + r];
+          inv[h] = L > 0.f ? 1.f / L : 0.f;
+          lse[h] = L > 0.f ? mref[j][h] + __log2f(L) : -INFINITY;
+        }
+  #pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = 8 * j + 2 * t + (q & 1), d = 16 * warp + g + ((q >> 1) << 3);
+          if (r >= R) continue;
+          const float val = o[j][q] * inv[q & 1];
+          const bool lead = warp == 0 && g == 0 && q < 2;  // one writer per row's lse
+          if (plan.n_splits == 1) {
+            const int ti = r / G, gi = r - ti * G;
+            out[static_cast<int64_t>(en.q_start + ti) * nh * kD + (kh * G + gi) * kD + d] =
+                __float2bfloat16_rn(val);
+          } else if (cluster_merge) {
+            cval[r * kD + d] = val;
+            if (lead) clse[r] = lse[q & 1];
+          } else {
+            const int64_t slot = (base + static_cast<int64_t>(split) * R + r) * nkv + kh;
+            part_o[slot * kD + d] = val;
+            if (lead) part_lse[slot] = lse[q & 1];
+          }
+        }
+      }
+    } else {
+      float o[8][NT][4];
+      float m_run[NT][2], l_run[NT][2];  // l_run: this lane's keys only (reduced at the end)
+    #pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        m_run[j][0] = m_run[j][1] = -INFINITY;
+        l_run[j][0] = l_run[j][1] = 0.f;
+    #pragma unroll
+        for (int i = 0; i < 8; ++i) o[i][j][0] = o[i][j][1] = o[i][j][2] = o[i][j][3] = 0.f;
+      }
+      const int kw = warp * kKeysPerWarp;
+      // per-lane ldmatrix rows: K (A, row-major) and V (A = V^T via .trans)
+      const int k_row = kw + (lane & 7) + ((lane >> 3) & 1) * 8, k_chunk = lane >> 4;
+      const int v_row = kw + (lane & 7) + ((lane >> 4) << 3), v_chunk = (lane >> 3) & 1;
+
+      for (int it = 0; it < ntiles; ++it) {
+        const int st = it % n_stages;
+        mbar_wait(&full[st], (it / n_stages) & 1);
+        if (it == 0) K7_STAMP(2);
+        const uint32_t ks_u = smem_u32(smem + st * kStageBytes), vs_u = ks_u + kHalfBytes;
+        float s[NT][4];
+    #pragma unroll
+        for (int j = 0; j < NT; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+    #pragma unroll
+        for (int kk = 0; kk < 8; kk += 2) {
+          uint32_t a0[4], a1[4];
+          ldsm_x4(a0[0], a0[1], a0[2], a0[3], ks_u + tswz(k_row, 2 * kk + k_chunk));
+          ldsm_x4(a1[0], a1[1], a1[2], a1[3], ks_u + tswz(k_row, 2 * kk + 2 + k_chunk));
+    #pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            uint32_t b[4];
+            if constexpr (kQSmem) {
+              ldsm_x4(b[0], b[1], b[2], b[3], smem_u32(qs) + qswz(8 * j + (lane & 7), 2 * kk + (lane >> 3)));
+            } else {
+              b[0] = qb[j][kk][0];
+              b[1] = qb[j][kk][1];
+              b[2] = qb[j][kk + 1][0];
+              b[3] = qb[j][kk + 1][1];
+            }
+            mma_bf16_16816(s[j], a0, b[0], b[1]);
+            mma_bf16_16816(s[j], a1, b[2], b[3]);
+          }
+        }
+        // s[j][q]: key kt + g (+8 for q >= 2), row 8j + 2t + (q & 1)
+        const int kt = k_begin + it * kTile + kw;
+        const bool need_mask = (kt + kKeysPerWarp > k_end) || (kt + kKeysPerWarp - 1 > en.past);
+        uint32_t pb[NT][2];
+    #pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          float mx[2] = {m_run[j][0], m_run[j][1]};
+    #pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float v = s[j][q] * scale_log2;
+            if (need_mask) {
+              const int key = kt + g + ((q >> 1) << 3);
+              v = (key < k_end && key <= qpos[j][q & 1]) ? v : -INFINITY;
+            }
+            s[j][q] = v;
+            mx[q & 1] = fmaxf(mx[q & 1], v);
+          }
+          float alpha[2], mref[2];
+    #pragma unroll
+          for (int h = 0; h < 2; ++h) {  // row max over the warp's 16 keys (lanes sharing t)
+            mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 4));
+            mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 8));
+            mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 16));
+            mref[h] = mx[h] == -INFINITY ? 0.f : mx[h];
+            alpha[h] = fast_exp2(m_run[j][h] - mref[h]);
+            m_run[j][h] = mx[h];
+            l_run[j][h] *= alpha[h];
+          }
+          if (__any_sync(0xffffffffu, alpha[0] != 1.f || alpha[1] != 1.f)) {
+    #pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              o[i][j][0] *= alpha[0];
+              o[i][j][1] *= alpha[1];
+              o[i][j][2] *= alpha[0];
+              o[i][j][3] *= alpha[1];
+            }
+          }
+          float p[4];
+    #pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            p[q] = fast_exp2(s[j][q] - mref[q & 1]);
+            l_run[j][q & 1] += p[q];
+          }
+          // (keys g | g+8, rows 2t, 2t+1) -> transposed: (keys 2t, 2t+1 | +8, row g)
+          pb[j][0] = movm_t(pack_bf16(p[0], p[1]));
+          pb[j][1] = movm_t(pack_bf16(p[2], p[3]));
+        }
+    #pragma unroll
+        for (int i = 0; i < 8; ++i) {  // d rows [16i, 16i+16)
+          uint32_t a[4];
+          ldsm_x4_t(a[0], a[1], a[2], a[3], vs_u + tswz(v_row, 2 * i + v_chunk));
+    #pragma unroll
+          for (int j = 0; j < NT; ++j) mma_bf16_16816(o[i][j], a, pb[j][0], pb[j][1]);
+        }
+        // generic-proxy reads of the stage complete before the producer's TMA
+        // (async proxy) refills it (measured necessary in the skinny GEMM ring)
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+      }
+      named_bar_sync(1, kConsumers * 32);  // all consumers done with the ring
+      K7_STAMP(3);
+
+      // ---- merge the 8 warps' states (ring memory is free now) ----
+      // Two rounds through a [4][24][132] buffer (fits the one-stage ring):
+      // warps 4-7 publish (m, l, O), warps 0-3 fold their partner's state into
+      // registers and publish the result; then per-row weights are computed once
+      // and every output element is a 4-term dot product (independent loads).
+      constexpr int kHalfW = kConsumers / 2;
+      float* osm = reinterpret_cast<float*>(smem);             // [4][24][132]
+      float* msm = osm + kHalfW * kMaxRows * kOsmStride;       // [4][24]
+      float* lsm = msm + kHalfW * kMaxRows;                    // [4][24]
+      float* wsm = lsm + kHalfW * kMaxRows;                    // [24][4] row weights
+      float* rlse = wsm + kMaxRows * kHalfW;                   // [24] row log2-sum-exp
+      const int slotw = warp & (kHalfW - 1);
+    #pragma unroll
+      for (int j = 0; j < NT; ++j)
+    #pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float l = l_run[j][h];
+          l += __shfl_xor_sync(0xffffffffu, l, 4);
+          l += __shfl_xor_sync(0xffffffffu, l, 8);
+          l += __shfl_xor_sync(0xffffffffu, l, 16);
+          l_run[j][h] = l;  // the warp's row total
+        }
+      auto publish = [&]() {
+    #pragma unroll
+        for (int j = 0; j < NT; ++j) {
+    #pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = 8 * j + 2 * t + h;
+            if (g == 0) {
+              msm[slotw * kMaxRows + r] = m_run[j][h];
+              lsm[slotw * kMaxRows + r] = l_run[j][h];
+            }
+          }
+    #pragma unroll
+          for (int i = 0; i < 8; ++i)
+    #pragma unroll
+            for (int q = 0; q < 4; ++q)
+              osm[(slotw * kMaxRows + 8 * j + 2 * t + (q & 1)) * kOsmStride + 16 * i + g +
+                  ((q >> 1) << 3)] = o[i][j][q];
+        }
+      };
+      if (warp >= kHalfW) publish();
+      named_bar_sync(1, kConsumers * 32);
+      if (warp < kHalfW) {  // fold the partner warp (warp + 4): same fragment positions
+    #pragma unroll
+        for (int j = 0; j < NT; ++j)
+    #pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = 8 * j + 2 * t + h;
+            const float mb = msm[slotw * kMaxRows + r], lb = lsm[slotw * kMaxRows + r];
+            const float ma = m_run[j][h];
+            const float mm = fmaxf(ma, mb);
+            const float mref = mm == -INFINITY ? 0.f : mm;
+            const float sa = fast_exp2(ma - mref), sb = fast_exp2(mb - mref);
+            m_run[j][h] = mm;
+            l_run[j][h] = l_run[j][h] * sa + lb * sb;
+    #pragma unroll
+            for (int i = 0; i < 8; ++i)
+    #pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if ((q & 1) == h) {
+                  const float ob = osm[(slotw * kMaxRows + r) * kOsmStride + 16 * i + g +
+                                       ((q >> 1) << 3)];
+                  o[i][j][q] = o[i][j][q] * sa + ob * sb;
+                }
+          }
+      }
+      named_bar_sync(1, kConsumers * 32);
+      if (warp < kHalfW) publish();
+      named_bar_sync(1, kConsumers * 32);
+      if (tid < R) {
+        float mv[kHalfW], lv[kHalfW];
+    #pragma unroll
+        for (int w = 0; w < kHalfW; ++w) {
+          mv[w] = msm[w * kMaxRows + tid];
+          lv[w] = lsm[w * kMaxRows + tid];
+        }
+        float mm = -INFINITY;
+    #pragma unroll
+        for (int w = 0; w < kHalfW; ++w) mm = fmaxf(mm, mv[w]);
+        const float mref = mm == -INFINITY ? 0.f : mm;
+        float L = 0.f;
+    #pragma unroll
+        for (int w = 0; w < kHalfW; ++w) {
+          mv[w] = fast_exp2(mv[w] - mref);
+          L += lv[w] * mv[w];
+        }
+        const float inv = L > 0.f ? 1.f / L : 0.f;
+    #pragma unroll
+        for (int w = 0; w < kHalfW; ++w) wsm[tid * kHalfW + w] = mv[w] * inv;
+        rlse[tid] = L > 0.f ? mm + __log2f(L) : -INFINITY;
+      }
+      named_bar_sync(1, kConsumers * 32);
+      for (int idx = tid; idx < R * kD; idx += kConsumers * 32) {
+        const int r = idx / kD, d = idx - r * kD;
+        float ov[kHalfW];
+    #pragma unroll
+        for (int w = 0; w < kHalfW; ++w) ov[w] = osm[(w * kMaxRows + r) * kOsmStride + d];
+        float val = 0.f;
+    #pragma unroll
+        for (int w = 0; w < kHalfW; ++w) val += wsm[r * kHalfW + w] * ov[w];
+        if (plan.n_splits == 1) {  // no split: write the row directly
+          const int ti = r / G, gi = r - ti * G;
+          out[static_cast<int64_t>(en.q_start + ti) * nh * kD + (kh * G + gi) * kD + d] =
+              __float2bfloat16_rn(val);
+        } else if (cluster_merge) {  // this split's normalised rows -> its cluster buffer
+          cval[r * kD + d] = val;
+          if (d == 0) clse[r] = rlse[r];
+        } else {  // -> global partials
+          const int64_t slot = (base + static_cast<int64_t>(split) * R + r) * nkv + kh;
+          part_o[slot * kD + d] = val;
+          if (d == 0) part_lse[slot] = rlse[r];
+        }
       }
     }
     if (plan.n_splits > 1 && !cluster_merge && last_merge)  // last split to arrive merges
@@ -577,6 +751,9 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
   // next projection's
   static const int early_env = getenv("DS_K7_EARLY") ? atoi(getenv("DS_K7_EARLY")) : 1;
   const int early = (max_splits > kDecodeMaxCluster && !last_merge) || (early_env && n_stages == 1);
+  static const int one_pass_env = getenv("DS_K7_ONEPASS") ? atoi(getenv("DS_K7_ONEPASS")) : 1;
+  // every split's tiles fit the ring at once: the one-pass softmax (no refills)
+  const int one_pass = one_pass_env && max_split_len <= kStages * kTile;
   const char* l2p = static_cast<const char*>(g_l2_ptr);
   const int64_t l2_bytes = g_l2_bytes;
   g_l2_ptr = nullptr;
@@ -596,14 +773,14 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
                          max_splits, static_cast<const __nv_bfloat16*>(k_pool),
                          static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv,
                          sl2, static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride,
-                         counters, *tk, *tv, l2p, l2_bytes, last_merge, n_stages, early);
+                         counters, *tk, *tv, l2p, l2_bytes, last_merge, n_stages, early, one_pass);
   else
     launch_pdl(kern, grid, dim3(kThreads), smem, stream, static_cast<const __nv_bfloat16*>(qkv),
                stride, entries_dev, n_entries, max_splits,
                static_cast<const __nv_bfloat16*>(k_pool),
                static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv, sl2,
                static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride, counters, *tk,
-               *tv, l2p, l2_bytes, last_merge, n_stages, early);
+               *tv, l2p, l2_bytes, last_merge, n_stages, early, one_pass);
   return (int)cudaGetLastError();
 }
 
