@@ -170,7 +170,8 @@ typedef struct {
   int32_t q_len;     /* batch rows */
   int32_t q_start;   /* first packed row */
   int32_t kind;      /* DS_ENTRY_* */
-  int32_t n_draft;   /* k for VERIFY */
+  int32_t n_draft;   /* k for VERIFY; -1 on the PREFILL chunk that ends a prompt: the
+                        next proposal (ds_forward_args.next_*) follows its sampled token */
   int32_t out_start; /* first output (sampled) row */
   int32_t n_out;     /* sampled rows: 1 (prefill/decode) or k+1 (verify) */
   uint64_t hash_in;  /* FNV-1a64 of the sequence's first `past` tokens */
@@ -307,6 +308,11 @@ typedef struct {
    * before the launch.  Y may then be NULL: no product is stored (needs
    * y_f32 = 1, accumulate = 0, no other fusion). */
   uint64_t* argmax_out;
+  /* bytes every CTA pulls into L2 (its equal share) BEFORE the dependency
+   * wait - for a projection launched early beside a latency-bound kernel
+   * (the decode attention), whose HBM would otherwise idle (0 = none) */
+  const void* l2_pre;
+  int64_t l2_pre_bytes;
 } ds_skinny_epi;
 
 int ds_gemm_skinny_ex(const void* X, const void* W, void* Y, int M, int N, int K, int y_f32,

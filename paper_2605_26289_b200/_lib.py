@@ -60,7 +60,7 @@ class SkinnyEpi(ctypes.Structure):
                 ("pos2cell", c_vp), ("pos_stride", c_i64), ("rope_cos", c_vp),
                 ("rope_sin", c_vp), ("k_pool_l", c_vp), ("v_pool_l", c_vp),
                 ("kv_head_stride", c_i64), ("l2_next", c_vp), ("l2_next_bytes", c_i64),
-                ("argmax_out", c_vp)]
+                ("argmax_out", c_vp), ("l2_pre", c_vp), ("l2_pre_bytes", c_i64)]
 
 
 class ForwardArgs(ctypes.Structure):

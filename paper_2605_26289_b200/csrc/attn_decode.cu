@@ -91,18 +91,16 @@ constexpr int kOsmStride = kD + 4;  // padded [warp][row] stride of the merge bu
 
 // one-shot hint from the forward runtime: bytes to pull into L2 while the
 // attention runs (consumed by the next decode launch on this thread)
-static thread_local const void* g_l2_ptr = nullptr;
-static thread_local int64_t g_l2_bytes = 0;
-void set_attn_l2_prefetch(const void* ptr, int64_t bytes) {
-  g_l2_ptr = ptr;
-  g_l2_bytes = bytes;
+static thread_local L2Hint g_l2 = {{nullptr, nullptr}, {0, 0}};
+void set_attn_l2_prefetch(const void* ptr, int64_t bytes, const void* ptr2, int64_t bytes2) {
+  g_l2 = L2Hint{{static_cast<const char*>(ptr), static_cast<const char*>(ptr2)}, {bytes, bytes2}};
 }
 
 int launch_attn_decode_tc(const ds_entry* entries_dev, int n_entries, const void* qkv,
                           const void* k_pool, const void* v_pool, int64_t head_stride,
                           const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv,
                           int max_splits, float scale, void* out, float* part_o, float* part_lse,
-                          const void* l2p, int64_t l2_bytes, cudaStream_t stream);
+                          const L2Hint& l2, cudaStream_t stream);
 
 constexpr int kBarBytes = 64;                                     // full/empty mbarriers
 constexpr int kMergeBytes = (kMaxRows * kD + kMaxRows + kMaxRows * 8) * 4;  // cval/clse/cw
@@ -118,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     int64_t pos_stride, int nh, int nkv, float scale_log2, __nv_bfloat16* __restrict__ out,
     float* __restrict__ part_o, float* __restrict__ part_lse, int64_t head_stride,
     int* __restrict__ counters, const __grid_constant__ CUtensorMap tmk,
-    const __grid_constant__ CUtensorMap tmv, const char* __restrict__ l2p, int64_t l2_bytes,
+    const __grid_constant__ CUtensorMap tmv, const L2Hint l2,
     int last_merge, int n_stages, int early_trigger, int one_pass) {
   K7_STAMP(6);
   const bool cluster_merge = max_splits <= kDecodeMaxCluster;  // launched with clusters
@@ -229,18 +227,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     }
     if (!waited) pdl_wait();
     if (early_trigger) pdl_trigger();  // combine kernel / co-resident projection
-    if (l2p && lane == 0) {  // this CTA's share of the next projection's weights -> L2
-      const int64_t n_cta = static_cast<int64_t>(gridDim.y) * gridDim.z;
-      const int64_t share = ((l2_bytes + n_cta - 1) / n_cta + 15) & ~15ll;
-      const int64_t beg = share * (blockIdx.z * gridDim.y + blockIdx.y);
-      const int64_t lim = l2_bytes & ~15ll;
-      const int64_t end = beg + share < lim ? beg + share : lim;
-      for (int64_t off = beg; off < end; off += 32768) {
-        const uint32_t n = static_cast<uint32_t>(end - off < 32768 ? end - off : 32768);
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(l2p + off), "r"(n)
-                     : "memory");
-      }
-    }
+    if (lane == 0)  // this CTA's share of the next projections' weights -> L2
+      l2_prefetch_share(l2, blockIdx.z * gridDim.y + blockIdx.y,
+                        static_cast<int64_t>(gridDim.y) * gridDim.z);
   } else {
     // ================= consumers =================
     K7_STAMP(0);
@@ -754,16 +743,14 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
   static const int one_pass_env = getenv("DS_K7_ONEPASS") ? atoi(getenv("DS_K7_ONEPASS")) : 1;
   // every split's tiles fit the ring at once: the one-pass softmax (no refills)
   const int one_pass = one_pass_env && max_split_len <= kStages * kTile;
-  const char* l2p = static_cast<const char*>(g_l2_ptr);
-  const int64_t l2_bytes = g_l2_bytes;
-  g_l2_ptr = nullptr;
-  g_l2_bytes = 0;
+  const L2Hint l2 = g_l2;
+  g_l2 = L2Hint{{nullptr, nullptr}, {0, 0}};
   // more than 8 rows over a long prefix: the legacy HMMA pipe would bound the
   // mma.sync kernel below the HBM rate - run the tcgen05 variant
   if (max_R > kDecodeTcMinRows && max_kv >= kDecodeTcMinKeys)
     return launch_attn_decode_tc(entries_dev, n_entries, qkv, k_pool, v_pool, head_stride,
                                  pos2cell, pos_stride, nh, nkv, max_splits, scale, out, part_o,
-                                 part_lse, l2p, l2_bytes, stream);
+                                 part_lse, l2, stream);
   auto kern = max_R <= 8 ? attn_decode_kernel<1>
               : max_R <= 16 ? attn_decode_kernel<2>
                             : attn_decode_kernel<3>;
@@ -773,14 +760,14 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
                          max_splits, static_cast<const __nv_bfloat16*>(k_pool),
                          static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv,
                          sl2, static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride,
-                         counters, *tk, *tv, l2p, l2_bytes, last_merge, n_stages, early, one_pass);
+                         counters, *tk, *tv, l2, last_merge, n_stages, early, one_pass);
   else
     launch_pdl(kern, grid, dim3(kThreads), smem, stream, static_cast<const __nv_bfloat16*>(qkv),
                stride, entries_dev, n_entries, max_splits,
                static_cast<const __nv_bfloat16*>(k_pool),
                static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv, sl2,
                static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride, counters, *tk,
-               *tv, l2p, l2_bytes, last_merge, n_stages, early, one_pass);
+               *tv, l2, last_merge, n_stages, early, one_pass);
   return (int)cudaGetLastError();
 }
 

@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
     int64_t pos_stride, int nh, int nkv, float scale_log2, __nv_bfloat16* __restrict__ out,
     float* __restrict__ part_o, float* __restrict__ part_lse, int64_t head_stride,
     const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
-    const char* __restrict__ l2p, int64_t l2_bytes) {
+    const L2Hint l2) {
   TC_STAMP(6);
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // SW128 alignment
@@ -223,18 +223,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
     if (ntiles > 0) load_v(ntiles - 1, prev);
     if (!waited) pdl_wait();
     if (!cluster_merge) pdl_trigger();
-    if (l2p && lane == 0) {  // this CTA's share of the next projection's weights -> L2
-      const int64_t n_cta = static_cast<int64_t>(gridDim.y) * gridDim.z;
-      const int64_t share = ((l2_bytes + n_cta - 1) / n_cta + 15) & ~15ll;
-      const int64_t beg = share * (blockIdx.z * gridDim.y + blockIdx.y);
-      const int64_t lim = l2_bytes & ~15ll;
-      const int64_t end = beg + share < lim ? beg + share : lim;
-      for (int64_t off = beg; off < end; off += 32768) {
-        const uint32_t n = static_cast<uint32_t>(end - off < 32768 ? end - off : 32768);
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(l2p + off), "r"(n)
-                     : "memory");
-      }
-    }
+    if (lane == 0)  // this CTA's share of the next projections' weights -> L2
+      l2_prefetch_share(l2, blockIdx.z * gridDim.y + blockIdx.y,
+                        static_cast<int64_t>(gridDim.y) * gridDim.z);
   } else if (warp == 2) {
     // ======================= MMA issuer =======================
     if (lane == 0 && ntiles > 0) {
@@ -428,7 +419,7 @@ int launch_attn_decode_tc(const ds_entry* entries_dev, int n_entries, const void
                           const void* k_pool, const void* v_pool, int64_t head_stride,
                           const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv,
                           int max_splits, float scale, void* out, float* part_o, float* part_lse,
-                          const void* l2p, int64_t l2_bytes, cudaStream_t stream) {
+                          const L2Hint& l2, cudaStream_t stream) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -447,14 +438,14 @@ int launch_attn_decode_tc(const ds_entry* entries_dev, int n_entries, const void
                          n_entries, max_splits, static_cast<const __nv_bfloat16*>(k_pool),
                          static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv,
                          sl2, static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride,
-                         *tk, *tv, static_cast<const char*>(l2p), l2_bytes);
+                         *tk, *tv, l2);
   else
     launch_pdl(attn_decode_tc_kernel, grid, dim3(kThreads), kSmemBytes, stream,
                static_cast<const __nv_bfloat16*>(qkv), stride, entries_dev, n_entries, max_splits,
                static_cast<const __nv_bfloat16*>(k_pool),
                static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv, sl2,
                static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride, *tk, *tv,
-               static_cast<const char*>(l2p), l2_bytes);
+               l2);
   return (int)cudaGetLastError();
 }
 

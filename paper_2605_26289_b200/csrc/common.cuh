@@ -174,6 +174,30 @@ namespace ds {
 DS_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 DS_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
+// Up to two byte ranges to pull into L2 while a latency-bound kernel leaves
+// HBM idle (the attention pulls the next projections' weights): CTA `cta` of
+// `n_cta` prefetches its equal share of the two ranges laid end to end.
+struct L2Hint {
+  const char* p[2];
+  int64_t n[2];
+};
+DS_DEVICE void l2_prefetch_share(const L2Hint& h, int64_t cta, int64_t n_cta) {
+  const int64_t n0 = h.p[0] ? h.n[0] & ~15ll : 0, n1 = h.p[1] ? h.n[1] & ~15ll : 0;
+  const int64_t total = n0 + n1;
+  if (total <= 0) return;
+  const int64_t share = ((total + n_cta - 1) / n_cta + 15) & ~15ll;
+  const int64_t beg = share * cta, end = beg + share < total ? beg + share : total;
+  for (int64_t off = beg; off < end;) {
+    const bool first = off < n0;
+    const int64_t lim = first ? (end < n0 ? end : n0) : end;
+    const int64_t c = lim - off < 32768 ? lim - off : 32768;
+    const char* src = first ? h.p[0] + off : h.p[1] + (off - n0);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(static_cast<uint32_t>(c))
+                 : "memory");
+    off += c;
+  }
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t stream, Args... args) {

@@ -248,6 +248,10 @@ __global__ void __launch_bounds__((kGemvWarps + 1) * 32, 1) gemm_ring_kernel(
         mbar_expect_tx(&full[it], wbytes + xbytes);
         tma_load_3d(smem + it * SB, &tw, 0, unit_of(it) * 16, (it % nst) * kSlabs, &full[it]);
       }
+      if (epi.l2_pre) {  // this CTA's share of a later kernel's weights, while waiting
+        const L2Hint h{{static_cast<const char*>(epi.l2_pre), nullptr}, {epi.l2_pre_bytes, 0}};
+        l2_prefetch_share(h, blockIdx.x, gridDim.x);
+      }
       pdl_wait();
       for (int it = 0; it < pre; ++it)
         tma_load_3d(smem + it * SB + wbytes, &tx, 0, 0, (it % nst) * kSlabs, &full[it]);

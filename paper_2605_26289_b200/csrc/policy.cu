@@ -330,6 +330,10 @@ __global__ void next_draft_prep_kernel(const ds_entry* __restrict__ entries, int
     const int acc = en.kind == DS_ENTRY_VERIFY ? out_accept[e] : 0;
     n = en.past + acc + 2;  // committed tokens incl. the pending bonus
     hist[static_cast<int64_t>(en.seq) * pos_stride + n - 1] = out_tok[en.out_start + acc];
+  } else if (en.kind == DS_ENTRY_PREFILL && en.n_draft < 0) {
+    // the chunk that ends the prompt: the first decode step's proposal
+    n = en.past + en.q_len + 1;  // the prompt + its sampled token
+    hist[static_cast<int64_t>(en.seq) * pos_stride + n - 1] = out_tok[en.out_start];
   }
   const int ln = n < window ? n : window;
   ring_off[e] = static_cast<int64_t>(en.seq) * pos_stride + n - ln;

@@ -19,7 +19,8 @@
 
 namespace ds {
 
-void set_attn_l2_prefetch(const void* ptr, int64_t bytes);
+void set_attn_l2_prefetch(const void* ptr, int64_t bytes, const void* ptr2 = nullptr,
+                          int64_t bytes2 = 0);
 int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_entry* entries_dev,
                       int n_entries, const void* k_pool, const void* v_pool, int64_t head_stride,
                       const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv, int hd,
@@ -465,10 +466,15 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
     }
     // the attention leaves HBM mostly idle (short contexts): K7's producer
     // warps pull wo's weights into L2 for the next projection meanwhile
+    // (and the head of gate_up's: DS_GU_L2_MB, continued by wo's own prefetch)
     static const double wo_l2_frac = getenv("DS_WO_L2_FRAC") ? atof(getenv("DS_WO_L2_FRAC")) : 1.0;
-    if (fused && small && wo_l2_frac > 0)
+    static const int64_t gu_l2_bytes = static_cast<int64_t>(
+        (getenv("DS_GU_L2_MB") ? atof(getenv("DS_GU_L2_MB")) : 0.0) * 1048576.0) & ~15ll;
+    const int64_t gu_head = fused && small ? gu_l2_bytes : 0;
+    if (fused && small && (wo_l2_frac > 0 || gu_head > 0))
       set_attn_l2_prefetch(wo + static_cast<size_t>(l) * H * nh * hd,
-                           static_cast<int64_t>(wo_l2_frac * H * nh * hd * 2) & ~15ll);
+                           static_cast<int64_t>(wo_l2_frac * H * nh * hd * 2) & ~15ll,
+                           wgu + static_cast<size_t>(l) * 2 * F * H, gu_head);
     if (n_long > 0 && n_long < a->n_entries) {  // mixed plan: K6 for prefill chunks, K7 rest
       DS_CHECK(ds_attention(b.qkv, a->entries_host, a->entries, n_long, T, kp + l * kv_layer,
                             vp + l * kv_layer, kv->capacity, kv->pos2cell, kv->pos_stride, nh,
@@ -488,7 +494,14 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
     const __nv_bfloat16* wd_l = wd + static_cast<size_t>(l) * H * F;
     if (fused) {
       ds_skinny_epi eo{};
-      eo.l2_next = wgu_l;
+      // wo's CTAs sit beside the attention (one-stage K7) waiting for it: they
+      // pull the head of gate_up's weights meanwhile (DS_WO_PRE_MB)
+      static const int64_t wo_pre_bytes = static_cast<int64_t>(
+          (getenv("DS_WO_PRE_MB") ? atof(getenv("DS_WO_PRE_MB")) : 0.0) * 1048576.0) & ~15ll;
+      const int64_t gu_pre = small ? wo_pre_bytes : 0;
+      eo.l2_pre = gu_pre ? reinterpret_cast<const char*>(wgu_l) + gu_head : nullptr;
+      eo.l2_pre_bytes = gu_pre;
+      eo.l2_next = reinterpret_cast<const char*>(wgu_l) + gu_head + gu_pre;
       eo.l2_next_bytes = l2_next_bytes;
       eo.ss_out = ss_mlp;
       eo.ss_zero = ss_attn;

@@ -409,7 +409,12 @@ class GpuEngine:
         ents = np.zeros(n_e, dtype=_ENTRY_DT)
         ents["seq"], ents["past"], ents["q_len"], ents["q_start"] = seqs, pasts, qs, q_starts
         ents["kind"], ents["out_start"], ents["n_out"] = kinds, out_starts, n_outs
-        ents["n_draft"] = np.fromiter((r.n_draft for r in rs), dtype=np.int64, count=n_e)
+        # a chunk that ends its prompt (no generated token yet) also gets the
+        # first decode step's proposal from the forward (n_draft = -1)
+        final = [r.kind == _lib.ENTRY_PREFILL and r.past + len(r.batch) == len(r.tokens)
+                 for r in rs]
+        ents["n_draft"] = np.fromiter((-1 if f else r.n_draft for r, f in zip(rs, final)),
+                                      dtype=np.int64, count=n_e)
         ents["hash_in"] = np.fromiter((self._hash_in(r.seq, r.past, r.tokens) for r in rs),
                                       dtype=np.uint64, count=n_e)
         row_entry = np.repeat(np.arange(n_e), qs)
@@ -464,9 +469,10 @@ class GpuEngine:
         self._ev[0].record(stream)  # device time includes the metadata kernels
         self._apply_metadata(*meta, sp)
         res = self.res_dev
-        # decode / verify only: the next proposal rides in the same launch
-        nd = self.fused_drafts and all(r.kind != _lib.ENTRY_PREFILL and not r.scratch
-                                       for r in reqs)
+        # the next proposal of every decode / verify entry and prompt-ending
+        # chunk rides in the same launch (other prefill chunks: empty ring)
+        nd = self.fused_drafts and any(r.kind != _lib.ENTRY_PREFILL for r in reqs) or \
+            (self.fused_drafts and any(final))
         args = _lib.ForwardArgs(
             n_e, q_start, out_start, self.policy, self.cfg.copy_min_match, self.cfg.vocab,
             st.hptr(o_ent), st.dptr(o_ent), st.dptr(o_tok), st.dptr(o_seq), st.dptr(o_pos),
@@ -495,6 +501,11 @@ class GpuEngine:
             dlen = h[o + 2 * n_e: o + 3 * n_e]
             drafts = h[o + 3 * n_e: o + 3 * n_e + n_e * self.nd_cap].reshape(n_e, self.nd_cap)
             for i, r in enumerate(rs):
+                if r.kind == _lib.ENTRY_PREFILL:
+                    if final[i]:
+                        self._draft_cache[r.seq] = (r.past + len(r.batch) + 1,
+                                                    drafts[i, : dlen[i]].tolist())
+                    continue
                 a = int(acc[i]) if r.kind == _lib.ENTRY_VERIFY else 0
                 self._draft_cache[r.seq] = (r.past + a + 2, drafts[i, : dlen[i]].tolist())
         out = [None] * n_e

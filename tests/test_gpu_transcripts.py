@@ -76,16 +76,19 @@ def test_batched_capacity_precheck_gpu(cuda):
     assert isinstance(c1.engine, GpuEngine)
 
 
-@pytest.mark.parametrize("name", ["c2", "c4_small"])
-def test_fused_next_proposal_matches_k1(cuda, name):
+@pytest.mark.parametrize("name,batched", [("c2", False), ("c4_small", False), ("c3", True),
+                                          ("c5_small", True), ("c11_tight", True)])
+def test_fused_next_proposal_matches_k1(cuda, name, batched):
     """The proposal computed inside each decode/verify forward (bonus token
     written on device, suffix match over the post-commit ring) equals a fresh
     K1 launch over the host's token list, for every proposal the scheduler
-    makes; and every cached proposal is actually used (no silent misses)."""
+    makes; and every cached proposal is actually used (no silent misses).
+    Batched plans: mixed prefill + decode / verify plans, scratch-cell rows and
+    deferred commits (c11_tight: KV pressure) included."""
     from paper_2605_26289_b200 import engine as E
 
     tr = load_trace(name)
-    core = InferenceCore(core_config_for(tr, model="tiny"))
+    core = InferenceCore(core_config_for(tr, model="tiny", batched_forward=batched))
     eng = core.engine
     stats = {"hits": 0, "calls": 0}
     orig = E.GpuEngine.propose
