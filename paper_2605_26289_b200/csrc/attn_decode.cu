@@ -100,7 +100,7 @@ int launch_attn_decode_tc(const ds_entry* entries_dev, int n_entries, const void
                           const void* k_pool, const void* v_pool, int64_t head_stride,
                           const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv,
                           int max_splits, float scale, void* out, float* part_o, float* part_lse,
-                          const L2Hint& l2, cudaStream_t stream);
+                          const L2Hint& l2, int* merged, cudaStream_t stream);
 
 constexpr int kBarBytes = 64;                                     // full/empty mbarriers
 constexpr int kMergeBytes = (kMaxRows * kD + kMaxRows + kMaxRows * 8) * 4;  // cval/clse/cw
@@ -704,8 +704,9 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
                        int n_entries, const void* k_pool, const void* v_pool, int64_t head_stride,
                        const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv, int max_R,
                        int max_splits, float scale, void* out, float* part_o, float* part_lse,
-                       int* counters, cudaStream_t stream) {
+                       int* counters, int* merged, cudaStream_t stream) {
   if (max_R > kMaxRows) return DS_EUNSUPPORTED;
+  *merged = max_splits <= kDecodeMaxCluster || max_R <= kDecodeLastMergeRows;
   int max_kv = 0, max_split_len = 0;
   for (int e = 0; e < n_entries; ++e) {
     const int kv = entries_host[e].past + entries_host[e].q_len;
@@ -750,7 +751,7 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
   if (max_R > kDecodeTcMinRows && max_kv >= kDecodeTcMinKeys)
     return launch_attn_decode_tc(entries_dev, n_entries, qkv, k_pool, v_pool, head_stride,
                                  pos2cell, pos_stride, nh, nkv, max_splits, scale, out, part_o,
-                                 part_lse, l2, stream);
+                                 part_lse, l2, merged, stream);
   auto kern = max_R <= 8 ? attn_decode_kernel<1>
               : max_R <= 16 ? attn_decode_kernel<2>
                             : attn_decode_kernel<3>;

@@ -16,6 +16,7 @@ namespace ds {
 // sum in split order (the same arithmetic as a per-row weight pass, without
 // its barrier and second round trip).  cw and bar_id are unused (kept for the
 // callers' layout).
+template <int MAXC = kDecodeMaxCluster>  // the largest cluster the caller launches
 DS_DEVICE void decode_cluster_merge(const float* cval, const float* clse, float* cw, int R,
                                     int n_splits, int cluster, int tid, int nthreads, int bar_id,
                                     const ds_entry& en, int nh, int kh, int G,
@@ -28,26 +29,26 @@ DS_DEVICE void decode_cluster_merge(const float* cval, const float* clse, float*
        idx += cluster * nthreads) {
     const int r = idx / kD4, d4 = idx - r * kD4;
     const uint32_t a = smem_u32(cval + r * kD + 4 * d4), al = smem_u32(clse + r);
-    float4 v[kDecodeMaxCluster];
-    float lv[kDecodeMaxCluster];
+    float4 v[MAXC];
+    float lv[MAXC];
 #pragma unroll
-    for (int p = 0; p < kDecodeMaxCluster; ++p) {
+    for (int p = 0; p < MAXC; ++p) {
       v[p] = p < n_splits ? dsmem_ld_f32x4(dsmem_map(a, p)) : make_float4(0.f, 0.f, 0.f, 0.f);
       lv[p] = p < n_splits ? dsmem_ld_f32(dsmem_map(al, p)) : -INFINITY;
     }
     float lmax = -INFINITY;
 #pragma unroll
-    for (int p = 0; p < kDecodeMaxCluster; ++p) lmax = fmaxf(lmax, lv[p]);
+    for (int p = 0; p < MAXC; ++p) lmax = fmaxf(lmax, lv[p]);
     float wsum = 0.f;
 #pragma unroll
-    for (int p = 0; p < kDecodeMaxCluster; ++p) {
+    for (int p = 0; p < MAXC; ++p) {
       lv[p] = lv[p] == -INFINITY ? 0.f : exp2f(lv[p] - lmax);
       wsum += lv[p];
     }
     const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int p = 0; p < kDecodeMaxCluster; ++p) {
+    for (int p = 0; p < MAXC; ++p) {
       const float w = lv[p] * inv;
       acc.x += w * v[p].x;
       acc.y += w * v[p].y;

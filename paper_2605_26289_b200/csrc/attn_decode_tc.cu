@@ -23,6 +23,9 @@
 #include "tc.cuh"
 #include "tma.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace ds {
 
 #ifdef DS_K7_TRACE
@@ -46,13 +49,20 @@ constexpr int kBM = 128;                       // MMA rows (R <= 24 real, rest p
 constexpr int kBN = 128;                       // keys per tile
 constexpr int kHalf = kBN * 128;               // 64-column half of a [128][128] bf16 tile
 constexpr int kTileBytes = 2 * kHalf;          // 32 KB
-constexpr int kKStages = 3, kVStages = 3;
+#ifndef DS_K7TC_KST  // K / V ring depths (A/B); K + V <= 6 stages of 32 KB
+#define DS_K7TC_KST 3
+#endif
+#ifndef DS_K7TC_VST
+#define DS_K7TC_VST 3
+#endif
+constexpr int kKStages = DS_K7TC_KST, kVStages = DS_K7TC_VST;
+static_assert(kKStages + kVStages <= 6 && kKStages >= 2 && kVStages >= 2, "K7-tc ring");
 constexpr int kSmemQ = 0;                      // 32 KB
 constexpr int kSmemK = kSmemQ + kTileBytes;    // 96 KB
 constexpr int kSmemV = kSmemK + kKStages * kTileBytes;  // 64 KB
 constexpr int kSmemBar = kSmemV + kVStages * kTileBytes;
 constexpr int kSmemBytes = kSmemBar + 256 + 1024;  // + barriers, + 1 KB alignment slack
-constexpr int kThreads = 3 * 32;
+constexpr int kThreads = 4 * 32;  // softmax, K producer, MMA, V producer
 constexpr int kTmemCols = 512;  // S0 [0,128) S1 [128,256) O [256,384)
 constexpr int kMaxRows = kDecodeMaxRows;
 
@@ -70,19 +80,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
     int64_t pos_stride, int nh, int nkv, float scale_log2, __nv_bfloat16* __restrict__ out,
     float* __restrict__ part_o, float* __restrict__ part_lse, int64_t head_stride,
     const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
-    const L2Hint l2) {
+    const L2Hint l2, int cluster) {
   TC_STAMP(6);
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // SW128 alignment
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
-  uint64_t* k_full = bars;        // [3]
-  uint64_t* k_empty = bars + 3;   // [3]
-  uint64_t* v_full = bars + 6;    // [kVStages <= 3]
-  uint64_t* v_empty = bars + 9;   // [kVStages]
-  uint64_t* s_full = bars + 12;   // [2]
-  uint64_t* pv_done = bars + 14;
-  uint64_t* p_full = bars + 15;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* k_full = bars;  // [kKStages]
+  uint64_t* k_empty = k_full + kKStages;
+  uint64_t* v_full = k_empty + kKStages;
+  uint64_t* v_empty = v_full + kVStages;
+  uint64_t* s_full = v_empty + kVStages;  // [2]
+  uint64_t* pv_done = s_full + 2;
+  uint64_t* p_full = pv_done + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_full + 1);
   // split-merge buffers over the K ring (free once the last PV completed)
   float* cval = reinterpret_cast<float*>(smem + kSmemK);  // [R][128]
   float* clse = cval + kMaxRows * kD;                     // [R]
@@ -96,7 +106,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
   const int kv_len = en.past + en.q_len;
   const AttnSplitPlan plan = attn_split_plan(1, kv_len, nkv, n_entries, 1, R);
   const bool active = split < plan.n_splits;  // idle CTAs still join the cluster merge
-  const bool cluster_merge = max_splits <= kDecodeMaxCluster;
+  const bool cluster_merge = cluster > 0;  // launched with clusters of `cluster` splits
   const int kh = blockIdx.y;
   const int k_begin = split * plan.split_len;
   const int k_end = min(k_begin + plan.split_len, kv_len);
@@ -132,12 +142,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
   const int32_t* p2c = pos2cell + static_cast<int64_t>(en.seq) * pos_stride;
 
   if (!active) {
-  } else if (warp == 1) {
-    // ======================= TMA producer =======================
-    if (lane == 0) {
-      tma_prefetch_desc(&tmk);
-      tma_prefetch_desc(&tmv);
-    }
+  } else if (warp == 1 || warp == 3) {
+    // =========== TMA producers: K tiles (warp 1), V tiles (warp 3) ===========
+    // separate issuing threads: a V load waits only for its own ring (the PV
+    // that frees it), never behind a K load waiting for the K ring
+    const bool is_v = warp == 3;
+    if (lane == 0) tma_prefetch_desc(is_v ? &tmv : &tmk);
     const int64_t hrow = kh * head_stride;
     struct Cells {
       int c[4], c0;
@@ -188,24 +198,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
       }
     };
     bool waited = false;
-    auto wait_if_new = [&](int jj) {  // before the first tile holding this batch's K/V
-      const int kt = k_begin + jj * kBN;
-      if (!waited && min(kt + kBN, k_end) > en.past) {
-        pdl_wait();
-        waited = true;
-      }
-    };
-    auto load_v = [&](int jj, const Cells& cc) {
-      const int st = jj % kVStages;
-      if (jj >= kVStages) mbar_wait(&v_empty[st], ((jj / kVStages) - 1) & 1);
-      wait_if_new(jj);
-      load(cc, &tmv, vpool, smem + kSmemV + st * kTileBytes, &v_full[st]);
-    };
-    Cells prev{};
+    const int n_st = is_v ? kVStages : kKStages;
+    uint64_t* fulls = is_v ? v_full : k_full;
+    uint64_t* empties = is_v ? v_empty : k_empty;
+    uint8_t* ring = smem + (is_v ? kSmemV : kSmemK);
     int raw0[4], raw1[4], raw2[4];
     cells_load(0, raw0);
     cells_load(1, raw1);
-    for (int jj = 0; jj < ntiles; ++jj) {  // K_jj, then V_{jj-1}
+    for (int jj = 0; jj < ntiles; ++jj) {
       cells_load(jj + 2, raw2);
       const Cells cc = cells_resolve(raw0);
 #pragma unroll
@@ -213,19 +213,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
         raw0[i] = raw1[i];
         raw1[i] = raw2[i];
       }
-      const int st = jj % kKStages;
-      if (jj >= kKStages) mbar_wait(&k_empty[st], ((jj / kKStages) - 1) & 1);
-      wait_if_new(jj);
-      load(cc, &tmk, kpool, smem + kSmemK + st * kTileBytes, &k_full[st]);
-      if (jj > 0) load_v(jj - 1, prev);
-      prev = cc;
+      const int st = jj % n_st;
+      if (jj >= n_st) mbar_wait(&empties[st], ((jj / n_st) - 1) & 1);
+      const int kt = k_begin + jj * kBN;
+      if (!waited && min(kt + kBN, k_end) > en.past) {  // this batch's own K/V rows
+        pdl_wait();
+        waited = true;
+      }
+      load(cc, is_v ? &tmv : &tmk, is_v ? vpool : kpool, ring + st * kTileBytes, &fulls[st]);
     }
-    if (ntiles > 0) load_v(ntiles - 1, prev);
     if (!waited) pdl_wait();
-    if (!cluster_merge) pdl_trigger();
-    if (lane == 0)  // this CTA's share of the next projections' weights -> L2
-      l2_prefetch_share(l2, blockIdx.z * gridDim.y + blockIdx.y,
-                        static_cast<int64_t>(gridDim.y) * gridDim.z);
+    if (!is_v) {
+      if (!cluster_merge) pdl_trigger();
+      if (lane == 0)  // this CTA's share of the next projections' weights -> L2
+        l2_prefetch_share(l2, blockIdx.z * gridDim.y + blockIdx.y,
+                          static_cast<int64_t>(gridDim.y) * gridDim.z);
+    }
   } else if (warp == 2) {
     // ======================= MMA issuer =======================
     if (lane == 0 && ntiles > 0) {
@@ -399,8 +402,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
   }
   if (cluster_merge && plan.n_splits > 1) {
     cluster_sync_all();  // every split's rows are in its cluster buffer
-    decode_cluster_merge(cval, clse, cw, R, plan.n_splits, max_splits, tid, kThreads, 1, en, nh,
-                         kh, G, out);
+    decode_cluster_merge<kDecodeTcMaxCluster>(cval, clse, cw, R, plan.n_splits, cluster, tid,
+                                              kThreads, 1, en, nh, kh, G, out);
     cluster_sync_all();  // peers keep their smem until every read is done
   }
   // PDL: see K7 (triggers only as the grid retires; more splits than a
@@ -415,15 +418,41 @@ extern "C" int ds_debug_k7tc_trace(unsigned long long* out) {
 }
 #endif
 
+// clusters of `size` CTAs of the K7-tc kernel co-resident on the GPU (0: none)
+static int tc_max_clusters(int size) {
+  static int cache[17] = {};
+  if (size < 1 || size > 16) return 0;
+  if (cache[size]) return cache[size] > 0 ? cache[size] : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1, 1, size);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = size;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, attn_decode_tc_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  cache[size] = n > 0 ? n : -1;
+  return n;
+}
+
 int launch_attn_decode_tc(const ds_entry* entries_dev, int n_entries, const void* qkv,
                           const void* k_pool, const void* v_pool, int64_t head_stride,
                           const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv,
                           int max_splits, float scale, void* out, float* part_o, float* part_lse,
-                          const L2Hint& l2, cudaStream_t stream) {
+                          const L2Hint& l2, int* merged, cudaStream_t stream) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSmemBytes);
+    cudaFuncSetAttribute(attn_decode_tc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
   const CUtensorMap* tk = kv_tensor_map(k_pool, static_cast<int64_t>(nkv) * head_stride, kBN);
@@ -432,20 +461,38 @@ int launch_attn_decode_tc(const ds_entry* entries_dev, int n_entries, const void
   dim3 grid(1, nkv, n_entries * max_splits);
   const float sl2 = scale * 1.4426950408889634f;
   const int stride = (nh + 2 * nkv) * kD;
+  // the splits of one (entry, kv head) merge in one cluster: up to 8 always,
+  // up to kDecodeTcMaxCluster when every cluster of the grid is co-resident
+  int cluster = 0;
   if (max_splits <= kDecodeMaxCluster)
-    launch_pdl_cluster_z(attn_decode_tc_kernel, grid, dim3(kThreads), kSmemBytes, max_splits,
+    cluster = max_splits;
+  else if (max_splits <= kDecodeTcMaxCluster && tc_max_clusters(max_splits) >= nkv * n_entries)
+    cluster = max_splits;
+  *merged = cluster > 0;
+  static const bool verbose = getenv("DS_K7_VERBOSE") != nullptr;
+  static bool once = false;
+  if (verbose && !once) {
+    once = true;
+    for (int c = 8; c <= 16; ++c) fprintf(stderr, "K7-tc cluster %d: %d co-resident\n", c, tc_max_clusters(c));
+  }
+  if (verbose)
+    fprintf(stderr, "K7-tc: %d entries x %d kv heads, %d splits, cluster %d (co-resident %d)\n",
+            n_entries, nkv, max_splits, cluster,
+            max_splits <= 16 ? tc_max_clusters(max_splits) : 0);
+  if (cluster)
+    launch_pdl_cluster_z(attn_decode_tc_kernel, grid, dim3(kThreads), kSmemBytes, cluster,
                          stream, static_cast<const __nv_bfloat16*>(qkv), stride, entries_dev,
                          n_entries, max_splits, static_cast<const __nv_bfloat16*>(k_pool),
                          static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv,
                          sl2, static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride,
-                         *tk, *tv, l2);
+                         *tk, *tv, l2, cluster);
   else
     launch_pdl(attn_decode_tc_kernel, grid, dim3(kThreads), kSmemBytes, stream,
                static_cast<const __nv_bfloat16*>(qkv), stride, entries_dev, n_entries, max_splits,
                static_cast<const __nv_bfloat16*>(k_pool),
                static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv, sl2,
                static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride, *tk, *tv,
-               l2);
+               l2, 0);
   return (int)cudaGetLastError();
 }
 

@@ -68,7 +68,7 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
                        int n_entries, const void* k_pool, const void* v_pool, int64_t head_stride,
                        const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv, int max_R,
                        int max_splits, float scale, void* out, float* part_o, float* part_lse,
-                       int* counters, cudaStream_t stream);
+                       int* counters, int* merged, cudaStream_t stream);
 
 int launch_attn_prefill_sm100(const void* qkv, const ds_entry* entries_host,
                               const ds_entry* entries_dev, int n_entries, const void* k_pool,
@@ -114,15 +114,15 @@ int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_en
   const int64_t slots = attn_partial_slots(entries_host, n_entries, nh, nkv, mode);
   float* part_lse = part_o + slots * kD;
   {
+    int merged = 0;
     const int rc = launch_attn_decode(qkv, entries_host, entries_dev, n_entries, k_pool, v_pool,
                                       head_stride, pos2cell, pos_stride, nh, nkv, max_R,
-                                      max_splits, scale, out, part_o, part_lse, counters, stream);
+                                      max_splits, scale, out, part_o, part_lse, counters, &merged,
+                                      stream);
     // K7 merges up to kDecodeMaxCluster key splits in-cluster; more through
     // global partials: merged by the last split to arrive for <= 8 rows,
     // else by the combine kernel (launched early: K7 has not triggered it)
-    if (rc != 0 || !any_split || max_splits <= kDecodeMaxCluster ||
-        max_R <= kDecodeLastMergeRows)
-      return rc;
+    if (rc != 0 || !any_split || merged) return rc;
     dim3 cgrid(max_R, nkv, n_entries);
     launch_pdl(attn_combine_kernel, cgrid, dim3(kD), 0, stream, entries_dev, n_entries, nh, nkv,
                kSplitNW * 16, 1, (const float*)part_o, (const float*)part_lse,

@@ -32,6 +32,19 @@ constexpr int kDecodeTcMinRows = 8;
 // combine kernel
 constexpr int kDecodeLastMergeRows = 8;
 constexpr int kDecodeTcMinKeys = 4096;
+// K7-tc (R > 8 rows over >= kDecodeTcMinKeys keys) takes at most this many key
+// splits and merges them in ONE (non-portable) cluster through distributed
+// shared memory when the clusters fit the GPU in one wave - no combine launch
+// and no global partials on the critical path.  Off by default (0): on the
+// B200 only 7 clusters of 11..16 one-CTA-per-SM CTAs are co-resident (9: 15,
+// 10: 11), fewer than the 8 kv heads of one verify entry, so the 16-split
+// plan fell back to the combine kernel with fewer CTAs (m=32k q=5 30.5 ->
+// 36.9 us); the one-CTA-per-SM plan + attn_combine_kernel stays
+#ifndef DS_K7_TC_CLUSTER
+#define DS_K7_TC_CLUSTER 0
+#endif
+constexpr int kDecodeTcMaxCluster = DS_K7_TC_CLUSTER > kDecodeMaxCluster ? DS_K7_TC_CLUSTER
+                                                                           : kDecodeMaxCluster;
 #ifndef DS_K7_SHORT_TILES
 #define DS_K7_SHORT_TILES (8 * kDecodeMaxCluster)
 #endif
@@ -69,6 +82,9 @@ DS_HD AttnSplitPlan attn_split_plan(int qblocks, int kv_len, int nkv, int n_entr
   if (mode && rows <= kDecodeLastMergeRows && n > DS_K7_SHORT_SPLITS_SMALL &&
       by_len <= kDecodeShortTiles)
     n = DS_K7_SHORT_SPLITS_SMALL;
+  if (DS_K7_TC_CLUSTER > kDecodeMaxCluster && mode && rows > kDecodeTcMinRows &&
+      kv_len >= kDecodeTcMinKeys && n > kDecodeTcMaxCluster)
+    n = kDecodeTcMaxCluster;
   if (n > 64) n = 64;
   if (n < 1) n = 1;
   const int gran = mode ? 128 : 64;  // key tile of the kernel

@@ -59,12 +59,7 @@ namespace ds {
 namespace {
 constexpr int kBM = 128;
 constexpr int kSlabA = kBM * 128;  // 16 KB: 128 weight rows x 64 columns
-constexpr int kThreads = 11 * 32;  // weight producer, MMA, 8 epilogue warps, token producer
-constexpr int kTokWarp = 10;
-// one thread issues a TMA box only every ~190 ns whatever its size up to 32 KB
-// (tools/micro_sm_bw.cu: 16 KB boxes from one thread stream 89 GB/s per SM,
-// from two threads 165), so the weight and token boxes of a stage come from
-// different warps
+constexpr int kThreads = 10 * 32;  // producer, MMA, 8 epilogue warps
 constexpr int kEpiThreads = 8 * 32;
 constexpr int kMaxNT = 256;
 constexpr int kAccCols = 256;
@@ -85,7 +80,6 @@ struct StreamArgs {
   int T, N, K, y_f32, accumulate;
   int NT, n_tt, kt, stages;
   unsigned long long* trace;  // DS_STREAM_TRACE: per-CTA globaltimer stamps [P][16]
-  int dbg_no_mma;             // DS_STREAM_NOMMA (measurement only): skip the MMAs
 };
 
 DS_DEVICE unsigned long long gtimer() {
@@ -396,35 +390,33 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_stream_kernel(
       tma_prefetch_desc(&tw);
       tma_prefetch_desc(&tx);
       const int64_t n = it_e - it_b;
-      // the weights do not depend on the previous kernel: no dependency wait
-      for (int64_t i = 0; i < n; ++i) {
-        const int st = static_cast<int>(i % a.stages);
-        if (i >= a.stages) mbar_wait(&empty[st], static_cast<uint32_t>((i / a.stages) - 1) & 1);
+      const int pre = static_cast<int>(n < a.stages ? n : a.stages);
+      for (int i = 0; i < pre; ++i) {
         const int64_t it = it_b + i;
         const int tile = static_cast<int>(it / kt), kk = static_cast<int>(it % kt);
+        mbar_expect_tx(&full[i], stage_bytes);
+        tma_load_3d(smem + i * stage_bytes, &tw, 0, (tile / a.n_tt) * kBM, kk, &full[i]);
+      }
+      pdl_wait();  // the activations come from the previous kernel
+      for (int i = 0; i < pre; ++i) {
+        const int64_t it = it_b + i;
+        const int tile = static_cast<int>(it / kt), kk = static_cast<int>(it % kt);
+        tma_load_3d(smem + i * stage_bytes + kSlabA, &tx, 0, (tile % a.n_tt) * a.NT, kk,
+                    &full[i]);
+      }
+      for (int64_t i = pre; i < n; ++i) {
+        const int st = static_cast<int>(i % a.stages);
+        mbar_wait(&empty[st], static_cast<uint32_t>((i / a.stages) - 1) & 1);
+        const int64_t it = it_b + i;
+        const int tile = static_cast<int>(it / kt), kk = static_cast<int>(it % kt);
+        uint8_t* sp = smem + st * stage_bytes;
         mbar_expect_tx(&full[st], stage_bytes);
-        tma_load_3d(smem + st * stage_bytes, &tw, 0, (tile / a.n_tt) * kBM, kk, &full[st]);
+        tma_load_3d(sp, &tw, 0, (tile / a.n_tt) * kBM, kk, &full[st]);
+        tma_load_3d(sp + kSlabA, &tx, 0, (tile % a.n_tt) * a.NT, kk, &full[st]);
       }
       if (tr) tr[2] = gtimer();
     }
     __syncwarp();  // reconverge before the CTA barrier (bar.sync is warp-aligned)
-  } else if (warp == kTokWarp) {
-    // token boxes (activations of the previous kernel); a box may land before
-    // the weight producer's expect_tx of the same phase (the tx count goes
-    // transiently negative; the phase still needs that arrival)
-    if (lane == 0) {
-      const int64_t n = it_e - it_b;
-      pdl_wait();
-      for (int64_t i = 0; i < n; ++i) {
-        const int st = static_cast<int>(i % a.stages);
-        if (i >= a.stages) mbar_wait(&empty[st], static_cast<uint32_t>((i / a.stages) - 1) & 1);
-        const int64_t it = it_b + i;
-        const int tile = static_cast<int>(it / kt), kk = static_cast<int>(it % kt);
-        tma_load_3d(smem + st * stage_bytes + kSlabA, &tx, 0, (tile % a.n_tt) * a.NT, kk,
-                    &full[st]);
-      }
-    }
-    __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_bf16(kBM, a.NT, false);
@@ -443,16 +435,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_stream_kernel(
           mbar_wait(&full[st], static_cast<uint32_t>(i / a.stages) & 1);
           tc::fence_after();
           const uint32_t pa = base + st * stage_bytes, pb = pa + kSlabA;
-          if (!a.dbg_no_mma) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tc::mma(d, tc::smem_desc(pa + k * 32, 16, 1024),
-                      tc::smem_desc(pb + k * 32, 16, 1024), idesc, (it != s0 || k > 0) ? 1u : 0u);
-          }
-          if (a.dbg_no_mma == 2)
-            mbar_arrive(&empty[st]);
-          else
-            tc::commit(&empty[st]);  // the stage is free once its MMAs completed
+          for (int k = 0; k < 4; ++k)
+            tc::mma(d, tc::smem_desc(pa + k * 32, 16, 1024), tc::smem_desc(pb + k * 32, 16, 1024),
+                    idesc, (it != s0 || k > 0) ? 1u : 0u);
+          tc::commit(&empty[st]);  // the stage is free once its MMAs completed
         }
         tc::commit(&acc_full[acc]);
       }
@@ -815,21 +802,21 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cluster_kernel(
     if (lane == 0) {
       tma_prefetch_desc(&tw);
       tma_prefetch_desc(&tx);
-      for (int i = 0; i < n; ++i) {
-        const int st = i % a.stages;
-        if (i >= a.stages) mbar_wait(&empty[st], static_cast<uint32_t>((i / a.stages) - 1) & 1);
-        mbar_expect_tx(&full[st], stage_bytes);
-        tma_load_3d(smem + st * stage_bytes, &tw, 0, wt * kBM, k_beg + i, &full[st]);
+      const int pre = n < a.stages ? n : a.stages;
+      for (int i = 0; i < pre; ++i) {
+        mbar_expect_tx(&full[i], stage_bytes);
+        tma_load_3d(smem + i * stage_bytes, &tw, 0, wt * kBM, k_beg + i, &full[i]);
       }
-    }
-    __syncwarp();
-  } else if (warp == kTokWarp) {  // token boxes (see gemm_stream_kernel)
-    if (lane == 0) {
       pdl_wait();  // the activations come from the previous kernel
-      for (int i = 0; i < n; ++i) {
+      for (int i = 0; i < pre; ++i)
+        tma_load_3d(smem + i * stage_bytes + kSlabA, &tx, 0, 0, k_beg + i, &full[i]);
+      for (int i = pre; i < n; ++i) {
         const int st = i % a.stages;
-        if (i >= a.stages) mbar_wait(&empty[st], static_cast<uint32_t>((i / a.stages) - 1) & 1);
-        tma_load_3d(smem + st * stage_bytes + kSlabA, &tx, 0, 0, k_beg + i, &full[st]);
+        mbar_wait(&empty[st], static_cast<uint32_t>((i / a.stages) - 1) & 1);
+        uint8_t* sp = smem + st * stage_bytes;
+        mbar_expect_tx(&full[st], stage_bytes);
+        tma_load_3d(sp, &tw, 0, wt * kBM, k_beg + i, &full[st]);
+        tma_load_3d(sp + kSlabA, &tx, 0, 0, k_beg + i, &full[st]);
       }
     }
     __syncwarp();
@@ -856,7 +843,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cluster_kernel(
   // (padded row: the thread-per-feature writes and the warp-per-token reads
   // are both bank-conflict free)
   const int ncols = (a.NT + 31) & ~31, nch = ncols / 32;
-  const bool epi_warp = warp >= 2 && warp < kTokWarp;
+  const bool epi_warp = warp >= 2;
   const int quad = warp & 3, r = quad * 32 + lane, half = (warp - 2) >> 2;
   const int et = threadIdx.x - 64;  // 0..255
   const int w8 = warp - 2;          // 0..7
@@ -1150,7 +1137,6 @@ extern "C" int ds_gemm_stream(const void* X, const void* W, void* Y, int T, int 
   a.kt = p.kt;
   a.stages = p.stages;
   a.trace = nullptr;
-  a.dbg_no_mma = getenv("DS_STREAM_NOMMA") ? atoi(getenv("DS_STREAM_NOMMA")) : 0;
   if (getenv("DS_STREAM_TRACE")) {
     if (!g_trace) {
       cudaMalloc(&g_trace, 4096 * 16 * 8);
