@@ -3,7 +3,7 @@
 // timed on the stream over rotating weight copies (> L2), against the
 // cublasGemmEx default the forward uses.  Measurement-only export
 // (tools/bench_lt.py); the forward picks its algorithm in runtime.cu.
-#include "../../include/deltaserve_b200.h"
+#include "deltaserve_b200.h"
 
 #include <cublasLt.h>
 #include <cublas_v2.h>
