@@ -129,10 +129,6 @@ __global__ void silu_mul_kernel(const uint4* __restrict__ gu, int chunks, uint4*
 // RoPE-pair interleaved (ds_model.wqkv: column 16t+j = dim 8t+j or 64+8t+j-8),
 // so the row's q/k part is staged in smem before the in-place rewrite.  One
 // CTA per batch row.  (The decode forward folds this into the wqkv epilogue.)
-DS_DEVICE int qk_col(int dim) {  // column of head dim `dim` (hd = 128)
-  const int hi = dim >= 64, i = dim - 64 * hi;
-  return 16 * (i >> 3) + 8 * hi + (i & 7);
-}
 
 __global__ void rope_kv_store_kernel(__nv_bfloat16* __restrict__ qkv, const int32_t* row_seq,
                                      const int32_t* row_pos, const int32_t* __restrict__ pos2cell,
@@ -154,25 +150,46 @@ __global__ void rope_kv_store_kernel(__nv_bfloat16* __restrict__ qkv, const int3
   for (int j = threadIdx.x; j < qk_chunks; j += blockDim.x)
     reinterpret_cast<uint4*>(stage)[j] = reinterpret_cast<const uint4*>(row)[j];
   __syncthreads();
+  // pair block t of a head (dims 8t..8t+7 and 64+8t..64+8t+7) is the one
+  // contiguous 32-byte column chunk [16t, 16t+16): one thread per block reads
+  // it from the staged copy and writes two 16-byte rows of rotated output
+  // (in place for q and k, and k into the pool) - vector stores, not bf16
+  // scalars
   const float* cs = rope_cos + static_cast<int64_t>(pos) * half;
   const float* sn = rope_sin + static_cast<int64_t>(pos) * half;
-  const int n_pairs = (nh + nkv) * half;
-  for (int idx = threadIdx.x; idx < n_pairs; idx += blockDim.x) {
-    const int head = idx / half;
-    const int i = idx - head * half;
-    const __nv_bfloat16* xs = stage + head * hd;
-    const float x1 = __bfloat162float(xs[qk_col(i)]);
-    const float x2 = __bfloat162float(xs[qk_col(i + half)]);
-    const float c = __ldg(cs + i), s = __ldg(sn + i);
-    const __nv_bfloat16 y1 = __float2bfloat16_rn(x1 * c - x2 * s);
-    const __nv_bfloat16 y2 = __float2bfloat16_rn(x2 * c + x1 * s);
+  const int blocks_per_head = half / 8;
+  const int n_blocks = (nh + nkv) * blocks_per_head;
+  for (int idx = threadIdx.x; idx < n_blocks; idx += blockDim.x) {
+    const int head = idx / blocks_per_head;
+    const int t = idx - head * blocks_per_head;
+    const uint4* xs = reinterpret_cast<const uint4*>(stage + head * hd) + 2 * t;
+    const uint4 lo = xs[0], hi = xs[1];
+    const __nv_bfloat162* pl = reinterpret_cast<const __nv_bfloat162*>(&lo);
+    const __nv_bfloat162* ph = reinterpret_cast<const __nv_bfloat162*>(&hi);
+    const float4 c0 = __ldg(reinterpret_cast<const float4*>(cs + 8 * t));
+    const float4 c1 = __ldg(reinterpret_cast<const float4*>(cs + 8 * t) + 1);
+    const float4 s0 = __ldg(reinterpret_cast<const float4*>(sn + 8 * t));
+    const float4 s1 = __ldg(reinterpret_cast<const float4*>(sn + 8 * t) + 1);
+    const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    const float ss[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    uint4 o1, o2;
+    uint32_t* p1 = reinterpret_cast<uint32_t*>(&o1);
+    uint32_t* p2 = reinterpret_cast<uint32_t*>(&o2);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 a = __bfloat1622float2(pl[q]), b = __bfloat1622float2(ph[q]);
+      const int j = 2 * q;
+      // y1 = x1 c - x2 s (dim i), y2 = x2 c + x1 s (dim i + 64), each rounded
+      p1[q] = pack_bf16(a.x * cc[j] - b.x * ss[j], a.y * cc[j + 1] - b.y * ss[j + 1]);
+      p2[q] = pack_bf16(b.x * cc[j] + a.x * ss[j], b.y * cc[j + 1] + a.y * ss[j + 1]);
+    }
     __nv_bfloat16* x = row + head * hd;
-    x[i] = y1;
-    x[i + half] = y2;
+    reinterpret_cast<uint4*>(x + 8 * t)[0] = o1;
+    reinterpret_cast<uint4*>(x + half + 8 * t)[0] = o2;
     if (head >= nh) {
       __nv_bfloat16* kd = k_pool + ((head - nh) * head_stride + cell) * hd;
-      kd[i] = y1;
-      kd[i + half] = y2;
+      reinterpret_cast<uint4*>(kd + 8 * t)[0] = o1;
+      reinterpret_cast<uint4*>(kd + half + 8 * t)[0] = o2;
     }
   }
   // v: 16-byte chunks, head-major pool ([kv_head][cell][hd])
