@@ -52,8 +52,13 @@ DS_DEVICE unsigned long long gtime() {
 #define K7_STAMP(i)                                                                        \
   if (threadIdx.x == 0)                                                                    \
   g_k7_trace[(blockIdx.z * gridDim.y + blockIdx.y) & 1023][i] = gtime()
+// SM-clock stamps of thread 0 (same SM: exact intra-CTA deltas)
+__device__ long long g_k7_clk[1024][16];
+#define K7_CLK(i)                                                                          \
+  if (threadIdx.x == 0) g_k7_clk[(blockIdx.z * gridDim.y + blockIdx.y) & 1023][i] = clock64()
 #else
 #define K7_STAMP(i)
+#define K7_CLK(i)
 #endif
 
 namespace {
@@ -99,8 +104,9 @@ void set_attn_l2_prefetch(const void* ptr, int64_t bytes, const void* ptr2, int6
 int launch_attn_decode_tc(const ds_entry* entries_dev, int n_entries, const void* qkv,
                           const void* k_pool, const void* v_pool, int64_t head_stride,
                           const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv,
-                          int max_splits, float scale, void* out, float* part_o, float* part_lse,
-                          const L2Hint& l2, int* merged, cudaStream_t stream);
+                          int max_splits, int max_split_len, float scale, void* out,
+                          float* part_o, float* part_lse, const L2Hint& l2, int* merged,
+                          cudaStream_t stream);
 
 constexpr int kBarBytes = 64;                                     // full/empty mbarriers
 constexpr int kMergeBytes = (kMaxRows * kD + kMaxRows + kMaxRows * 8) * 4;  // cval/clse/cw
@@ -235,6 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
     K7_STAMP(0);
     pdl_wait();  // q comes from the preceding projection
     K7_STAMP(1);
+    K7_CLK(0);
     if (early_trigger) pdl_trigger();
     const int g = lane >> 2, t = lane & 3;
     // Q^T as the B operand: qb[j][kk] covers rows 8j + g, d [16kk + 2t, +1] and
@@ -297,7 +304,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
       for (int it = 0; it < kStages; ++it) {
         if (it >= ntiles) break;
         mbar_wait(&full[it], 0);
-        if (it == 0) K7_STAMP(2);
+        if (it == 0) {
+          K7_STAMP(2);
+          K7_CLK(1);
+        }
         const uint32_t ks_u = smem_u32(smem + it * kStageBytes);
   #pragma unroll
         for (int j = 0; j < NT; ++j) s[it][j][0] = s[it][j][1] = s[it][j][2] = s[it][j][3] = 0.f;
@@ -349,6 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
           if (g == 0) mxs[warp * kMaxRows + 8 * j + 2 * t + h] = m;
         }
       named_bar_sync(1, kConsumers * 32);  // maxima published; every warp is done with K
+      K7_CLK(2);
       // the K halves of the stages are free now: each tile's P^T fragments go
       // into its own K half, the row sums after stage 0's fragments
       constexpr int kPbsBytes = kConsumers * 3 * 32 * 8;  // [8 warps][NT <= 3][32 lanes] uint2
@@ -395,6 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
           if (g == 0) lsm[warp * kMaxRows + 8 * j + 2 * t + h] = v;
         }
       named_bar_sync(1, kConsumers * 32);  // every warp's P^T and row sums published
+      K7_CLK(3);
       float o[NT][4];
   #pragma unroll
       for (int j = 0; j < NT; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
@@ -416,6 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
         }
       }
       K7_STAMP(3);
+      K7_CLK(4);
       // o[j][q]: d = 16w + g (+8 for q >= 2), row 8j + 2t + (q & 1)
   #pragma unroll
       for (int j = 0; j < NT; ++j) {
@@ -678,12 +691,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
 
   // ---- split merge across the cluster (distributed shared memory) ----
   K7_STAMP(4);
+  K7_CLK(5);
   if (cluster_merge && plan.n_splits > 1) {
     cluster_sync_all();  // every split's rows are in its cbuf
+    K7_CLK(6);
     if (tid < kConsumers * 32)
       decode_cluster_merge(cval, clse, cw, R, plan.n_splits, max_splits, tid, kConsumers * 32, 1,
                            en, nh, kh, G, out);
+    K7_CLK(7);
     cluster_sync_all();  // peers keep their smem until every read is done
+    K7_CLK(8);
   }
   // PDL: when the dependent is the next projection it launches only as this
   // grid retires - an earlier trigger (even after the main loop) let its CTAs
@@ -697,6 +714,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
 #ifdef DS_K7_TRACE
 extern "C" int ds_debug_k7_trace(unsigned long long* out) {
   return (int)cudaMemcpyFromSymbol(out, g_k7_trace, sizeof(g_k7_trace));
+}
+extern "C" int ds_debug_k7_clk(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_k7_clk, sizeof(g_k7_clk));
 }
 #endif
 
@@ -748,10 +768,12 @@ int launch_attn_decode(const void* qkv, const ds_entry* entries_host, const ds_e
   g_l2 = L2Hint{{nullptr, nullptr}, {0, 0}};
   // more than 8 rows over a long prefix: the legacy HMMA pipe would bound the
   // mma.sync kernel below the HBM rate - run the tcgen05 variant
-  if (max_R > kDecodeTcMinRows && max_kv >= kDecodeTcMinKeys)
+  static const int tc_min_keys =
+      getenv("DS_K7_TC_MIN_KEYS") ? atoi(getenv("DS_K7_TC_MIN_KEYS")) : kDecodeTcMinKeys;
+  if (max_R > kDecodeTcMinRows && max_kv >= tc_min_keys)
     return launch_attn_decode_tc(entries_dev, n_entries, qkv, k_pool, v_pool, head_stride,
-                                 pos2cell, pos_stride, nh, nkv, max_splits, scale, out, part_o,
-                                 part_lse, l2, merged, stream);
+                                 pos2cell, pos_stride, nh, nkv, max_splits, max_split_len, scale,
+                                 out, part_o, part_lse, l2, merged, stream);
   auto kern = max_R <= 8 ? attn_decode_kernel<1>
               : max_R <= 16 ? attn_decode_kernel<2>
                             : attn_decode_kernel<3>;

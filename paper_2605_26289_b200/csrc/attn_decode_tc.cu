@@ -57,11 +57,18 @@ constexpr int kTileBytes = 2 * kHalf;          // 32 KB
 #endif
 constexpr int kKStages = DS_K7TC_KST, kVStages = DS_K7TC_VST;
 static_assert(kKStages + kVStages <= 6 && kKStages >= 2 && kVStages >= 2, "K7-tc ring");
-constexpr int kSmemQ = 0;                      // 32 KB
-constexpr int kSmemK = kSmemQ + kTileBytes;    // 96 KB
-constexpr int kSmemV = kSmemK + kKStages * kTileBytes;  // 64 KB
-constexpr int kSmemBar = kSmemV + kVStages * kTileBytes;
-constexpr int kSmemBytes = kSmemBar + 256 + 1024;  // + barriers, + 1 KB alignment slack
+constexpr int kSmemQ = 0;  // 32 KB
+// shared-memory layout of a KS-stage K ring and a VS-stage V ring (one CTA per
+// SM; a one-stage variant beside the next projection's CTA, as K7's, measured
+// no faster: C2 26.66 vs 26.69 turns/s)
+template <int KS, int VS>
+struct TcLayout {
+  static constexpr int kK = kSmemQ + kTileBytes;
+  static constexpr int kV = kK + KS * kTileBytes;
+  static constexpr int kBar = kV + VS * kTileBytes;
+  static constexpr int kBytes = kBar + 256 + 1024;  // + barriers, + 1 KB alignment slack
+};
+constexpr int kSmemBytes = TcLayout<kKStages, kVStages>::kBytes;
 constexpr int kThreads = 4 * 32;  // softmax, K producer, MMA, V producer
 constexpr int kTmemCols = 512;  // S0 [0,128) S1 [128,256) O [256,384)
 constexpr int kMaxRows = kDecodeMaxRows;
@@ -73,6 +80,7 @@ DS_DEVICE int sw128(int rows, int row, int chunk16) {
 
 int decode_tc_smem_bytes() { return kSmemBytes; }
 
+template <int KS, int VS>
 __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
     const __nv_bfloat16* __restrict__ qkv, int qkv_stride, const ds_entry* __restrict__ entries,
     int n_entries, int max_splits, const __nv_bfloat16* __restrict__ kpool,
@@ -81,20 +89,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
     float* __restrict__ part_o, float* __restrict__ part_lse, int64_t head_stride,
     const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
     const L2Hint l2, int cluster) {
+  using Lay = TcLayout<KS, VS>;
   TC_STAMP(6);
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // SW128 alignment
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
-  uint64_t* k_full = bars;  // [kKStages]
-  uint64_t* k_empty = k_full + kKStages;
-  uint64_t* v_full = k_empty + kKStages;
-  uint64_t* v_empty = v_full + kVStages;
-  uint64_t* s_full = v_empty + kVStages;  // [2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::kBar);
+  uint64_t* k_full = bars;  // [KS]
+  uint64_t* k_empty = k_full + KS;
+  uint64_t* v_full = k_empty + KS;
+  uint64_t* v_empty = v_full + VS;
+  uint64_t* s_full = v_empty + VS;  // [2]
   uint64_t* pv_done = s_full + 2;
   uint64_t* p_full = pv_done + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_full + 1);
   // split-merge buffers over the K ring (free once the last PV completed)
-  float* cval = reinterpret_cast<float*>(smem + kSmemK);  // [R][128]
+  float* cval = reinterpret_cast<float*>(smem + Lay::kK);  // [R][128]
   float* clse = cval + kMaxRows * kD;                     // [R]
   float* cw = clse + kMaxRows;                            // [R][kDecodeMaxCluster]
 
@@ -114,11 +123,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   if (warp == 1 && lane == 0) {
-    for (int i = 0; i < kKStages; ++i) {
+    for (int i = 0; i < KS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
     }
-    for (int i = 0; i < kVStages; ++i) {
+    for (int i = 0; i < VS; ++i) {
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
     }
@@ -198,10 +207,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
       }
     };
     bool waited = false;
-    const int n_st = is_v ? kVStages : kKStages;
+    const int n_st = is_v ? VS : KS;
     uint64_t* fulls = is_v ? v_full : k_full;
     uint64_t* empties = is_v ? v_empty : k_empty;
-    uint8_t* ring = smem + (is_v ? kSmemV : kSmemK);
+    uint8_t* ring = smem + (is_v ? Lay::kV : Lay::kK);
     int raw0[4], raw1[4], raw2[4];
     cells_load(0, raw0);
     cells_load(1, raw1);
@@ -235,13 +244,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
       constexpr uint32_t idesc_s = tc::idesc_bf16(kBM, kBN, false);
       constexpr uint32_t idesc_pv = tc::idesc_bf16(kBM, kD, true);
       const uint32_t q_base = smem_u32(smem + kSmemQ);
-      const uint32_t k_base = smem_u32(smem + kSmemK);
-      const uint32_t v_base = smem_u32(smem + kSmemV);
+      const uint32_t k_base = smem_u32(smem + Lay::kK);
+      const uint32_t v_base = smem_u32(smem + Lay::kV);
       mbar_wait(p_full, 0);  // q staged (the softmax warp's first p_full phase)
       tc::fence_after();
       auto issue_s = [&](int jj) {
-        const int st = jj % kKStages, sb = jj & 1;
-        mbar_wait(&k_full[st], (jj / kKStages) & 1);
+        const int st = jj % KS, sb = jj & 1;
+        mbar_wait(&k_full[st], (jj / KS) & 1);
         tc::fence_after();
         const uint32_t kb = k_base + st * kTileBytes;
 #pragma unroll
@@ -256,9 +265,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_tc_kernel(
       issue_s(0);
       for (int jj = 0; jj < ntiles; ++jj) {
         if (jj + 1 < ntiles) issue_s(jj + 1);
-        const int st = jj % kVStages;
+        const int st = jj % VS;
         mbar_wait(p_full, (jj + 1) & 1);  // P_jj (completion jj + 1)
-        mbar_wait(&v_full[st], (jj / kVStages) & 1);
+        mbar_wait(&v_full[st], (jj / VS) & 1);
         tc::fence_after();
         const uint32_t vb = v_base + st * kTileBytes;
 #pragma unroll
@@ -435,7 +444,8 @@ static int tc_max_clusters(int size) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, attn_decode_tc_kernel, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, attn_decode_tc_kernel<kKStages, kVStages>, &cfg) !=
+      cudaSuccess) {
     cudaGetLastError();
     n = 0;
   }
@@ -446,13 +456,15 @@ static int tc_max_clusters(int size) {
 int launch_attn_decode_tc(const ds_entry* entries_dev, int n_entries, const void* qkv,
                           const void* k_pool, const void* v_pool, int64_t head_stride,
                           const int32_t* pos2cell, int64_t pos_stride, int nh, int nkv,
-                          int max_splits, float scale, void* out, float* part_o, float* part_lse,
-                          const L2Hint& l2, int* merged, cudaStream_t stream) {
+                          int max_splits, int max_split_len, float scale, void* out,
+                          float* part_o, float* part_lse, const L2Hint& l2, int* merged,
+                          cudaStream_t stream) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmemBytes);
-    cudaFuncSetAttribute(attn_decode_tc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(attn_decode_tc_kernel<kKStages, kVStages>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaFuncSetAttribute(attn_decode_tc_kernel<kKStages, kVStages>,
+                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
   const CUtensorMap* tk = kv_tensor_map(k_pool, static_cast<int64_t>(nkv) * head_stride, kBN);
@@ -479,20 +491,20 @@ int launch_attn_decode_tc(const ds_entry* entries_dev, int n_entries, const void
     fprintf(stderr, "K7-tc: %d entries x %d kv heads, %d splits, cluster %d (co-resident %d)\n",
             n_entries, nkv, max_splits, cluster,
             max_splits <= 16 ? tc_max_clusters(max_splits) : 0);
+  auto kern = attn_decode_tc_kernel<kKStages, kVStages>;
   if (cluster)
-    launch_pdl_cluster_z(attn_decode_tc_kernel, grid, dim3(kThreads), kSmemBytes, cluster,
-                         stream, static_cast<const __nv_bfloat16*>(qkv), stride, entries_dev,
-                         n_entries, max_splits, static_cast<const __nv_bfloat16*>(k_pool),
-                         static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv,
-                         sl2, static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride,
-                         *tk, *tv, l2, cluster);
+    launch_pdl_cluster_z(kern, grid, dim3(kThreads), kSmemBytes, cluster, stream,
+                         static_cast<const __nv_bfloat16*>(qkv), stride, entries_dev, n_entries,
+                         max_splits, static_cast<const __nv_bfloat16*>(k_pool),
+                         static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh,
+                         nkv, sl2, static_cast<__nv_bfloat16*>(out), part_o, part_lse,
+                         head_stride, *tk, *tv, l2, cluster);
   else
-    launch_pdl(attn_decode_tc_kernel, grid, dim3(kThreads), kSmemBytes, stream,
+    launch_pdl(kern, grid, dim3(kThreads), kSmemBytes, stream,
                static_cast<const __nv_bfloat16*>(qkv), stride, entries_dev, n_entries, max_splits,
                static_cast<const __nv_bfloat16*>(k_pool),
                static_cast<const __nv_bfloat16*>(v_pool), pos2cell, pos_stride, nh, nkv, sl2,
-               static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride, *tk, *tv,
-               l2, 0);
+               static_cast<__nv_bfloat16*>(out), part_o, part_lse, head_stride, *tk, *tv, l2, 0);
   return (int)cudaGetLastError();
 }
 

@@ -31,7 +31,11 @@ constexpr int kDecodeTcMinRows = 8;
 // up to this many rows (measured cheaper than a launch); more rows use the
 // combine kernel
 constexpr int kDecodeLastMergeRows = 8;
-constexpr int kDecodeTcMinKeys = 4096;
+// measured crossover of the forward at q=5 (tools/sweep_env.sh DS_K7_TC_MIN_KEYS):
+// m=1k 2.85 (mma.sync) vs 2.84 ms (tcgen05, one-stage), m=2k 2.94 vs 2.90,
+// m=4k 3.20 vs 2.99 - the legacy HMMA pipe bounds the mma.sync kernel from
+// ~2k keys on (DS_K7_TC_MIN_KEYS overrides, A/B)
+constexpr int kDecodeTcMinKeys = 2048;
 // K7-tc (R > 8 rows over >= kDecodeTcMinKeys keys) takes at most this many key
 // splits and merges them in ONE (non-portable) cluster through distributed
 // shared memory when the clusters fit the GPU in one wave - no combine launch

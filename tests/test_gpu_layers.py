@@ -85,13 +85,14 @@ def _entries(entries):
     return arr
 
 
-# (4500, 5), (32768, 4), (8192, 3), (5000, 6), (20000, 5) run the tcgen05 K7
-# variant (R > 8 over >= 4k keys); (20000, 5) also takes the > 8-split combine;
+# (4500, 5), (32768, 4), (8192, 3), (5000, 6), (20000, 5), (3000, 5), (2043, 5)
+# run the tcgen05 K7 variant (R > 8 over >= 2k keys; (2040, 5) is the mma.sync
+# side of the threshold); (20000, 5) also takes the > 8-split combine;
 # (1100, 5), (3000, 5), (5000, 6), (8000, 5): R > 8 over <= 8k keys, capped at
 # a cluster's worth of splits (attn_split_plan)
 @pytest.mark.parametrize("past,q_len", [(0, 1), (5, 1), (1000, 1), (3000, 5), (31, 17), (2000, 8), (32768, 4),
                                         (4500, 5), (8192, 3), (5000, 6), (20000, 5), (777, 64), (1100, 5), (8000, 5),
-                                        (0, 150), (2048, 300)])
+                                        (0, 150), (2048, 300), (2040, 5), (2043, 5), (1023, 9)])
 @pytest.mark.parametrize("contiguous", [False, True])
 def test_attention_paged_vs_fp32(cuda, past, q_len, contiguous):
     _attention_case(cuda, past, q_len, contiguous, impl=1)

@@ -25,15 +25,21 @@ kind = _lib.ENTRY_VERIFY if q > 1 else _lib.ENTRY_DECODE
 req = EntryRequest(kind, 0, past, toks[past:past + q], toks, n_draft=q - 1 if q > 1 else 0)
 L = _lib.lib()
 buf = (ctypes.c_ulonglong * (1024 * 8))()
+cbuf = (ctypes.c_longlong * (1024 * 16))()
 res = []
+cres = []
 for rep in range(6):
     ctypes.memset(buf, 0, ctypes.sizeof(buf))
     eng.run([req], count=False)
     L.ds_debug_k7_trace(buf)
+    ctypes.memset(cbuf, 0, ctypes.sizeof(cbuf))
+    L.ds_debug_k7_clk(cbuf)
     a = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 8).astype(np.int64)
     a = a[a[:, 6] > 0]
+    c = np.frombuffer(cbuf, dtype=np.int64).reshape(1024, 16)
     if rep:
         res.append(a)
+        cres.append(c[: len(a)].copy())
 a = res[-1]
 t0 = a[:, 6].min()
 names = {6: "start", 0: "pre-wait", 1: "waited", 2: "tile0", 3: "loop", 7: "osm-wr", 4: "merge", 5: "exit"}
@@ -42,3 +48,17 @@ print(f"past={past} q={q}: {len(a)} CTAs; times (us) relative to the first CTA s
 for i in (6, 0, 1, 2, 3, 7, 4, 5):
     v = (a[:, i] - t0) / 1000.0
     print(f"  {names[i]:9s} {v.min():7.2f} {np.median(v):7.2f} {v.max():7.2f}")
+
+# SM-clock deltas of thread 0 from its dependency wait (cycles -> us at 1.965 GHz)
+c = cres[-1]
+c = c[c[:, 0] > 0]
+cn = {1: "tile0", 2: "max-exch", 3: "P-exch", 4: "PV done", 5: "rows out", 6: "csync1",
+      7: "merged", 8: "csync2"}
+print("thread-0 SM-clock phase ends after the wait (us, median / max over CTAs):")
+for i in range(1, 9):
+    v = c[:, i]
+    ok = v > 0
+    if not ok.any():
+        continue
+    d = (v[ok] - c[ok, 0]) / 1965.0
+    print(f"  {cn[i]:9s} {np.median(d):7.2f} {d.max():7.2f}")
