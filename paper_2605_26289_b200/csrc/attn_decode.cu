@@ -49,13 +49,18 @@ DS_DEVICE unsigned long long gtime() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// (globaltimer reads are slow enough to perturb the phases: only the cross-CTA
+// anchors 6 / 0 / 1 / 5 read it; the phases in between use clock64)
 #define K7_STAMP(i)                                                                        \
-  if (threadIdx.x == 0)                                                                    \
+  if (threadIdx.x == 0 && ((i) == 6 || (i) <= 1 || (i) == 5))                              \
   g_k7_trace[(blockIdx.z * gridDim.y + blockIdx.y) & 1023][i] = gtime()
 // SM-clock stamps of thread 0 (same SM: exact intra-CTA deltas)
 __device__ long long g_k7_clk[1024][16];
 #define K7_CLK(i)                                                                          \
-  if (threadIdx.x == 0) g_k7_clk[(blockIdx.z * gridDim.y + blockIdx.y) & 1023][i] = clock64()
+  do {                                                                                     \
+    __syncwarp();                                                                          \
+    if (threadIdx.x == 0) g_k7_clk[(blockIdx.z * gridDim.y + blockIdx.y) & 1023][i] = clock64(); \
+  } while (0)
 #else
 #define K7_STAMP(i)
 #define K7_CLK(i)
@@ -428,6 +433,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
         }
       }
       K7_STAMP(3);
+#ifdef DS_K7_TRACE
+      {  // trace build: the stamp waits for the PV products (register dependency)
+        float dep = 0.f;
+  #pragma unroll
+        for (int j = 0; j < NT; ++j) dep += o[j][0] + o[j][3];
+        if (dep == 1.2345e30f) g_k7_clk[1023][15] = 1;
+      }
+#endif
       K7_CLK(4);
       // o[j][q]: d = 16w + g (+8 for q >= 2), row 8j + 2t + (q & 1)
   #pragma unroll
@@ -442,6 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
           inv[h] = L > 0.f ? 1.f / L : 0.f;
           lse[h] = L > 0.f ? mref[j][h] + __log2f(L) : -INFINITY;
         }
+        if (j == 0) K7_CLK(9);
   #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int r = 8 * j + 2 * t + (q & 1), d = 16 * warp + g + ((q >> 1) << 3);

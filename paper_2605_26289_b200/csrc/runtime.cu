@@ -467,7 +467,11 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
     // the attention leaves HBM mostly idle (short contexts): K7's producer
     // warps pull wo's weights into L2 for the next projection meanwhile
     // (and the head of gate_up's: DS_GU_L2_MB, continued by wo's own prefetch)
-    static const double wo_l2_frac = getenv("DS_WO_L2_FRAC") ? atof(getenv("DS_WO_L2_FRAC")) : 1.0;
+    // half of wo: the rest streams through the wo CTAs' rings (measured, sweep
+    // of 0 / 0.25 / 0.5 / 1: m=300 q=1 forward 2.76 -> 2.67 ms, m=1k q=1 2.69 ->
+    // 2.62, q=5 2.85 -> 2.84; C2 26.78 -> 26.92 turns/s - the whole of wo
+    // crowded the short attention's own loads)
+    static const double wo_l2_frac = getenv("DS_WO_L2_FRAC") ? atof(getenv("DS_WO_L2_FRAC")) : 0.5;
     static const int64_t gu_l2_bytes = static_cast<int64_t>(
         (getenv("DS_GU_L2_MB") ? atof(getenv("DS_GU_L2_MB")) : 0.0) * 1048576.0) & ~15ll;
     const int64_t gu_head = fused && small ? gu_l2_bytes : 0;
