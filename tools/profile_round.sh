@@ -9,7 +9,7 @@ python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 python bench.py --workload c5 --no-micro --no-cpu > $OUT/bench_ours_c5.json 2> $OUT/bench_ours_c5.err
 python bench.py --workload c4 --steps 1 --warmup 1 --no-micro --no-cpu > $OUT/bench_ours_c4.json 2> $OUT/bench_ours_c4.err
 python bench.py --workload c3 --no-micro > $OUT/bench_ours_c3.json 2> $OUT/bench_ours_c3.err
-python bench.py --workload c1 --model tiny --no-micro > $OUT/bench_ours_c1.json 2> $OUT/bench_ours_c1.err
+python bench.py --workload c1 --model tiny --no-micro --steps 150 > $OUT/bench_ours_c1.json 2> $OUT/bench_ours_c1.err
 python bench.py --impl reference --workload c3 > $OUT/bench_ref_c3.json 2> $OUT/bench_ref_c3.err
 # launch list (cold-cache, serialised; shares only) of a short bench run, steady state
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 3000 -c 1500 --csv \
