@@ -201,7 +201,7 @@ DS_DEVICE uint4 lds128(uint32_t addr) {
 }
 
 template <int MT, int NS>  // NS = k32 steps per math warp per stage (KC = 256*NS)
-__global__ void __launch_bounds__((kGemvWarps + 1) * 32, 1) gemm_ring_kernel(
+__global__ void __launch_bounds__((kGemvWarps + 1) * 32, 2) gemm_ring_kernel(
     void* __restrict__ Y, int M, int N, int K, int y_f32, int accumulate, int n_stages,
     const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
     ds_skinny_epi epi) {
