@@ -755,12 +755,18 @@ DS_DEVICE void epilogue_tokrow(float4 y, const StreamArgs& a, const ds_skinny_ep
 // never touch L2 / HBM (through global memory they cost as much traffic as
 // the weights at these shapes, measured) - then each CTA finishes its share
 // of the chunks with the same fused epilogue.
+template <int kSl>
 __global__ void __launch_bounds__(kThreads, 1) gemm_cluster_kernel(
     StreamArgs a, ds_skinny_epi epi, const __grid_constant__ CUtensorMap tw,
     const __grid_constant__ CUtensorMap tx) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // SW128 atoms
-  const int stage_bytes = kSlabA + a.NT * 128;
+  // a stage = kSl 64-column slabs of both operands (one TMA box each: a
+  // thread issues a box every ~190 ns whatever its size, so the weight rate
+  // of one issuing thread doubles with two-slab boxes; kSl = 1 keeps the ring
+  // small enough for two CTAs per SM)
+  const int w_bytes = kSl * kSlabA, x_slab = a.NT * 128, x_bytes = kSl * x_slab;
+  const int stage_bytes = w_bytes + x_bytes;
   uint8_t* tail = smem + a.stages * stage_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(tail);
   uint64_t* empty = full + a.stages;
@@ -768,24 +774,24 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cluster_kernel(
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
   // epilogue-phase scalars live in the (then idle) ring after the partial tile
   constexpr int kPT = kBM + 4;  // token-major partial row (features + pad)
-  const int ncols_ = (a.NT + 31) & ~31;
-  float* s_inv = reinterpret_cast<float*>(smem + ncols_ * kPT * 4);
+  const int ncols = (a.NT + 31) & ~31, nch = ncols / 32;
+  float* s_inv = reinterpret_cast<float*>(smem + ncols * kPT * 4);
   int* s_pos = reinterpret_cast<int*>(s_inv + kMaxNT);
   int64_t* s_cell = reinterpret_cast<int64_t*>(s_pos + kMaxNT);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = gridDim.x, split = blockIdx.x;  // cluster = the S splits of one tile
   const int wt = blockIdx.y;
-  const int kt = a.kt;
-  const int k_beg = split * kt / S, k_end = (split + 1) * kt / S;
-  const int n = k_end - k_beg;
+  const int n2 = (a.kt + kSl - 1) / kSl;  // stage steps (an odd last slab reads zero-filled)
+  const int s_beg = split * n2 / S, s_end = (split + 1) * n2 / S;
+  const int n = s_end - s_beg;
   unsigned long long* tr =
       a.trace ? a.trace + (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 16 : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = gtimer();
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.stages; ++i) {
-      mbar_init(&full[i], 1);
+      mbar_init(&full[i], 2);  // the weight and the token producer each arrive
       mbar_init(&empty[i], 1);
     }
     mbar_init(acc_full, 1);
@@ -797,29 +803,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cluster_kernel(
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
+  if (tr && threadIdx.x == 0) tr[1] = gtimer();
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (lane == 0) {  // weight boxes: independent of the previous kernel
       tma_prefetch_desc(&tw);
-      tma_prefetch_desc(&tx);
-      const int pre = n < a.stages ? n : a.stages;
-      for (int i = 0; i < pre; ++i) {
-        mbar_expect_tx(&full[i], stage_bytes);
-        tma_load_3d(smem + i * stage_bytes, &tw, 0, wt * kBM, k_beg + i, &full[i]);
-      }
-      pdl_wait();  // the activations come from the previous kernel
-      for (int i = 0; i < pre; ++i)
-        tma_load_3d(smem + i * stage_bytes + kSlabA, &tx, 0, 0, k_beg + i, &full[i]);
-      for (int i = pre; i < n; ++i) {
+      for (int i = 0; i < n; ++i) {
         const int st = i % a.stages;
-        mbar_wait(&empty[st], static_cast<uint32_t>((i / a.stages) - 1) & 1);
-        uint8_t* sp = smem + st * stage_bytes;
-        mbar_expect_tx(&full[st], stage_bytes);
-        tma_load_3d(sp, &tw, 0, wt * kBM, k_beg + i, &full[st]);
-        tma_load_3d(sp + kSlabA, &tx, 0, 0, k_beg + i, &full[st]);
+        if (i >= a.stages) mbar_wait(&empty[st], static_cast<uint32_t>((i / a.stages) - 1) & 1);
+        mbar_expect_tx(&full[st], w_bytes);
+        tma_load_3d(smem + st * stage_bytes, &tw, 0, wt * kBM, kSl * (s_beg + i), &full[st]);
       }
+      if (tr) tr[2] = gtimer();
     }
     __syncwarp();
+  } else if (warp == 2 && lane == 0) {  // token boxes (then this warp joins the epilogue)
+    tma_prefetch_desc(&tx);
+    pdl_wait();  // the activations come from the previous kernel
+    for (int i = 0; i < n; ++i) {
+      const int st = i % a.stages;
+      if (i >= a.stages) mbar_wait(&empty[st], static_cast<uint32_t>((i / a.stages) - 1) & 1);
+      mbar_expect_tx(&full[st], x_bytes);
+      tma_load_3d(smem + st * stage_bytes + w_bytes, &tx, 0, 0, kSl * (s_beg + i), &full[st]);
+    }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_bf16(kBM, a.NT, false);
@@ -828,21 +834,24 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cluster_kernel(
         const int st = i % a.stages;
         mbar_wait(&full[st], static_cast<uint32_t>(i / a.stages) & 1);
         tc::fence_after();
-        const uint32_t pa = base + st * stage_bytes, pb = pa + kSlabA;
+        const uint32_t pa = base + st * stage_bytes, pb = pa + w_bytes;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          tc::mma(tmem, tc::smem_desc(pa + k * 32, 16, 1024), tc::smem_desc(pb + k * 32, 16, 1024),
-                  idesc, (i > 0 || k > 0) ? 1u : 0u);
+        for (int j = 0; j < kSl; ++j)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            tc::mma(tmem, tc::smem_desc(pa + j * kSlabA + k * 32, 16, 1024),
+                    tc::smem_desc(pb + j * x_slab + k * 32, 16, 1024), idesc,
+                    (i > 0 || j > 0 || k > 0) ? 1u : 0u);
         tc::commit(&empty[st]);
       }
       tc::commit(acc_full);
     }
     __syncwarp();
   }
+  __syncwarp();
   // partial tiles token-major in shared memory: [NT tokens][kPT features]
   // (padded row: the thread-per-feature writes and the warp-per-token reads
   // are both bank-conflict free)
-  const int ncols = (a.NT + 31) & ~31, nch = ncols / 32;
   const bool epi_warp = warp >= 2;
   const int quad = warp & 3, r = quad * 32 + lane, half = (warp - 2) >> 2;
   const int et = threadIdx.x - 64;  // 0..255
@@ -869,30 +878,28 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cluster_kernel(
   }
   if (tr && threadIdx.x == 64) tr[5] = gtimer();
   if (epi_warp) {
-    const uint32_t part_u = smem_u32(part);
-    for (int c = (S > 1 ? split : 0); c < nch; c += S) {  // chunk c -> split c mod S
-      const int c0 = c * 32;
-      if (et < 32) {  // per-token scalars of the chunk
-        const int tk = c0 + et, t = tk;
-        if (tk < a.NT && t < a.T) {
-          if (epi.row_ss) {
-            const unsigned long long rs =
-                __ldcg(reinterpret_cast<const unsigned long long*>(epi.row_ss) + t);
-            s_inv[tk] =
-                rsqrtf(__ull2float_rn(rs) / (kSsScale * static_cast<float>(a.K)) + epi.eps);
-          }
-          if (epi.rope) {
-            const int r_pos = __ldg(epi.row_pos + t), r_seq = __ldg(epi.row_seq + t);
-            s_pos[tk] = r_pos;
-            s_cell[tk] =
-                __ldg(epi.pos2cell + static_cast<int64_t>(r_seq) * epi.pos_stride + r_pos);
-          }
-          if (epi.ss_zero && wt == 0) epi.ss_zero[t] = 0;
-        }
+    // split q finishes token rows [rb, re): an equal share for every split
+    const int Tn = a.T < a.NT ? a.T : a.NT;
+    const int rb = split * Tn / S, re = (split + 1) * Tn / S;
+    if (et < re - rb) {  // per-token scalars of the share
+      const int tk = rb + et, t = tk;
+      if (epi.row_ss) {
+        const unsigned long long rs =
+            __ldcg(reinterpret_cast<const unsigned long long*>(epi.row_ss) + t);
+        s_inv[tk] = rsqrtf(__ull2float_rn(rs) / (kSsScale * static_cast<float>(a.K)) + epi.eps);
       }
-      named_bar_sync(1, kEpiThreads);
-      // warp w8 reduces token rows c0 + w8 + 8i (i < 4): all S splits' rows
-      // loaded before the fixed-order sum (deterministic)
+      if (epi.rope) {
+        const int r_pos = __ldg(epi.row_pos + t), r_seq = __ldg(epi.row_seq + t);
+        s_pos[tk] = r_pos;
+        s_cell[tk] = __ldg(epi.pos2cell + static_cast<int64_t>(r_seq) * epi.pos_stride + r_pos);
+      }
+      if (epi.ss_zero && wt == 0) epi.ss_zero[t] = 0;
+    }
+    named_bar_sync(1, kEpiThreads);
+    const uint32_t part_u = smem_u32(part);
+    // warp w8 reduces rows rb + w8 + 8i, four at a time: all S splits' rows
+    // loaded before the fixed-order sum (deterministic)
+    for (int g = rb + w8; g < re; g += 32) {
       float4 acc[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -900,7 +907,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cluster_kernel(
         float4 x[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const uint32_t ad = part_u + static_cast<uint32_t>(((c0 + w8 + 8 * i) * kPT + 4 * lane) * 4);
+          const int tk = g + 8 * i < re ? g + 8 * i : g;
+          const uint32_t ad = part_u + static_cast<uint32_t>((tk * kPT + 4 * lane) * 4);
           x[i] = S > 1 ? dsmem_ld_f32x4(dsmem_map(ad, q))
                        : *reinterpret_cast<const float4*>(smem + (ad - part_u));
         }
@@ -914,11 +922,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_cluster_kernel(
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int tk = c0 + w8 + 8 * i;
-        if (tk < a.NT && tk < a.T)  // warp-uniform
+        const int tk = g + 8 * i;
+        if (tk < re)  // warp-uniform
           epilogue_tokrow(acc[i], a, epi, wt, tk, lane, s_inv, s_pos, s_cell);
       }
-      named_bar_sync(1, kEpiThreads);  // the chunk's scalars are no longer read
     }
   }
   if (tr && threadIdx.x == 64) tr[9] = gtimer();
@@ -980,8 +987,8 @@ int max_clusters(int size, int smem) {
   const int wide = smem > 120 * 1024;
   if (size < 1 || size > 8) return 0;
   if (cache[size][wide]) return cache[size][wide];
-  cudaFuncSetAttribute(gemm_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
-  cudaFuncSetAttribute(gemm_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(gemm_cluster_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  cudaFuncSetAttribute(gemm_cluster_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(size, 1, 1);
   cfg.blockDim = dim3(kThreads);
@@ -994,7 +1001,7 @@ int max_clusters(int size, int smem) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, gemm_cluster_kernel, &cfg) != cudaSuccess || n <= 0) {
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_cluster_kernel<2>, &cfg) != cudaSuccess || n <= 0) {
     cudaGetLastError();
     n = num_sms() / size;
   }
@@ -1092,33 +1099,39 @@ extern "C" int ds_gemm_stream(const void* X, const void* W, void* Y, int T, int 
   // DS_STREAM_CL_BIG=1 (A/B): also one-token-tile shapes with up to two
   // tiles per SM (gate_up at T <= 256: 224 tiles), unsplit, two shallow-ring
   // CTAs per SM
-  static const int cl_big = getenv("DS_STREAM_CL_BIG") ? atoi(getenv("DS_STREAM_CL_BIG")) : 0;
+  static const int cl_big = getenv("DS_STREAM_CL_BIG") ? atoi(getenv("DS_STREAM_CL_BIG")) : 1;
   const bool big = cl_big && p.n_tt == 1 && p.tiles >= num_sms() && p.tiles <= 2 * num_sms();
+  int sl = 2;  // slabs per ring stage
   if (cl_env && p.n_tt == 1 && (p.tiles < num_sms() || big)) {
-    const int stage = kSlabA + p.NT * 128;
     // partial tile + the epilogue scalars (s_inv, s_pos, s_cell) in the ring
     const int64_t part = static_cast<int64_t>((p.NT + 31) & ~31) * (kBM + 4) * 4 +
                          kMaxNT * (4 + 4 + 8);
     const int fixed = 1024 + 256;  // alignment slack + barriers
-    cl_stages = static_cast<int>((part + stage - 1) / stage);
-    if (cl_stages < 3) cl_stages = 3;
-    cl_smem = fixed + cl_stages * stage;
-    // default: the deep ring of one CTA per SM - measured faster than two
-    // shallow-ring CTAs per SM (T=150: wo 15.9 vs 19.4 us, down 30.8 vs 39.2):
-    // the bytes in flight per SM matter more than overlapping the next
-    // kernel's prologue with this one's reduction
-    static const int cl_wide = getenv("DS_STREAM_CL_WIDE") ? atoi(getenv("DS_STREAM_CL_WIDE")) : 1;
-    if (cl_wide && !big) {
-      cl_stages = p.stages;
-      cl_smem = p.smem;
-    }
     if (big) {
-      S = 1;
-    } else if (cl_smem <= kSmemMax) {
-      S = num_sms() / p.tiles;
-      if (S > 8) S = 8;
-      while (S > 1 && p.kt / S < 4) --S;
-      while (S > 1 && max_clusters(S, cl_smem) < p.tiles) --S;
+      // unsplit, two CTAs per SM: single-slab stages, a ring of ~110 KB
+      sl = 1;
+      const int stage = kSlabA + p.NT * 128;
+      cl_stages = static_cast<int>((part + stage - 1) / stage);
+      if (cl_stages < 3) cl_stages = 3;
+      cl_smem = fixed + cl_stages * stage;
+      S = cl_smem <= kSmemMax ? 1 : 0;
+    } else {
+      // two-slab stages (weights 32 KB + tokens NT x 256 B per stage)
+      const int stage = 2 * (kSlabA + p.NT * 128);
+      cl_stages = (kSmemMax - fixed) / stage;
+      if (cl_stages > 4) cl_stages = 4;
+      if (static_cast<int64_t>(cl_stages) * stage < part)
+        cl_stages = static_cast<int>((part + stage - 1) / stage);
+      cl_smem = fixed + cl_stages * stage;
+      if (cl_stages >= 2 && cl_smem <= kSmemMax) {
+        static const int smax = getenv("DS_STREAM_SMAX") ? atoi(getenv("DS_STREAM_SMAX")) : 8;
+        const int n2 = (p.kt + 1) / 2;
+        S = num_sms() / p.tiles;
+        if (S > smax) S = smax;
+        if (S < 1) S = 1;
+        while (S > 1 && n2 / S < 2) --S;
+        while (S > 1 && max_clusters(S, cl_smem) < p.tiles) --S;
+      }
     }
   }
   StreamArgs a{};
@@ -1149,9 +1162,10 @@ extern "C" int ds_gemm_stream(const void* X, const void* W, void* Y, int T, int 
   if (S >= 1) {
     static bool cl_attr = false;
     if (!cl_attr) {
-      cudaFuncSetAttribute(gemm_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kSmemMax);
-      cudaFuncSetAttribute(gemm_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      for (auto k : {gemm_cluster_kernel<1>, gemm_cluster_kernel<2>}) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+        cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      }
       cl_attr = true;
     }
     if (getenv("DS_STREAM_VERBOSE"))
@@ -1179,7 +1193,11 @@ extern "C" int ds_gemm_stream(const void* X, const void* W, void* Y, int T, int 
       }
       a.trace = g_trace;
     }
-    e = cudaLaunchKernelEx(&cfg, gemm_cluster_kernel, a, epi, *tw, *tx);
+    const CUtensorMap* tw2 = slab_tensor_map(W, N, K, kBM, sl);
+    const CUtensorMap* tx2 = slab_tensor_map(X, T, K, p.NT, sl);
+    if (!tw2 || !tx2) return DS_EUNSUPPORTED;
+    e = cudaLaunchKernelEx(&cfg, sl == 1 ? gemm_cluster_kernel<1> : gemm_cluster_kernel<2>, a,
+                           epi, *tw2, *tx2);
     if (e != cudaSuccess) return static_cast<int>(e);
     return static_cast<int>(cudaGetLastError());
   }
