@@ -73,8 +73,11 @@ uint32_t ds_host_fnv1a32_tokens(const int32_t* tokens, int64_t n, uint32_t state
  * K4: paged KV store metadata (UnifiedKvCache kvcache.py:116-286).
  * pos2cell[seq*pos_stride + p] = physical cell of logical position p;
  * member[cell*mask_words + seq/32] bit seq%32 = sequence membership;
- * trie_ref[cell] = references held by radix nodes (radix.py:158-159, 184).
- * Ops are applied strictly in order by one CTA; 0 KV bytes move.
+ * trie_ref[cell] = references held by radix nodes (radix.py:158-159, 184);
+ * map_ref[cell] (optional) = page-table mappings of the cell, exact also when
+ * a sequence maps one cell twice (one membership bit cannot count that).
+ * Ops of one sequence apply in list order (one warp per sequence, across the
+ * grid); 0 KV bytes move.
  * ---------------------------------------------------------------------- */
 typedef struct {
   int32_t kind; /* DS_KV_MAP: pos2cell[seq][pos+i] = cell+i, set member bit;
@@ -94,7 +97,7 @@ typedef struct {
 
 int ds_kv_apply(const ds_kv_op* ops_dev, int n_ops, int32_t* pos2cell, int64_t pos_stride,
                 int n_seqs, uint32_t* member, int mask_words, int32_t* trie_ref,
-                ds_stream_t stream);
+                int32_t* map_ref /* nullable */, ds_stream_t stream);
 
 /* Token-history writes: segment i = {seq, start, len, src_offset} copies
  * src[src_offset : src_offset+len] to hist[seq*pos_stride + start ...]
@@ -117,11 +120,12 @@ int ds_kv_pack_cells(void* k_pool, void* v_pool, int layers, int n_kv_heads, int
                      int head_dim, const int32_t* cells, int n, void* buf, int unpack,
                      ds_stream_t stream);
 
-/* Derived refcount (popcount(member) + trie_ref) and occupancy (cells with
- * refcount > 0) - the device view of kvcache.py:91-100, 185-187. */
+/* Derived refcount (map_ref + trie_ref, or popcount(member) + trie_ref when
+ * map_ref is NULL) and occupancy (cells with refcount > 0) - the device view
+ * of kvcache.py:91-100, 185-187. */
 int ds_kv_refcount(const uint32_t* member, int mask_words, const int32_t* trie_ref,
-                   int64_t capacity, int32_t* refcnt_out, int32_t* occupancy_out,
-                   ds_stream_t stream);
+                   const int32_t* map_ref, int64_t capacity, int32_t* refcnt_out,
+                   int32_t* occupancy_out, ds_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * Model forward: the device realisation of MockEngine.forward

@@ -104,10 +104,10 @@ def lib() -> ctypes.CDLL:
                                             P]),
         "ds_host_fnv1a64_tokens": (c_u64, [P, c_i64, c_u64]),
         "ds_host_fnv1a32_tokens": (ctypes.c_uint32, [P, c_i64, ctypes.c_uint32]),
-        "ds_kv_apply": (c_i32, [P, c_i32, P, c_i64, c_i32, P, c_i32, P, P]),
+        "ds_kv_apply": (c_i32, [P, c_i32, P, c_i64, c_i32, P, c_i32, P, P, P]),
         "ds_hist_write": (c_i32, [P, P, c_i32, P, c_i64, P]),
         "ds_kv_copy_cells": (c_i32, [P, P, c_i32, c_i32, c_i64, c_i32, P, c_i32, P]),
-        "ds_kv_refcount": (c_i32, [P, c_i32, P, c_i64, P, P, P]),
+        "ds_kv_refcount": (c_i32, [P, c_i32, P, P, c_i64, P, P, P]),
         "ds_kv_pack_cells": (c_i32, [P, P, c_i32, c_i32, c_i64, c_i32, P, c_i32, P, c_i32, P]),
         "ds_forward_workspace_bytes": (ctypes.c_size_t, [P, c_i32, c_i32, c_i32]),
         "ds_model_forward": (c_i32, [P, P, P, P]),

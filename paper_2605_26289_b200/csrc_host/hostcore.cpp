@@ -148,9 +148,22 @@ class KvCore {
     }
     emit(KV_TRIE_INC, -1, 0, done);
   }
+  // the device log gets exactly the runs whose drop happened (a run failing
+  // its liveness check raises before it changes anything)
   int64_t decref_runs(const std::vector<Run>& runs) {
-    emit(KV_TRIE_DEC, -1, 0, runs);
-    return drop(runs);
+    std::vector<Run> done;
+    int64_t freed = 0;
+    try {
+      for (const auto& r : runs) {
+        freed += drop(std::vector<Run>{r});
+        done.push_back(r);
+      }
+    } catch (...) {
+      emit(KV_TRIE_DEC, -1, 0, done);
+      throw;
+    }
+    emit(KV_TRIE_DEC, -1, 0, done);
+    return freed;
   }
 
   // -- sequence operations --
@@ -207,9 +220,18 @@ class KvCore {
   void alias_runs(int64_t dest, const std::vector<Run>& runs) {
     const int64_t n = run_cells(runs);
     if (n == 0) return;
+    std::vector<Run> done;
     for (const auto& r : runs) {  // per-run check-then-increment (kvcache.py:248-252)
-      check_live(r, "alias of a dead cell");
+      try {
+        check_live(r, "alias of a dead cell");
+      } catch (...) {
+        // the runs already incremented stay held (reference semantics): the
+        // device mirrors them as holds without a mapping (exact refcount)
+        emit(KV_TRIE_INC, -1, 0, done);
+        throw;
+      }
       for (int64_t c = r.first; c < r.first + r.second; ++c) ++rc_[c];
+      done.push_back(r);
     }
     const int64_t p = append_span(dest, n, runs, false);
     emit(KV_MAP, dest, p, runs);

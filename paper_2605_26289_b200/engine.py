@@ -204,6 +204,9 @@ class GpuEngine:
         self.mask_words = (n_seqs + 31) // 32
         self.member = torch.zeros((self.capacity, self.mask_words), dtype=torch.int32, device=dev)
         self.trie_ref = torch.zeros(self.capacity, dtype=torch.int32, device=dev)
+        # exact page-table mappings per cell (the refcount observable also when
+        # a sequence maps one cell twice)
+        self.map_ref = torch.zeros(self.capacity, dtype=torch.int32, device=dev)
 
         # ---- per-forward buffers ----
         self.max_out = (cfg.spec_max_lookahead + 1) * (n_seqs if cfg.batched_forward else 1)
@@ -364,7 +367,8 @@ class GpuEngine:
         if n_ops:
             check(L.ds_kv_apply(self.stage.dptr(ops_off), n_ops, self.pos2cell.data_ptr(),
                                 self.pos_stride, self.n_seqs, self.member.data_ptr(),
-                                self.mask_words, self.trie_ref.data_ptr(), stream), "ds_kv_apply")
+                                self.mask_words, self.trie_ref.data_ptr(),
+                                self.map_ref.data_ptr(), stream), "ds_kv_apply")
             self.gpu_launches += 1
 
     def flush(self) -> None:
@@ -740,12 +744,14 @@ class GpuEngine:
     # -- diagnostics -------------------------------------------------------------------
 
     def device_refcounts(self) -> tuple[np.ndarray, int]:
-        """popcount(member)+trie_ref per cell and the device occupancy."""
+        """map_ref+trie_ref per cell (page-table mappings + radix holds) and the
+        device occupancy."""
         self.flush()
         rc = torch.empty(self.capacity, dtype=torch.int32, device=self.device)
         occ = torch.zeros(1, dtype=torch.int32, device=self.device)
         check(lib().ds_kv_refcount(self.member.data_ptr(), self.mask_words,
-                                   self.trie_ref.data_ptr(), self.capacity, rc.data_ptr(),
+                                   self.trie_ref.data_ptr(), self.map_ref.data_ptr(),
+                                   self.capacity, rc.data_ptr(),
                                    occ.data_ptr(), torch.cuda.current_stream().cuda_stream),
               "ds_kv_refcount")
         return rc.cpu().numpy(), int(occ.item())

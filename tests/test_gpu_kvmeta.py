@@ -14,7 +14,7 @@ from paper_2605_26289_b200.kvcache import CapacityExhausted, DonorRangeInvalid, 
 pytestmark = pytest.mark.gpu
 
 
-def _apply(cuda, ops, pos2cell, member, trie, n_seqs):
+def _apply(cuda, ops, pos2cell, member, trie, n_seqs, map_ref=None):
     from paper_2605_26289_b200._lib import check, lib
 
     ops = np.asarray(ops, dtype=np.int32).reshape(-1, 5)
@@ -23,16 +23,19 @@ def _apply(cuda, ops, pos2cell, member, trie, n_seqs):
     o = torch.tensor(ops).to(cuda)
     check(lib().ds_kv_apply(o.data_ptr(), len(ops), pos2cell.data_ptr(), pos2cell.shape[1],
                             n_seqs, member.data_ptr(), member.shape[1], trie.data_ptr(),
+                            None if map_ref is None else map_ref.data_ptr(),
                             torch.cuda.current_stream().cuda_stream))
 
 
-def _refcount(cuda, member, trie):
+def _refcount(cuda, member, trie, map_ref=None):
+    """map_ref + trie_ref (exact), or popcount(member) + trie_ref without map_ref."""
     from paper_2605_26289_b200._lib import check, lib
 
     cap = member.shape[0]
     rc = torch.empty(cap, dtype=torch.int32, device=cuda)
     occ = torch.zeros(1, dtype=torch.int32, device=cuda)
-    check(lib().ds_kv_refcount(member.data_ptr(), member.shape[1], trie.data_ptr(), cap,
+    check(lib().ds_kv_refcount(member.data_ptr(), member.shape[1], trie.data_ptr(),
+                               None if map_ref is None else map_ref.data_ptr(), cap,
                                rc.data_ptr(), occ.data_ptr(),
                                torch.cuda.current_stream().cuda_stream))
     return rc.cpu().numpy(), int(occ.item())
@@ -40,7 +43,7 @@ def _refcount(cuda, member, trie):
 
 def test_golden_ops_on_device(cuda):
     cases = load_golden("kvcache_ops.json.gz")
-    checked = 0
+    checked = dup_free = 0
     for case in cases:
         cap = case["capacity"]
         kv = UnifiedKvCache(cap)
@@ -48,6 +51,7 @@ def test_golden_ops_on_device(cuda):
         pos2cell = torch.full((6, cap), -1, dtype=torch.int32, device=cuda)
         member = torch.zeros((cap, 1), dtype=torch.int32, device=cuda)
         trie = torch.zeros(cap, dtype=torch.int32, device=cuda)
+        map_ref = torch.zeros(cap, dtype=torch.int32, device=cuda)
         ever_dup = False
         for op in case["ops"]:
             s = op["seq"]
@@ -68,16 +72,66 @@ def test_golden_ops_on_device(cuda):
                     kv.release_sequence(s)
             except (CapacityExhausted, DonorRangeInvalid, ValueError):
                 pass
-            _apply(cuda, kv.take_ops(), pos2cell, member, trie, 6)
+            _apply(cuda, kv.take_ops(), pos2cell, member, trie, 6, map_ref)
             p2c = pos2cell.cpu().numpy()
             for seq in range(6):
                 n = kv.seq_len(seq)
                 cells = kv.cell_ids(seq, 0, n) if n else []
                 assert p2c[seq, :n].tolist() == cells
                 ever_dup |= len(set(cells)) != len(cells)
-            if not ever_dup:
+            # exact mappings per cell: the refcount holds after every op, also
+            # once a sequence maps a cell twice
+            rc, occ = _refcount(cuda, member, trie, map_ref)
+            assert np.array_equal(rc, kv._refcnt)
+            assert occ == int(np.count_nonzero(kv._refcnt))
+            checked += 1
+            if not ever_dup:  # the membership bits (one per sequence) until then
                 rc, occ = _refcount(cuda, member, trie)
                 assert np.array_equal(rc, kv._refcnt)
-                assert occ == int(np.count_nonzero(kv._refcnt))
-                checked += 1
-    assert checked > 500
+                dup_free += 1
+    assert checked > 500 and dup_free > 500
+
+
+def test_many_sequences_large_flushes(cuda):
+    """The per-sequence parallel apply (one warp per sequence across the grid,
+    atomics on shared membership words and counters) over 300 sequences and
+    flushes of thousands of ops, with cells trimmed and re-allocated inside one
+    flush - page tables and exact refcounts equal the host allocator's."""
+    import random
+
+    rng = random.Random(11)
+    n_seqs, cap = 300, 60000
+    kv = UnifiedKvCache(cap)
+    kv.record_ops = True
+    pos2cell = torch.full((n_seqs, 4096), -1, dtype=torch.int32, device=cuda)
+    member = torch.zeros((cap, (n_seqs + 31) // 32), dtype=torch.int32, device=cuda)
+    trie = torch.zeros(cap, dtype=torch.int32, device=cuda)
+    map_ref = torch.zeros(cap, dtype=torch.int32, device=cuda)
+    for flush in range(12):
+        for _ in range(1500):
+            s = rng.randrange(n_seqs)
+            n = kv.seq_len(s)
+            r = rng.random()
+            try:
+                if r < 0.55 and n < 3000:
+                    kv.append_cells(s, rng.randrange(1, 40))
+                elif r < 0.8 and n:
+                    kv.trim(s, rng.randrange(n))
+                elif r < 0.95 and n:
+                    d = rng.randrange(n_seqs)
+                    if d != s and kv.seq_len(d) == 0:
+                        kv.seq_alias(s, d, 0, rng.randrange(1, n + 1))
+                else:
+                    kv.release_sequence(s)
+            except (CapacityExhausted, DonorRangeInvalid, ValueError):
+                pass
+        ops = kv.take_ops()
+        _apply(cuda, ops, pos2cell, member, trie, n_seqs, map_ref)
+        p2c = pos2cell.cpu().numpy()
+        for seq in range(n_seqs):
+            n = kv.seq_len(seq)
+            if n:
+                assert p2c[seq, :n].tolist() == kv.cell_ids(seq, 0, n)
+        rc, occ = _refcount(cuda, member, trie, map_ref)
+        assert np.array_equal(rc, kv._refcnt)
+        assert occ == int(np.count_nonzero(kv._refcnt))

@@ -22,14 +22,17 @@ class DeviceModel:
         self.pos2cell = np.full((n_seqs, capacity), -1, dtype=np.int64)
         self.member = np.zeros((capacity, n_seqs), dtype=bool)
         self.trie = np.zeros(capacity, dtype=np.int64)
+        self.map_ref = np.zeros(capacity, dtype=np.int64)  # exact mappings per cell
 
     def apply(self, ops):
         for kind, seq, pos, cell, ln in ops:
             if kind == 0:
                 self.pos2cell[seq, pos:pos + ln] = np.arange(cell, cell + ln)
                 self.member[cell:cell + ln, seq] = True
+                self.map_ref[cell:cell + ln] += 1
             elif kind == 1:
                 self.member[cell:cell + ln, seq] = False
+                self.map_ref[cell:cell + ln] -= 1
             elif kind == 2:
                 self.trie[cell:cell + ln] += 1
             else:
@@ -37,6 +40,9 @@ class DeviceModel:
 
     def refcount(self):
         return self.member.sum(1) + self.trie
+
+    def exact_refcount(self):
+        return self.map_ref + self.trie
 
 
 def _observe(kv, seqs):
@@ -84,6 +90,10 @@ def _run_case(case, check_device=True):
             for s2, v in op["obs"]["seqs"].items():
                 assert dev.pos2cell[int(s2), : v["len"]].tolist() == v["cells"]
             ever_dup |= dup
+            # the op log mirrors every refcount change, failed ops included
+            # (a failed decref logs the runs it dropped, a failed alias the
+            # holds it left): exact after every op
+            assert np.array_equal(dev.exact_refcount(), kv._refcnt), op
             if not ever_dup:
                 assert np.array_equal(dev.refcount(), kv._refcnt), op
 
