@@ -340,6 +340,16 @@ int ds_gemm_tc(const void* X, const void* W, void* Y, int T, int N, int K, int y
 int ds_gemm_stream(const void* X, const void* W, void* Y, int T, int N, int K, int y_f32,
                    int accumulate, const ds_skinny_epi* epi, ds_stream_t stream);
 
+/* K11: projection GEMM on CTA pairs (tcgen05.mma.cta_group::2, 256 tokens x
+ * 256 features per tile, persistent, double-buffered TMEM accumulator) for
+ * the compute-bound row counts of prefill chunks and batched plans:
+ * Y[T][N] (+)= X[T][K] . W[N][K]^T, tokens on the MMA M side so the fused
+ * epilogues (epi, as ds_gemm_stream) run per token row.  N % 256 == 0,
+ * K % 64 == 0.  Deterministic (no split-K).  Same boundary as K10
+ * (scheduler.py:652-660). */
+int ds_gemm_pair(const void* X, const void* W, void* Y, int T, int N, int K, int y_f32,
+                 int accumulate, const ds_skinny_epi* epi, ds_stream_t stream);
+
 /* K8: row argmax over fp32 logits (lowest index on ties, engine.py:146-159). */
 int ds_argmax(const float* logits, int n_rows, int vocab, int32_t* out, ds_stream_t stream);
 

@@ -124,6 +124,7 @@ def lib() -> ctypes.CDLL:
         "ds_gemm_skinny_ex": (c_i32, [P, P, P, c_i32, c_i32, c_i32, c_i32, c_i32, P, P]),
         "ds_gemm_tc": (c_i32, [P, P, P, c_i32, c_i32, c_i32, c_i32, c_i32, P]),
         "ds_gemm_stream": (c_i32, [P, P, P, c_i32, c_i32, c_i32, c_i32, c_i32, P, P]),
+        "ds_gemm_pair": (c_i32, [P, P, P, c_i32, c_i32, c_i32, c_i32, c_i32, P, P]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

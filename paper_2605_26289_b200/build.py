@@ -25,7 +25,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-re
 
 SOURCES = ["policy.cu", "kvmeta.cu", "layers.cu", "attn_dispatch.cu", "attn_decode.cu",
            "attn_decode_tc.cu", "attn_prefill_sm100.cu", "gemm_skinny.cu", "gemm_tc.cu",
-           "gemm_stream.cu", "tma.cu",
+           "gemm_stream.cu", "gemm_pair.cu", "tma.cu",
            "runtime.cu"]
 
 

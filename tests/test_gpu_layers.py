@@ -225,10 +225,18 @@ def test_gemm_skinny_vs_fp32(cuda, M, N, K, y_f32, acc):
     assert err < (1e-3 if y_f32 else 1e-2 * ref.abs().max().item()), err
 
 
-def _gemm_ex(L, X, W, Y, M, N, K, y_f32, acc, epi, s):
-    """The forward's GEMM for M rows: skinny (M <= 32) or stream-K K10."""
+def _gemm_ex(L, X, W, Y, M, N, K, y_f32, acc, epi, s, impl="auto"):
+    """The forward's GEMM for M rows: skinny (M <= 32) or stream-K K10; with
+    impl="pair" the CTA-pair K11 (M > 32)."""
+    if impl == "pair":
+        return L.ds_gemm_pair(X, W, Y, M, N, K, y_f32, acc, epi, s)
     f = L.ds_gemm_skinny_ex if M <= 32 else L.ds_gemm_stream
     return f(X, W, Y, M, N, K, y_f32, acc, epi, s)
+
+
+def _skip_pair(impl, M, N):
+    if impl == "pair" and (M <= 32 or N % 256):
+        pytest.skip("K11 serves M > 32 rows, N % 256 == 0")
 
 
 # K10 (persistent stream-K tcgen05, the product GEMM for M > 32): every shape
@@ -267,6 +275,39 @@ def test_gemm_stream_vs_fp32(cuda, T, N, K, y_f32, acc):
         assert torch.equal(Y, Y2)
 
 
+# K11 (CTA-pair tcgen05, persistent, split tail): the same shapes (N % 256),
+# plus multi-wave row counts; deterministic (fixed-order tail partials).
+@pytest.mark.parametrize("T,N,K", [(150, 4096, 4096), (150, 6144, 4096), (150, 28672, 4096),
+                                   (150, 4096, 14336), (33, 1024, 1024), (415, 4096, 4096),
+                                   (881, 1536, 1024), (881, 6144, 4096), (200, 5632, 1024),
+                                   (100, 1024, 2816), (4096, 1024, 4096), (256, 4096, 4096),
+                                   (257, 4096, 4096), (64, 128256, 4096), (512, 4096, 14336),
+                                   (1300, 28672, 4096), (2048, 6144, 4096), (4096, 4096, 4096)])
+@pytest.mark.parametrize("y_f32,acc", [(0, 0), (1, 1)])
+def test_gemm_pair_vs_fp32(cuda, T, N, K, y_f32, acc):
+    from paper_2605_26289_b200._lib import check, lib
+
+    g = torch.Generator(device=cuda).manual_seed(T + N + K)
+    X = torch.randn(T, K, device=cuda, generator=g).bfloat16()
+    W = (0.02 * torch.randn(N, K, device=cuda, generator=g)).bfloat16()
+    Y0 = torch.randn(T, N, device=cuda, generator=g)
+    Y = Y0.clone() if y_f32 else Y0.bfloat16()
+    s = torch.cuda.current_stream().cuda_stream
+    L = lib()
+    check(L.ds_gemm_pair(X.data_ptr(), W.data_ptr(), Y.data_ptr(), T, N, K, y_f32, acc, None, s))
+    torch.cuda.synchronize()
+    ref = X.float() @ W.float().T
+    if acc:
+        ref = ref + (Y0 if y_f32 else Y0.bfloat16().float())
+    err = (Y.float() - ref).abs().max().item()
+    assert err < (2e-3 if y_f32 else 1e-2 * ref.abs().max().item()), err
+    if y_f32:
+        Y2 = Y0.clone()
+        check(L.ds_gemm_pair(X.data_ptr(), W.data_ptr(), Y2.data_ptr(), T, N, K, 1, acc, None, s))
+        torch.cuda.synchronize()
+        assert torch.equal(Y, Y2)
+
+
 # K9 (tcgen05): prefill chunks and batched plans.  Shapes cover one token tile
 # (150 -> N=160), ragged multi-tile (415 -> 2 x 208, 881 -> 4 x 224, 4096), the
 # cluster split-K (wo/down/wqkv-like N with few row tiles) and the tiny model.
@@ -299,7 +340,8 @@ def test_gemm_tc_vs_fp32(cuda, T, N, K, y_f32, acc):
 
 
 @pytest.mark.parametrize("M", [1, 5, 13, 20, 32, 33, 150, 300, 881])
-def test_gemm_skinny_epilogue_fusions(cuda, M):
+@pytest.mark.parametrize("impl", ["auto", "pair"])
+def test_gemm_skinny_epilogue_fusions(cuda, M, impl):
     """ds_gemm_skinny_ex: residual producer (y += X.W^T, h = bf16(y*w_norm),
     per-CTA partial sums of y^2) feeding a norm consumer (row scale
     rsqrt(mean(y^2)+eps)) and a SwiGLU consumer (8-row interleaved gate|up) -
@@ -307,6 +349,7 @@ def test_gemm_skinny_epilogue_fusions(cuda, M):
     unfused path's bf16 storage points."""
     from paper_2605_26289_b200._lib import SkinnyEpi, check, lib
 
+    _skip_pair(impl, M, 512)
     L = lib()
     s = torch.cuda.current_stream().cuda_stream
     H, F, Kin = 2048, 1024, 1024
@@ -324,15 +367,15 @@ def test_gemm_skinny_epilogue_fusions(cuda, M):
     prod = SkinnyEpi(ss_out=ss.data_ptr(), ss_zero=other.data_ptr(), h_out=h.data_ptr(),
                      h_w=nw.data_ptr())
     check(_gemm_ex(L, Xin.data_ptr(), Wo.data_ptr(), x.data_ptr(), M, H, Kin, 1, 1,
-                   ctypes.byref(prod), s))
+                   ctypes.byref(prod), s, impl))
     act = torch.empty(M, F, device=cuda, dtype=torch.bfloat16)
     cons = SkinnyEpi(row_ss=ss.data_ptr(), eps=1e-5, swiglu=1)
     check(_gemm_ex(L, h.data_ptr(), Wgu.data_ptr(), act.data_ptr(), M, 2 * F, H, 0, 0,
-                   ctypes.byref(cons), s))
+                   ctypes.byref(cons), s, impl))
     q = torch.empty(M, 512, device=cuda, dtype=torch.bfloat16)
     cons2 = SkinnyEpi(row_ss=ss.data_ptr(), eps=1e-5)
     check(_gemm_ex(L, h.data_ptr(), Wgu[:512].contiguous().data_ptr(), q.data_ptr(), M,
-                   512, H, 0, 0, ctypes.byref(cons2), s))
+                   512, H, 0, 0, ctypes.byref(cons2), s, impl))
     torch.cuda.synchronize()
     x_ref = x0 + Xin.float() @ Wo.float().T
     assert (x - x_ref).abs().max().item() < 1e-3
@@ -351,13 +394,15 @@ def test_gemm_skinny_epilogue_fusions(cuda, M):
 
 
 @pytest.mark.parametrize("M", [1, 5, 6, 17, 32, 33, 100, 300])
-def test_gemm_skinny_argmax_epilogue(cuda, M):
+@pytest.mark.parametrize("impl", ["auto", "pair"])
+def test_gemm_skinny_argmax_epilogue(cuda, M, impl):
     """Fused LM-head argmax (ds_skinny_epi.argmax_out): the
     packed per-row key decodes to np.argmax of the same kernel's fp32 product
     (largest value, lowest column on exact ties - duplicated weight rows make
     bit-identical columns), with and without the product stored."""
     from paper_2605_26289_b200._lib import SkinnyEpi, check, lib
 
+    _skip_pair(impl, M, 128256)
     L = lib()
     s = torch.cuda.current_stream().cuda_stream
     V, H = 128256, 4096
@@ -370,11 +415,11 @@ def test_gemm_skinny_argmax_epilogue(cuda, M):
     keys = torch.zeros(R, device=cuda, dtype=torch.int64)
     epi = SkinnyEpi(argmax_out=keys.data_ptr())
     check(_gemm_ex(L, X.data_ptr(), W.data_ptr(), Y.data_ptr(), M, V, H, 1, 0,
-                   ctypes.byref(epi), s))
+                   ctypes.byref(epi), s, impl))
     keys2 = torch.zeros(R, device=cuda, dtype=torch.int64)
     epi2 = SkinnyEpi(argmax_out=keys2.data_ptr())
     check(_gemm_ex(L, X.data_ptr(), W.data_ptr(), None, M, V, H, 1, 0,
-                   ctypes.byref(epi2), s))
+                   ctypes.byref(epi2), s, impl))
     torch.cuda.synchronize()
     idx = (0xFFFFFFFF - (keys[:M] & 0xFFFFFFFF)).cpu()
     assert torch.equal(idx, Y.argmax(-1).cpu())  # torch: first maximal index
@@ -387,7 +432,8 @@ def test_gemm_skinny_argmax_epilogue(cuda, M):
 
 @pytest.mark.parametrize("M", [1, 5, 17, 32, 48, 150, 300])
 @pytest.mark.parametrize("norm", [False, True])
-def test_gemm_skinny_rope_kv_epilogue(cuda, M, norm):
+@pytest.mark.parametrize("impl", ["auto", "pair"])
+def test_gemm_skinny_rope_kv_epilogue(cuda, M, norm, impl):
     """ds_gemm_skinny_ex rope mode (wqkv projection + RoPE + KV store, the
     decode forward's K5 fusion) vs torch: qkv = bf16(X.W^T) in the wqkv
     RoPE-pair interleaved layout, un-permuted, rotated, q to Y, k/v into the
@@ -396,6 +442,7 @@ def test_gemm_skinny_rope_kv_epilogue(cuda, M, norm):
 
     nh, nkv, d, H = 8, 2, 128, 1024
     QKV = (nh + 2 * nkv) * d
+    _skip_pair(impl, M, QKV)
     g = torch.Generator(device="cpu").manual_seed(M + 100 * norm)
     X = torch.randn(M, H, generator=g).bfloat16()
     W = (0.05 * torch.randn(QKV, H, generator=g)).bfloat16()
@@ -425,7 +472,7 @@ def test_gemm_skinny_rope_kv_epilogue(cuda, M, norm):
                     rope_sin=sd.data_ptr(), k_pool_l=kp.data_ptr(), v_pool_l=vp.data_ptr(),
                     kv_head_stride=head_stride)
     check(_gemm_ex(lib(), Xd.data_ptr(), Wd.data_ptr(), Y.data_ptr(), M, QKV, H, 0, 0,
-                   ctypes.byref(epi), torch.cuda.current_stream().cuda_stream))
+                   ctypes.byref(epi), torch.cuda.current_stream().cuda_stream, impl))
     torch.cuda.synchronize()
     qkv = unpermute_qk(_bf((X.float() @ W.float().T) * scale[:, None]), nh, nkv, d).float()
     from oracle.llama_ref import rope
