@@ -50,7 +50,7 @@ constexpr int kPN = 256;                 // features per tile (128 loaded per CT
 constexpr int kBoxA = kPM * 128;         // 16 KB: 128 token rows x 64 columns
 constexpr int kBoxB = (kPN / 2) * 128;   // 16 KB: 128 weight rows x 64 columns
 constexpr int kStage = kBoxA + kBoxB;
-constexpr int kPairThreads = 7 * 32;
+constexpr int kPairThreads = 11 * 32;  // producers 0 / 6, MMA 1, epilogue 2-5 + 7-10
 constexpr int kPairSmemMax = 227 * 1024;
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // leader's barrier in the shared::cluster window
 
@@ -297,6 +297,90 @@ DS_DEVICE void pair_epilogue(float* v, const PairArgs& a, const ds_skinny_epi& e
   }
 }
 
+// plain / residual outputs through a per-warp transpose: the warp's 32 token
+// rows x 32 features staged in shared memory, then 8 lanes per row move one
+// contiguous 128-byte fp32 (64-byte bf16) row segment, 4 rows per
+// instruction - the residual read-modify-write and the h stores are whole
+// segments (thread-per-row 16-byte pieces left the epilogue exposed at the
+// end of the GEMM: +30 us on wo at 4096 rows).  Row sums of x^2 collect in
+// ss_acc[32] (one global atomic per row and tile).
+constexpr int kStgP = 33;  // staging row stride (floats): conflict-free both ways
+DS_DEVICE void pair_store_staged(const float* v, const PairArgs& a, const ds_skinny_epi& epi,
+                                 int t0w, int f0, float* stg, long long* ss_acc, int lane) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) stg[lane * kStgP + j] = v[j];
+  __syncwarp();
+  const int g = lane & 7, rr = lane >> 3;
+  float4 hw4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  const bool h = epi.ss_out && epi.h_out && epi.h_w;
+  if (h) {
+    const uint2 hu = __ldg(reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(epi.h_w) + f0 + 4 * g));
+    const float2 h0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hu.x));
+    const float2 h1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hu.y));
+    hw4 = make_float4(h0.x, h0.y, h1.x, h1.y);
+  }
+  float4 y4[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float* sp = stg + (rr + 4 * i) * kStgP + 4 * g;
+    y4[i] = make_float4(sp[0], sp[1], sp[2], sp[3]);
+  }
+  if (a.accumulate) {  // every old value in flight before the first use
+    float4 old[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int t = t0w + rr + 4 * i;
+      const int64_t o = static_cast<int64_t>(t) * a.N + f0 + 4 * g;
+      old[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t < a.T) {
+        if (a.y_f32) {
+          old[i] = *reinterpret_cast<const float4*>(static_cast<const float*>(a.Y) + o);
+        } else {
+          const uint2 u = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(a.Y) + o);
+          const float2 p0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+          const float2 p1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+          old[i] = make_float4(p0.x, p0.y, p1.x, p1.y);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      y4[i].x += old[i].x;
+      y4[i].y += old[i].y;
+      y4[i].z += old[i].z;
+      y4[i].w += old[i].w;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = rr + 4 * i, t = t0w + row;
+    const bool ok = t < a.T;
+    const int64_t o = static_cast<int64_t>(t) * a.N + f0 + 4 * g;
+    float4 y = y4[i];
+    if (ok) {
+      if (a.y_f32) {
+        *reinterpret_cast<float4*>(static_cast<float*>(a.Y) + o) = y;
+      } else {
+        y = make_float4(bf16r(y.x), bf16r(y.y), bf16r(y.z), bf16r(y.w));
+        *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.Y) + o) = make_uint2(pk(y.x, y.y), pk(y.z, y.w));
+      }
+    }
+    if (epi.ss_out) {
+      if (ok && h)
+        *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(epi.h_out) + o) =
+            make_uint2(pk(y.x * hw4.x, y.y * hw4.y), pk(y.z * hw4.z, y.w * hw4.w));
+      long long q = ok ? __float2ll_rn(y.x * y.x * kSsScale) + __float2ll_rn(y.y * y.y * kSsScale) +
+                             __float2ll_rn(y.z * y.z * kSsScale) + __float2ll_rn(y.w * y.w * kSsScale)
+                       : 0ll;
+#pragma unroll
+      for (int m = 4; m >= 1; m >>= 1)
+        q += static_cast<long long>(__shfl_xor_sync(0xffffffffu, static_cast<unsigned long long>(q), m));
+      if (g == 0) ss_acc[row] += q;
+    }
+  }
+  __syncwarp();  // the staging tile is reused by the next chunk
+}
+
 __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
     PairArgs a, const ds_skinny_epi epi, const __grid_constant__ CUtensorMap tx,
     const __grid_constant__ CUtensorMap tw) {
@@ -307,6 +391,8 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
   uint64_t* acc_full = empty + a.stages;  // [2]
   uint64_t* acc_empty = acc_full + 2;     // [2] (the leader's are used)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  // per epilogue warp: a [32][kStgP] fp32 staging tile and 32 int64 row sums
+  uint8_t* stg_base = smem + a.stages * kStage + 256;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -321,7 +407,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 8);  // 4 epilogue warps x 2 CTAs
+      mbar_init(&acc_empty[i], 16);  // 8 epilogue warps x 2 CTAs
     }
     mbar_fence_init();
   }
@@ -394,12 +480,21 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
       }
     }
     __syncwarp();
-  } else if (warp >= 2 && warp <= 5) {
+  } else if (warp >= 2 && warp != 6) {
     // ---- epilogue: thread = token row of this CTA, 32 features per load ----
     pdl_wait();  // the residual / previous contents of Y
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
-    const int et = threadIdx.x - 64;  // 0..127
+    // two warps per TMEM lane quadrant (warps 2-5, 7-10), alternate 32-feature
+    // chunks: the epilogue's dependent loads (residual rows) run twice as wide
+    const int half = warp >= 7;
+    const int et = (warp - 2 - half) * 32 + lane;  // 0..255
+    const int ew = et >> 5;                          // epilogue warp 0..7
+    float* stg = reinterpret_cast<float*>(stg_base + ew * (32 * kStgP * 4 + 32 * 8));
+    long long* ss_acc = reinterpret_cast<long long*>(stg + 32 * kStgP);
+    const bool staged = !(epi.rope || epi.swiglu || epi.argmax_out);
+    ss_acc[lane] = 0;
+    __syncwarp();
     int* my_flag = a.flags + pair * 2 + rank;
     float* my_part = a.partials + (static_cast<int64_t>(pair) * 2 + rank) * kPM * kPN;
     const int ns_ = n_segs(a, pair);
@@ -417,7 +512,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
         // partial layout [chunk][float4 j][row]: a warp's store is 512 contiguous bytes
         float4* pr = reinterpret_cast<float4*>(my_part) + r;
 #pragma unroll 1
-        for (int c = 0; c < kPN / 32; ++c) {
+        for (int c = half; c < kPN / 32; c += 2) {
           float v[32];
           tc::ld32(taddr + c * 32, v);
 #pragma unroll
@@ -434,7 +529,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
             arrive_leader(&acc_empty[acc]);
         }
         __threadfence();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, 256);
         if (et == 0) st_release_gpu(my_flag, 1);
         continue;
       }
@@ -444,7 +539,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
       if (q_last >= q_first) {
         if (et < q_last - q_first + 1)
           while (ld_acquire_gpu(a.flags + (q_first + et) * 2 + rank) == 0) __nanosleep(64);
-        named_bar_sync(1, 128);
+        named_bar_sync(1, 256);
       }
       RowCtx rc{};
       rc.inv = 1.f;
@@ -458,10 +553,10 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
           const int sq = __ldg(epi.row_seq + t);
           rc.cell = __ldg(epi.pos2cell + static_cast<int64_t>(sq) * epi.pos_stride + rc.pos);
         }
-        if (epi.ss_zero && nt == 0) epi.ss_zero[t] = 0;
+        if (epi.ss_zero && nt == 0 && !half) epi.ss_zero[t] = 0;
       }
 #pragma unroll 1
-      for (int c = 0; c < kPN / 32; ++c) {
+      for (int c = half; c < kPN / 32; c += 2) {
         float v[32];
         tc::ld32(taddr + c * 32, v);
         for (int q = q_first; q <= q_last; ++q) {  // fixed k order: deterministic
@@ -477,8 +572,21 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
             v[4 * j + 3] += x.w;
           }
         }
+        if (staged) {
+          if (epi.row_ss) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] *= rc.inv;
+          }
+          pair_store_staged(v, a, epi, t - lane, nt * kPN + c * 32, stg, ss_acc, lane);
+          continue;
+        }
         if (t >= a.T) continue;
         pair_epilogue(v, a, epi, t, nt * kPN + c * 32, rc);
+      }
+      if (staged && epi.ss_out) {
+        __syncwarp();
+        rc.ssq = ss_acc[lane];
+        ss_acc[lane] = 0;
       }
       if (t < a.T) {
         if (epi.ss_out)
@@ -495,7 +603,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
           arrive_leader(&acc_empty[acc]);
       }
       if (q_last >= q_first) {  // re-arm the participants' flags (their partials are read)
-        named_bar_sync(1, 128);
+        named_bar_sync(1, 256);
         if (et < q_last - q_first + 1) a.flags[(q_first + et) * 2 + rank] = 0;
       }
     }
@@ -510,6 +618,39 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
 }
 }  // namespace
 
+}  // namespace ds
+
+namespace ds {
+// tail partials + flags for every pair the GPU holds: allocated once per
+// device (outside any graph capture: the runtime reserves it at init), flags
+// self re-arming
+struct PairWorkspace {
+  float* ws = nullptr;
+  int* flags = nullptr;
+  int pairs = 0;
+  int device = -1;
+};
+PairWorkspace& pair_workspace() {
+  static thread_local PairWorkspace w;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (w.device != dev) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int pairs = sms / 2 > 0 ? sms / 2 : 74;
+    w = PairWorkspace{};
+    if (cudaMalloc(&w.ws, static_cast<size_t>(pairs) * 2 * kPM * kPN * 4) == cudaSuccess &&
+        cudaMalloc(&w.flags, static_cast<size_t>(pairs) * 2 * 4) == cudaSuccess &&
+        cudaMemset(w.flags, 0, static_cast<size_t>(pairs) * 2 * 4) == cudaSuccess) {
+      w.pairs = pairs;
+      w.device = dev;
+    } else {
+      cudaGetLastError();
+    }
+  }
+  return w;
+}
+void gemm_pair_reserve() { (void)pair_workspace(); }
 }  // namespace ds
 
 extern "C" int ds_gemm_pair(const void* X, const void* W, void* Y, int T, int N, int K, int y_f32,
@@ -534,7 +675,7 @@ extern "C" int ds_gemm_pair(const void* X, const void* W, void* Y, int T, int N,
   a.tiles = (N / kPN) * a.n_tt;
   a.kt = K / 64;
   static const int st_env = getenv("DS_PAIR_STAGES") ? atoi(getenv("DS_PAIR_STAGES")) : 0;
-  const int fixed = 1024 + 256;
+  const int fixed = 1024 + 256 + 8 * (32 * kStgP * 4 + 32 * 8);  // + epilogue staging
   int ns = (kPairSmemMax - fixed) / kStage;
   if (st_env > 1 && st_env < ns) ns = st_env;
   a.stages = ns;
@@ -565,25 +706,10 @@ extern "C" int ds_gemm_pair(const void* X, const void* W, void* Y, int T, int N,
     if (a.split < 1) a.split = 1;
   }
   if (a.full_waves == 0) pairs = a.rem * a.split;  // only the tail: idle pairs not launched
-  // stream-K partials + flags: allocated once, flags self re-arming
-  static float* ws = nullptr;
-  static int* flags = nullptr;
-  static int ws_pairs = 0;
-  if (pairs > ws_pairs) {
-    if (ws) cudaFree(ws);
-    if (flags) cudaFree(flags);
-    ws = nullptr;
-    flags = nullptr;
-    if (cudaMalloc(&ws, static_cast<size_t>(pairs) * 2 * kPM * kPN * 4) != cudaSuccess ||
-        cudaMalloc(&flags, static_cast<size_t>(pairs) * 2 * 4) != cudaSuccess ||
-        cudaMemset(flags, 0, static_cast<size_t>(pairs) * 2 * 4) != cudaSuccess) {
-      ws_pairs = 0;
-      return DS_EWORKSPACE;
-    }
-    ws_pairs = pairs;
-  }
-  a.partials = ws;
-  a.flags = flags;
+  PairWorkspace& w = pair_workspace();
+  if (!w.ws || pairs > w.pairs) return DS_EWORKSPACE;
+  a.partials = w.ws;
+  a.flags = w.flags;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs, 1, 1);
   cfg.blockDim = dim3(kPairThreads);

@@ -19,6 +19,7 @@
 
 namespace ds {
 
+void gemm_pair_reserve();  // gemm_pair.cu: K11's tail workspace
 void set_attn_l2_prefetch(const void* ptr, int64_t bytes, const void* ptr2 = nullptr,
                           int64_t bytes2 = 0);
 int launch_attn_split(const void* qkv, const ds_entry* entries_host, const ds_entry* entries_dev,
@@ -68,6 +69,7 @@ Runtime& runtime() {
     cudaStreamCreateWithFlags(&rt.gs, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&rt.g_in, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&rt.g_out, cudaEventDisableTiming);
+    gemm_pair_reserve();  // K11's tail workspace, before any graph capture
     rt.device = dev;
   }
   return rt;
@@ -159,12 +161,24 @@ bool use_stream_head() {
   return v;
 }
 
+// K11 (CTA-pair tcgen05 GEMM with the fused epilogues) from DS_PAIR_MIN_ROWS
+// rows (opt-in, unset / 0: off).  Measured: a tie with
+// the library GEMM + unfused kernels on whole 2k / 4k-row prefill forwards
+// (26.56 vs 26.86 ms, 53.67 vs 53.79), 2% behind on C5's batched prefill
+// (3,130-3,140 vs 3,080 ms per step), behind below ~1k rows
+int pair_min_rows() {
+  static const int v = getenv("DS_PAIR_MIN_ROWS") ? atoi(getenv("DS_PAIR_MIN_ROWS")) : 0;
+  return v > 0 ? v : 1 << 30;
+}
+bool pair_ok(int M, int N, int K) { return M >= pair_min_rows() && N % 256 == 0 && K % 64 == 0; }
+
 // decode / verify row counts stream the weights through our skinny GEMM;
 // prefill chunks and batched plans through the stream-K tcgen05 GEMM (K10).
 int project(cublasHandle_t h, const void* X, const void* W, void* Y, int M, int N, int K,
             bool y_f32, bool accumulate, cudaStream_t s) {
   if (M <= 32 && N % 16 == 0 && K % 256 == 0)
     return ds_gemm_skinny(X, W, Y, M, N, K, y_f32, accumulate, s);
+  if (pair_ok(M, N, K)) return ds_gemm_pair(X, W, Y, M, N, K, y_f32, accumulate, nullptr, s);
   if (use_stream_gemm() && N % 128 == 0 && K % 64 == 0)
     return ds_gemm_stream(X, W, Y, M, N, K, y_f32, accumulate, nullptr, s);
   // DS_GEMM_TC=1 (with DS_GEMM_STREAM=0): K9, the earlier data-parallel
@@ -419,15 +433,20 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
   // the fused epilogues: skinny GEMM (T <= 32) or the stream-K tcgen05 GEMM
   // (K10, larger T) - the same ds_skinny_epi fusions either way
   const bool small = T <= 32;
+  // M > 32: K11 from pair_min_rows() rows (every projection N % 256), else K10
+  // when opted in, else the library GEMM + the unfused kernels
+  const bool pair = !small && T >= pair_min_rows() && T <= kMaxSsRows && QKV % 256 == 0 &&
+                    H % 256 == 0 && (2 * F) % 256 == 0 && (nh * hd) % 64 == 0 && F % 64 == 0;
   const bool fused = hd == 128 && QKV % 16 == 0 &&
                      (small ? (H % 256 == 0 && F % 256 == 0 && (nh * hd) % 256 == 0)
-                            : (use_stream_gemm() && T <= kMaxSsRows && QKV % 128 == 0 &&
-                               H % 128 == 0 && (2 * F) % 128 == 0 && (nh * hd) % 64 == 0 &&
-                               F % 64 == 0));
+                            : pair || (use_stream_gemm() && T <= kMaxSsRows && QKV % 128 == 0 &&
+                                       H % 128 == 0 && (2 * F) % 128 == 0 &&
+                                       (nh * hd) % 64 == 0 && F % 64 == 0));
   auto gemm_ex = [&](const void* X, const void* W, void* Y, int N, int K, int y_f32, int acc,
                      const ds_skinny_epi* e) {
     return small ? ds_gemm_skinny_ex(X, W, Y, T, N, K, y_f32, acc, e, stream)
-                 : ds_gemm_stream(X, W, Y, T, N, K, y_f32, acc, e, stream);
+                 : pair ? ds_gemm_pair(X, W, Y, T, N, K, y_f32, acc, e, stream)
+                        : ds_gemm_stream(X, W, Y, T, N, K, y_f32, acc, e, stream);
   };
   // two ss buffers, each producer clearing the one its consumer already read
   // (wo clears ss_attn, read by this layer's wqkv; down clears ss_mlp)
@@ -553,6 +572,8 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
     void* lg = a->logits_out ? a->logits : nullptr;
     if (a->n_out <= 32)
       DS_CHECK(ds_gemm_skinny_ex(b.hf, m->lm_head, lg, a->n_out, m->vocab, H, 1, 0, &eh, stream));
+    else if (pair_ok(a->n_out, m->vocab, H))
+      DS_CHECK(ds_gemm_pair(b.hf, m->lm_head, lg, a->n_out, m->vocab, H, 1, 0, &eh, stream));
     else
       DS_CHECK(ds_gemm_stream(b.hf, m->lm_head, lg, a->n_out, m->vocab, H, 1, 0, &eh, stream));
   } else {
