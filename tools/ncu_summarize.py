@@ -57,7 +57,7 @@ def main(tag: str) -> None:
           "Captured with `tools/profile_round.sh` under gpurun on one B200 "
           "(`ncu --set full --clock-control none`); numbers per launch.\n"]
     for name in ("ncu_gemm_ring", "ncu_k7_decode", "ncu_k7_decode_q1", "ncu_k6_prefill",
-                 "ncu_k10_cluster"):
+                 "ncu_k10_cluster", "ncu_k11_pair", "ncu_cublas_gu4096"):
         rep = os.path.join(OUT, name + ".ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -116,7 +116,7 @@ def main(tag: str) -> None:
         summary["gemm_ring_dram"] = [[r["dram__bytes_read.sum"], r["dram__bytes_write.sum"]]
                                      for r in g]
     for f in ("timeline_verify_m1000.txt", "timeline_prefill_m1000.txt", "fwd_time.txt",
-              "forward_critical_path.txt"):
+              "forward_critical_path.txt", "bench_gemm_pair.txt", "bench_gemm_pair_epi.txt"):
         src = os.path.join(OUT, f)
         if os.path.exists(src):
             with open(src) as fi, open(os.path.join(dst, f), "w") as fo:

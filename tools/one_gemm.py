@@ -1,4 +1,5 @@
-"""Run one projection shape through ds_gemm_stream (or cuBLAS) a few times - for ncu."""
+"""Run one projection shape through ds_gemm_stream (k10), ds_gemm_pair (k11) or cuBLAS a
+few times - for ncu.  Usage: one_gemm.py T N K [reps] [k10|k11|cublas]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -16,6 +17,9 @@ for _ in range(reps):
     if impl == "k10":
         check(lib().ds_gemm_stream(X.data_ptr(), W.data_ptr(), Y.data_ptr(), T, N, K, 0, 0, None,
                                    s.cuda_stream))
+    elif impl == "k11":
+        check(lib().ds_gemm_pair(X.data_ptr(), W.data_ptr(), Y.data_ptr(), T, N, K, 0, 0, None,
+                                 s.cuda_stream))
     else:
         torch.matmul(X, W.T, out=Y)
 torch.cuda.synchronize()

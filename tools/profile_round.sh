@@ -35,5 +35,12 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 20000 -
 # K10 (opt-in stream-K GEMM) on the prefill qkv shape, for the record
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:gemm_cluster -s 2 -c 1 \
   -o $OUT/ncu_k10_cluster python tools/one_gemm.py 150 6144 4096 4 > /dev/null 2>&1
+# K11 (opt-in CTA-pair GEMM) on the 4k-row gate_up shape, and cuBLAS on the same shape
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:gemm_pair -s 2 -c 1 \
+  -o $OUT/ncu_k11_pair python tools/one_gemm.py 4096 28672 4096 4 k11 > /dev/null 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:nvjet -s 2 -c 1 \
+  -o $OUT/ncu_cublas_gu4096 python tools/one_gemm.py 4096 28672 4096 4 cublas > /dev/null 2>&1
+python tools/bench_gemm_pair.py 881 2048 4096 > $OUT/bench_gemm_pair.txt 2>&1
+python tools/bench_gemm_pair_epi.py 4096 > $OUT/bench_gemm_pair_epi.txt 2>&1
 python tools/fwd_time.py llama3-8b 1000:5 2048:5 8192:5 32768:5 1000:1 32768:1 1000:150 > $OUT/fwd_time.txt 2>&1
 ls -la $OUT
