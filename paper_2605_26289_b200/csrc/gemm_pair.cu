@@ -60,7 +60,8 @@ struct PairArgs {
   int* flags;       // [pairs][2]: partial written (self re-arming)
   int T, N, K, y_f32, accumulate;
   int n_tt, tiles, kt, stages;
-  int full_waves, rem, split;  // tiles = full_waves * pairs + rem; tail tiles split `split` ways
+  int full_waves, rem, split;  // tiles = full_waves * groups + rem; tail tiles split `split` ways
+  int G;                       // pairs per cluster sharing the token tile (1, or 2: multicast)
 };
 
 // segment `idx` of pair `pair`: the full-wave tiles round-robin (concurrent
@@ -98,6 +99,16 @@ DS_DEVICE void tma_load_3d_pair(void* dst, const CUtensorMap* map, int c0, int c
       "r"(smem_u32(bar) & kPeerMask)
       : "memory");
 }
+// the same, multicast to the cluster CTAs in `mask` (each pair's leader barrier)
+DS_DEVICE void tma_load_3d_pair_mc(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                   uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(smem_u32(bar) & kPeerMask), "h"(mask)
+      : "memory");
+}
 DS_DEVICE void alloc_pair(uint32_t* smem_dst, uint32_t cols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                    smem_u32(smem_dst)),
@@ -117,12 +128,13 @@ DS_DEVICE void mma_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint3
       "}\n" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
-// every prior MMA of this thread complete -> one arrive on `bar` in both CTAs
-DS_DEVICE void commit_pair(uint64_t* bar) {
+// every prior MMA of this thread complete -> one arrive on `bar` in the
+// cluster CTAs of `mask`
+DS_DEVICE void commit_pair(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
       "[%0], %1;\n" ::"r"(smem_u32(bar)),
-      "h"(static_cast<uint16_t>(3))
+      "h"(mask)
       : "memory");
 }
 DS_DEVICE int ld_acquire_gpu(const int* p) {
@@ -133,8 +145,8 @@ DS_DEVICE int ld_acquire_gpu(const int* p) {
 DS_DEVICE void st_release_gpu(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
-DS_DEVICE void arrive_leader(uint64_t* bar) {  // arrive on the leader CTA's copy of `bar`
-  const uint32_t ra = dsmem_map(smem_u32(bar), 0);
+DS_DEVICE void arrive_leader(uint64_t* bar, uint32_t leader_rank) {  // the pair leader's copy
+  const uint32_t ra = dsmem_map(smem_u32(bar), leader_rank);
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(ra)
                : "memory");
 }
@@ -395,15 +407,24 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
   uint8_t* stg_base = smem + a.stages * kStage + 256;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
+  // cluster = G CTA pairs; the pairs of a cluster work on adjacent weight
+  // tiles of the SAME token tile, each CTA loading 1/G of the token rows for
+  // all (multicast): the L2 -> SM token traffic drops by G
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank & 1;             // rank in the pair
+  const int gp = static_cast<int>(crank >> 1);  // pair in the cluster
   const bool leader = rank == 0;
-  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const uint32_t leader_rank = crank & ~1u;
+  const uint16_t pair_mask = static_cast<uint16_t>(3u << (2 * gp));
+  const uint16_t all_mask = static_cast<uint16_t>((1u << (2 * a.G)) - 1);
+  const int grp = blockIdx.x / (2 * a.G), n_grp = gridDim.x / (2 * a.G);
+  const int pair = grp * a.G + gp;  // global pair id (partial slots, flags)
   const int kt = a.kt;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.stages; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], a.G);  // every pair sharing the token stage releases it
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
@@ -413,7 +434,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
   }
   if (warp == 1) alloc_pair(tmem_slot, 512);
   tc::fence_before();
-  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  cluster_sync_all();  // barriers initialised and TMEM allocated in every CTA
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -425,13 +446,15 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
     if (lane == 0) {
       const bool is_w = warp == 6;
       tma_prefetch_desc(is_w ? &tw : &tx);
-      const int ns_ = n_segs(a, pair);
+      const int ns_ = n_segs(a, grp);
       int it = 0;
       bool waited = false;
+      const int xrows = kPM / a.G;  // token rows this CTA loads (for every pair)
+      const uint16_t x_mask = static_cast<uint16_t>((1u << rank) | (1u << (2 + rank)));
       for (int q = 0; q < ns_; ++q) {
-        const Seg g = seg_of(a, pair, n_pairs, q);
-        const int nt = g.tile / a.n_tt, tt = g.tile - nt * a.n_tt;
-        const int rx = tt * 2 * kPM + static_cast<int>(rank) * kPM;
+        const Seg g = seg_of(a, grp, n_grp, q);
+        const int nt = (g.tile / a.n_tt) * a.G + gp, tt = g.tile % a.n_tt;
+        const int rx = tt * 2 * kPM + static_cast<int>(rank) * kPM + gp * xrows;
         const int rw = nt * kPN + static_cast<int>(rank) * (kPN / 2);
         for (int k = g.kb; k < g.ke; ++k, ++it) {
           const int st = it % a.stages;
@@ -447,7 +470,10 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
               pdl_wait();  // the activations come from the previous kernel
               waited = true;
             }
-            tma_load_3d_pair(sp, &tx, 0, rx, k, &full[st]);
+            if (a.G > 1)
+              tma_load_3d_pair_mc(sp + gp * xrows * 128, &tx, 0, rx, k, &full[st], x_mask);
+            else
+              tma_load_3d_pair(sp, &tx, 0, rx, k, &full[st]);
           }
         }
       }
@@ -457,10 +483,10 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
     if (leader && lane == 0) {
       const uint32_t idesc = tc::idesc_bf16(2 * kPM, kPN, false);
       const uint32_t base = smem_u32(smem);
-      const int ns_ = n_segs(a, pair);
+      const int ns_ = n_segs(a, grp);
       int n = 0;  // ring iteration
       for (int i = 0; i < ns_; ++i) {
-        const Seg g = seg_of(a, pair, n_pairs, i);
+        const Seg g = seg_of(a, grp, n_grp, i);
         const int acc = i & 1;
         if (i >= 2) mbar_wait(&acc_empty[acc], static_cast<uint32_t>((i >> 1) - 1) & 1);
         tc::fence_after();
@@ -474,9 +500,9 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
           for (int kk = 0; kk < 4; ++kk)
             mma_pair(d, tc::smem_desc(pa + kk * 32, 16, 1024), tc::smem_desc(pb + kk * 32, 16, 1024),
                      idesc, (k > g.kb || kk > 0) ? 1u : 0u);
-          commit_pair(&empty[st]);  // the stage is free in both CTAs once read
+          commit_pair(&empty[st], all_mask);  // every cluster CTA may refill the stage
         }
-        commit_pair(&acc_full[acc]);
+        commit_pair(&acc_full[acc], pair_mask);
       }
     }
     __syncwarp();
@@ -497,13 +523,13 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
     __syncwarp();
     int* my_flag = a.flags + pair * 2 + rank;
     float* my_part = a.partials + (static_cast<int64_t>(pair) * 2 + rank) * kPM * kPN;
-    const int ns_ = n_segs(a, pair);
+    const int ns_ = n_segs(a, grp);
     for (int i = 0; i < ns_; ++i) {
-      const Seg g = seg_of(a, pair, n_pairs, i);
+      const Seg g = seg_of(a, grp, n_grp, i);
       const int tile = g.tile;
       const bool finisher = g.j == 0;
       const int acc = i & 1;
-      const int nt = tile / a.n_tt, tt = tile - nt * a.n_tt;
+      const int nt = (tile / a.n_tt) * a.G + gp, tt = tile % a.n_tt;
       const int t = tt * 2 * kPM + static_cast<int>(rank) * kPM + r;
       mbar_wait(&acc_full[acc], static_cast<uint32_t>(i >> 1) & 1);
       tc::fence_after();
@@ -526,19 +552,20 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
           if (leader)
             mbar_arrive(&acc_empty[acc]);
           else
-            arrive_leader(&acc_empty[acc]);
+            arrive_leader(&acc_empty[acc], leader_rank);
         }
         __threadfence();
         named_bar_sync(1, 256);
         if (et == 0) st_release_gpu(my_flag, 1);
         continue;
       }
-      // participants: the pairs holding the tile's later k ranges, in k order
-      const int q_first = pair + 1;
-      const int q_last = g.ke < a.kt ? pair + a.split - 1 : pair;
-      if (q_last >= q_first) {
-        if (et < q_last - q_first + 1)
-          while (ld_acquire_gpu(a.flags + (q_first + et) * 2 + rank) == 0) __nanosleep(64);
+      // participants: the same pair of the next groups, holding the tile's later
+      // k ranges, in k order
+      const int n_part = g.ke < a.kt ? a.split - 1 : 0;
+      auto partner = [&](int d) { return (grp + 1 + d) * a.G + gp; };
+      if (n_part > 0) {
+        if (et < n_part)
+          while (ld_acquire_gpu(a.flags + partner(et) * 2 + rank) == 0) __nanosleep(64);
         named_bar_sync(1, 256);
       }
       RowCtx rc{};
@@ -559,9 +586,9 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
       for (int c = half; c < kPN / 32; c += 2) {
         float v[32];
         tc::ld32(taddr + c * 32, v);
-        for (int q = q_first; q <= q_last; ++q) {  // fixed k order: deterministic
+        for (int d = 0; d < n_part; ++d) {  // fixed k order: deterministic
           const float4* pq = reinterpret_cast<const float4*>(
-                                 a.partials + (static_cast<int64_t>(q) * 2 + rank) * kPM * kPN) +
+                                 a.partials + (static_cast<int64_t>(partner(d)) * 2 + rank) * kPM * kPN) +
                              c * 8 * kPM + r;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -600,11 +627,11 @@ __global__ void __launch_bounds__(kPairThreads, 1) gemm_pair_kernel(
         if (leader)
           mbar_arrive(&acc_empty[acc]);
         else
-          arrive_leader(&acc_empty[acc]);
+          arrive_leader(&acc_empty[acc], leader_rank);
       }
-      if (q_last >= q_first) {  // re-arm the participants' flags (their partials are read)
+      if (n_part > 0) {  // re-arm the participants' flags (their partials are read)
         named_bar_sync(1, 256);
-        if (et < q_last - q_first + 1) a.flags[(q_first + et) * 2 + rank] = 0;
+        if (et < n_part) a.flags[partner(et) * 2 + rank] = 0;
       }
     }
   }
@@ -672,46 +699,76 @@ extern "C" int ds_gemm_pair(const void* X, const void* W, void* Y, int T, int N,
   a.y_f32 = y_f32;
   a.accumulate = accumulate;
   a.n_tt = (T + 2 * kPM - 1) / (2 * kPM);
-  a.tiles = (N / kPN) * a.n_tt;
   a.kt = K / 64;
+  // DS_PAIR_MC=1 (A/B): two pairs per cluster sharing the token tile through
+  // multicast when the weight tiles pair up (N % 512).  Correct, but measured
+  // slower (T=4096 gate_up 674 vs 649 us, down 345-358 vs 336): one pair per
+  // cluster by default
+  static const int mc_env = getenv("DS_PAIR_MC") ? atoi(getenv("DS_PAIR_MC")) : 0;
+  a.G = (mc_env && N % (2 * kPN) == 0) ? 2 : 1;
+  a.tiles = (N / (kPN * a.G)) * a.n_tt;  // cluster tiles
   static const int st_env = getenv("DS_PAIR_STAGES") ? atoi(getenv("DS_PAIR_STAGES")) : 0;
   const int fixed = 1024 + 256 + 8 * (32 * kStgP * 4 + 32 * 8);  // + epilogue staging
   int ns = (kPairSmemMax - fixed) / kStage;
   if (st_env > 1 && st_env < ns) ns = st_env;
   a.stages = ns;
   const int smem = fixed + ns * kStage;
-  const CUtensorMap* tx = slab_tensor_map(X, T, K, kPM, 1);
+  const CUtensorMap* tx = slab_tensor_map(X, T, K, kPM / a.G, 1);
   const CUtensorMap* tw = slab_tensor_map(W, N, K, kPN / 2, 1);
   if (!tx || !tw) return DS_EUNSUPPORTED;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmemMax);
+    cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
-  int sms = 0, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // every cluster must be co-resident (the tail's partial hand-off spins)
+  static int max_cl[3] = {0, 0, 0};
+  if (!max_cl[a.G]) {
+    cudaLaunchConfig_t q = {};
+    q.gridDim = dim3(2 * a.G, 1, 1);
+    q.blockDim = dim3(kPairThreads);
+    q.dynamicSmemBytes = smem;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = 2 * a.G;
+    qa[0].val.clusterDim.y = 1;
+    qa[0].val.clusterDim.z = 1;
+    q.attrs = qa;
+    q.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_pair_kernel, &q) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      int sms = 0, dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      n = sms / (2 * a.G);
+    }
+    max_cl[a.G] = n;
+  }
   static const int pairs_env = getenv("DS_PAIR_CTAS") ? atoi(getenv("DS_PAIR_CTAS")) / 2 : 0;
-  int pairs = pairs_env > 0 ? pairs_env : sms / 2;
-  if (pairs > a.tiles * 4) pairs = a.tiles * 4;
-  // full waves data-parallel; the tail tiles (< pairs) cut into up to 4 k ranges
-  a.full_waves = a.tiles / pairs;
-  a.rem = a.tiles - a.full_waves * pairs;
+  int groups = max_cl[a.G];
+  if (pairs_env > 0 && pairs_env / a.G < groups) groups = pairs_env / a.G;
+  if (groups > a.tiles * 4) groups = a.tiles * 4;
+  // full waves data-parallel; the tail tiles (< groups) cut into up to 4 k ranges
+  a.full_waves = a.tiles / groups;
+  a.rem = a.tiles - a.full_waves * groups;
   static const int split_max = getenv("DS_PAIR_SPLIT") ? atoi(getenv("DS_PAIR_SPLIT")) : 4;
   a.split = 1;
   if (a.rem) {
-    a.split = pairs / a.rem;
+    a.split = groups / a.rem;
     if (a.split > split_max) a.split = split_max;
     if (a.split > a.kt) a.split = a.kt;
     if (a.split < 1) a.split = 1;
   }
-  if (a.full_waves == 0) pairs = a.rem * a.split;  // only the tail: idle pairs not launched
+  if (a.full_waves == 0) groups = a.rem * a.split;  // only the tail: idle clusters not launched
+  const int pairs = groups * a.G;
   PairWorkspace& w = pair_workspace();
   if (!w.ws || pairs > w.pairs) return DS_EWORKSPACE;
   a.partials = w.ws;
   a.flags = w.flags;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * pairs, 1, 1);
+  cfg.gridDim = dim3(2 * pairs, 1, 1);  // groups x G pairs x 2 CTAs
   cfg.blockDim = dim3(kPairThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = (cudaStream_t)stream;
@@ -719,7 +776,7 @@ extern "C" int ds_gemm_pair(const void* X, const void* W, void* Y, int T, int N,
   attr2[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr2[0].val.programmaticStreamSerializationAllowed = 1;
   attr2[1].id = cudaLaunchAttributeClusterDimension;
-  attr2[1].val.clusterDim.x = 2;
+  attr2[1].val.clusterDim.x = 2 * a.G;
   attr2[1].val.clusterDim.y = 1;
   attr2[1].val.clusterDim.z = 1;
   cfg.attrs = attr2;
