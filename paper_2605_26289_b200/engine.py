@@ -75,7 +75,7 @@ class CostLedger:
                     "forward_calls": self.forward_calls, "batch_tokens": self.batch_tokens}
 
 
-@dataclass
+@dataclass(slots=True)
 class RowResult:
     """One sampled position: the reference Logits' argmax_id / copy_source."""
 
@@ -84,14 +84,14 @@ class RowResult:
     scratch: list | None = None
 
 
-@dataclass
+@dataclass(slots=True)
 class VerifyResult:
     accepted: int
     rows: list
     scratch: list | None = None
 
 
-@dataclass
+@dataclass(slots=True)
 class EntryRequest:
     """One plan entry for a (possibly batched) forward."""
 
@@ -394,16 +394,39 @@ class GpuEngine:
         if n_e > self.max_entries:
             raise ValueError(f"{n_e} entries > engine max {self.max_entries}")
         G = self.shape.n_heads // self.shape.n_kv_heads
-        order = sorted(range(n_e),
-                       key=lambda i: 0 if len(reqs[i].batch) * G > DECODE_MAX_ROWS else 1)
-        # per-entry columns in one pass, then vectorised row arrays
+        # prefill-sized entries first (stable: the order of sorted() with a 0/1 key)
+        lim = DECODE_MAX_ROWS // G
+        order = [i for i, r in enumerate(reqs) if len(r.batch) > lim]
+        if order:
+            order += [i for i, r in enumerate(reqs) if len(r.batch) <= lim]
+        else:
+            order = list(range(n_e))
+        # every per-entry column in ONE pass over the requests (a batched plan
+        # has hundreds of entries: separate generator passes cost ~1 ms per forward)
         rs = [reqs[ri] for ri in order]
-        qs = np.fromiter((len(r.batch) for r in rs), dtype=np.int64, count=n_e)
+        PRE = _lib.ENTRY_PREFILL
+        q_l, k_l, p_l, s_l, nd_l, h_l, final, tok_l = [], [], [], [], [], [], [], []
+        hash_in = self._hash_in
+        for r in rs:
+            b = r.batch
+            q, kd, pa, sq = len(b), r.kind, r.past, r.seq
+            f = kd == PRE and pa + q == len(r.tokens)
+            q_l.append(q)
+            k_l.append(kd)
+            p_l.append(pa)
+            s_l.append(sq)
+            final.append(f)
+            # a chunk that ends its prompt (no generated token yet) also gets the
+            # first decode step's proposal from the forward (n_draft = -1)
+            nd_l.append(-1 if f else r.n_draft)
+            h_l.append(hash_in(sq, pa, r.tokens))
+            tok_l.extend(b)
+        qs = np.array(q_l, dtype=np.int64)
         if n_e and qs.min() == 0:
             raise ValueError("batch must be non-empty")
-        kinds = np.fromiter((r.kind for r in rs), dtype=np.int64, count=n_e)
-        pasts = np.fromiter((r.past for r in rs), dtype=np.int64, count=n_e)
-        seqs = np.fromiter((r.seq for r in rs), dtype=np.int64, count=n_e)
+        kinds = np.array(k_l, dtype=np.int64)
+        pasts = np.array(p_l, dtype=np.int64)
+        seqs = np.array(s_l, dtype=np.int64)
         n_outs = np.where(kinds == _lib.ENTRY_VERIFY, qs, 1)
         q_starts = np.concatenate(([0], np.cumsum(qs)[:-1]))
         out_starts = np.concatenate(([0], np.cumsum(n_outs)[:-1]))
@@ -413,19 +436,10 @@ class GpuEngine:
         ents = np.zeros(n_e, dtype=_ENTRY_DT)
         ents["seq"], ents["past"], ents["q_len"], ents["q_start"] = seqs, pasts, qs, q_starts
         ents["kind"], ents["out_start"], ents["n_out"] = kinds, out_starts, n_outs
-        # a chunk that ends its prompt (no generated token yet) also gets the
-        # first decode step's proposal from the forward (n_draft = -1)
-        final = [r.kind == _lib.ENTRY_PREFILL and r.past + len(r.batch) == len(r.tokens)
-                 for r in rs]
-        ents["n_draft"] = np.fromiter((-1 if f else r.n_draft for r, f in zip(rs, final)),
-                                      dtype=np.int64, count=n_e)
-        ents["hash_in"] = np.fromiter((self._hash_in(r.seq, r.past, r.tokens) for r in rs),
-                                      dtype=np.uint64, count=n_e)
+        ents["n_draft"] = nd_l
+        ents["hash_in"] = np.array(h_l, dtype=np.uint64)
         row_entry = np.repeat(np.arange(n_e), qs)
         row_in = np.arange(q_start) - np.repeat(q_starts, qs)  # row index within its entry
-        tok_l = []
-        for r in rs:
-            tok_l.extend(r.batch)
         toks = [np.asarray(tok_l, dtype=np.int32)]
         rseq = [seqs[row_entry].astype(np.int32)]
         rpos = [(pasts[row_entry] + row_in).astype(np.int32)]
@@ -502,16 +516,19 @@ class GpuEngine:
         tok, src, acc = h[: self.max_out], h[self.max_out: 2 * self.max_out], h[2 * self.max_out:]
         if nd:  # cache the proposals for the token lists the scheduler will hold next
             o = self.nd_off
-            dlen = h[o + 2 * n_e: o + 3 * n_e]
-            drafts = h[o + 3 * n_e: o + 3 * n_e + n_e * self.nd_cap].reshape(n_e, self.nd_cap)
+            dlen = h[o + 2 * n_e: o + 3 * n_e].tolist()
+            d0 = o + 3 * n_e
+            cap = self.nd_cap
+            acc_l = acc[:n_e].tolist()
+            dc = self._draft_cache
             for i, r in enumerate(rs):
                 if r.kind == _lib.ENTRY_PREFILL:
                     if final[i]:
-                        self._draft_cache[r.seq] = (r.past + len(r.batch) + 1,
-                                                    drafts[i, : dlen[i]].tolist())
+                        dc[r.seq] = (r.past + len(r.batch) + 1,
+                                     h[d0 + i * cap: d0 + i * cap + dlen[i]].tolist())
                     continue
-                a = int(acc[i]) if r.kind == _lib.ENTRY_VERIFY else 0
-                self._draft_cache[r.seq] = (r.past + a + 2, drafts[i, : dlen[i]].tolist())
+                a = acc_l[i] if r.kind == _lib.ENTRY_VERIFY else 0
+                dc[r.seq] = (r.past + a + 2, h[d0 + i * cap: d0 + i * cap + dlen[i]].tolist())
         out = [None] * n_e
         tok_all, src_all = tok[:out_start].tolist(), src[:out_start].tolist()
         acc_all = acc[:n_e].tolist()

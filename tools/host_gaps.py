@@ -72,18 +72,20 @@ class _Proxy:
 _proxy = _Proxy()
 E.lib = lambda: _proxy
 tr = load_trace(sys.argv[1] if len(sys.argv) > 1 else "c2")
-core = InferenceCore(core_config_for(tr, model=os.environ.get("DS_MODEL", "llama3-8b")))
-for _ in range(2):
+core = InferenceCore(core_config_for(tr, model=os.environ.get("DS_MODEL", "llama3-8b"),
+                                    batched_forward=bool(int(os.environ.get("BATCHED", "0")))))
+REPS = int(os.environ.get("REPS", "3"))
+for _ in range(2 if REPS > 1 else 1):
     core.reset_state(); replay(core, tr)
 for k in acc: acc[k] = 0 if k in ("n", "np") else 0.0
 last_exit[0] = None
 core.engine.reset_counters()
 t0 = time.perf_counter()
-for _ in range(3):
+for _ in range(REPS):
     core.reset_state(); replay(core, tr)
 wall = time.perf_counter() - t0
 n = acc["n"]
-print(f"wall/step {wall / 3 * 1e3:.1f} ms, device/step {core.engine.device_seconds() / 3 * 1e3:.1f} ms, "
-      f"forwards/step {n / 3:.0f}, proposes/step {acc['np'] / 3:.0f}")
+print(f"wall/step {wall / REPS * 1e3:.1f} ms, device/step {core.engine.device_seconds() / REPS * 1e3:.1f} ms, "
+      f"forwards/step {n / REPS:.0f}, proposes/step {acc['np'] / REPS:.0f}")
 for k in ("in_run_pre", "native", "apply_meta", "sync", "in_run_post", "between", "propose"):
-    print(f"  {k:12s} {acc[k] / n * 1e6:8.1f} us per forward   ({acc[k] / 3 * 1e3:6.1f} ms/step)")
+    print(f"  {k:12s} {acc[k] / n * 1e6:8.1f} us per forward   ({acc[k] / REPS * 1e3:6.1f} ms/step)")
