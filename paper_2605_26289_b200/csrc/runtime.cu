@@ -478,10 +478,32 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
     } else {
       DS_CHECK(ds_rmsnorm(b.x, 1, nullptr, T, H, an + static_cast<size_t>(l) * H, m->rms_eps, b.h,
                           stream));
-      DS_CHECK(project(rt.blas, b.h, wqkv_l, b.qkv, T, QKV, H, false, false, stream));
-      DS_CHECK(ds_rope_kv_store(b.qkv, T, a->row_seq, a->row_pos, kv->pos2cell, kv->pos_stride,
-                                nh, nkv, hd, m->rope_cos, m->rope_sin, kp + l * kv_layer,
-                                vp + l * kv_layer, kv->capacity, stream));
+      // wqkv on K11 with RoPE + the KV store in its epilogue from
+      // DS_PAIR_QKV_MIN_ROWS rows (default 2048; with K11 gate_up: 2k / 4k rows
+      // 26.7 -> 26.4, 53.6 -> 53.2 ms; at 1.5k rows it lost 21.41 -> 21.75)
+      static const int qkv_min =
+          getenv("DS_PAIR_QKV_MIN_ROWS") ? atoi(getenv("DS_PAIR_QKV_MIN_ROWS")) : 2048;
+      if (qkv_min > 0 && T >= qkv_min && QKV % 256 == 0 && H % 64 == 0 && hd == 128) {
+        ds_skinny_epi e{};
+        e.rope = 1;
+        e.n_heads = nh;
+        e.n_kv_heads = nkv;
+        e.row_seq = a->row_seq;
+        e.row_pos = a->row_pos;
+        e.pos2cell = kv->pos2cell;
+        e.pos_stride = kv->pos_stride;
+        e.rope_cos = m->rope_cos;
+        e.rope_sin = m->rope_sin;
+        e.k_pool_l = kp + l * kv_layer;
+        e.v_pool_l = vp + l * kv_layer;
+        e.kv_head_stride = kv->capacity;
+        DS_CHECK(ds_gemm_pair(b.h, wqkv_l, b.qkv, T, QKV, H, 0, 0, &e, stream));
+      } else {
+        DS_CHECK(project(rt.blas, b.h, wqkv_l, b.qkv, T, QKV, H, false, false, stream));
+        DS_CHECK(ds_rope_kv_store(b.qkv, T, a->row_seq, a->row_pos, kv->pos2cell,
+                                  kv->pos_stride, nh, nkv, hd, m->rope_cos, m->rope_sin,
+                                  kp + l * kv_layer, vp + l * kv_layer, kv->capacity, stream));
+      }
     }
     // the attention leaves HBM mostly idle (short contexts): K7's producer
     // warps pull wo's weights into L2 for the next projection meanwhile
@@ -553,8 +575,19 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
       DS_CHECK(project(rt.blas, b.attn, wo_l, b.x, T, H, nh * hd, true, true, stream));
       DS_CHECK(ds_rmsnorm(b.x, 1, nullptr, T, H, mn + static_cast<size_t>(l) * H, m->rms_eps,
                           b.h, stream));
-      DS_CHECK(project(rt.blas, b.h, wgu_l, b.gu, T, 2 * F, H, false, false, stream));
-      DS_CHECK(ds_silu_mul(b.gu, T, F, b.act, stream));
+      // gate_up on K11 with the SwiGLU in its epilogue from DS_PAIR_GU_MIN_ROWS
+      // rows (default 1024; no [T][2F] intermediate, no SiLU launch): whole
+      // forward at 1.5k / 2k / 4k rows 22.06 -> 21.41, 27.5 -> 26.7, 55.6 -> 53.6 ms
+      static const int gu_min =
+          getenv("DS_PAIR_GU_MIN_ROWS") ? atoi(getenv("DS_PAIR_GU_MIN_ROWS")) : 1024;
+      if (gu_min > 0 && T >= gu_min && (2 * F) % 256 == 0 && H % 64 == 0 && hd == 128) {
+        ds_skinny_epi eg{};
+        eg.swiglu = 1;
+        DS_CHECK(ds_gemm_pair(b.h, wgu_l, b.act, T, 2 * F, H, 0, 0, &eg, stream));
+      } else {
+        DS_CHECK(project(rt.blas, b.h, wgu_l, b.gu, T, 2 * F, H, false, false, stream));
+        DS_CHECK(ds_silu_mul(b.gu, T, F, b.act, stream));
+      }
       DS_CHECK(project(rt.blas, b.act, wd_l, b.x, T, H, F, true, true, stream));
     }
   }
