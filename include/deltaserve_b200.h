@@ -322,14 +322,6 @@ typedef struct {
 int ds_gemm_skinny_ex(const void* X, const void* W, void* Y, int M, int N, int K, int y_f32,
                       int accumulate, const ds_skinny_epi* epi, ds_stream_t stream);
 
-/* K9: projection GEMM for 33..4096 rows on tcgen05/TMEM (prefill chunks,
- * batched plans): Y[T][N] (+)= X[T][K] . W[N][K]^T, bf16 in, fp32 accumulate,
- * Y bf16 or fp32 (y_f32), accumulate adds into Y.  N % 128 == 0, K % 64 == 0.
- * Replaces the library GEMM the reference has no counterpart for (its
- * forward is a mock, engine.py:268-281). */
-int ds_gemm_tc(const void* X, const void* W, void* Y, int T, int N, int K, int y_f32,
-               int accumulate, ds_stream_t stream);
-
 /* K10: persistent stream-K projection GEMM on tcgen05/TMEM for prefill chunks
  * and batched plans (any T): Y[T][N] (+)= X[T][K] . W[N][K]^T with the
  * ds_skinny_epi fusions (norm consumer, residual producer + row sums,

@@ -122,7 +122,6 @@ def lib() -> ctypes.CDLL:
         "ds_argmax": (c_i32, [P, c_i32, c_i32, P, P]),
         "ds_gemm_skinny": (c_i32, [P, P, P, c_i32, c_i32, c_i32, c_i32, c_i32, P]),
         "ds_gemm_skinny_ex": (c_i32, [P, P, P, c_i32, c_i32, c_i32, c_i32, c_i32, P, P]),
-        "ds_gemm_tc": (c_i32, [P, P, P, c_i32, c_i32, c_i32, c_i32, c_i32, P]),
         "ds_gemm_stream": (c_i32, [P, P, P, c_i32, c_i32, c_i32, c_i32, c_i32, P, P]),
         "ds_gemm_pair": (c_i32, [P, P, P, c_i32, c_i32, c_i32, c_i32, c_i32, P, P]),
     }

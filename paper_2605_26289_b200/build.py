@@ -24,7 +24,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-re
          "-I" + os.path.join(ROOT, "include")] + os.environ.get("DS_NVCC_EXTRA", "").split()
 
 SOURCES = ["policy.cu", "kvmeta.cu", "layers.cu", "attn_dispatch.cu", "attn_decode.cu",
-           "attn_decode_tc.cu", "attn_prefill_sm100.cu", "gemm_skinny.cu", "gemm_tc.cu",
+           "attn_decode_tc.cu", "attn_prefill_sm100.cu", "gemm_skinny.cu",
            "gemm_stream.cu", "gemm_pair.cu", "tma.cu",
            "runtime.cu"]
 

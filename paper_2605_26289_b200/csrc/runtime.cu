@@ -181,11 +181,6 @@ int project(cublasHandle_t h, const void* X, const void* W, void* Y, int M, int 
   if (pair_ok(M, N, K)) return ds_gemm_pair(X, W, Y, M, N, K, y_f32, accumulate, nullptr, s);
   if (use_stream_gemm() && N % 128 == 0 && K % 64 == 0)
     return ds_gemm_stream(X, W, Y, M, N, K, y_f32, accumulate, nullptr, s);
-  // DS_GEMM_TC=1 (with DS_GEMM_STREAM=0): K9, the earlier data-parallel
-  // tcgen05 GEMM with cluster split-K - kept for A/B
-  static const bool use_tc = getenv("DS_GEMM_TC") && atoi(getenv("DS_GEMM_TC")) == 1;
-  if (use_tc && N % 128 == 0 && K % 64 == 0 && K >= 128)
-    return ds_gemm_tc(X, W, Y, M, N, K, y_f32, accumulate, s);
   const cublasStatus_t st = gemm(h, X, W, Y, M, N, K, accumulate ? 1.f : 0.f,
                                  y_f32 ? CUDA_R_32F : CUDA_R_16BF);
   return st == CUBLAS_STATUS_SUCCESS ? 0 : 1000 + static_cast<int>(st);

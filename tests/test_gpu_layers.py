@@ -308,37 +308,6 @@ def test_gemm_pair_vs_fp32(cuda, T, N, K, y_f32, acc):
         assert torch.equal(Y, Y2)
 
 
-# K9 (tcgen05): prefill chunks and batched plans.  Shapes cover one token tile
-# (150 -> N=160), ragged multi-tile (415 -> 2 x 208, 881 -> 4 x 224, 4096), the
-# cluster split-K (wo/down/wqkv-like N with few row tiles) and the tiny model.
-@pytest.mark.parametrize("T,N,K", [(150, 4096, 4096), (150, 6144, 4096), (150, 28672, 4096),
-                                   (150, 4096, 14336), (33, 1024, 1024), (415, 4096, 4096),
-                                   (881, 1536, 1024), (200, 5632, 1024), (100, 1024, 2816),
-                                   (4096, 1024, 4096), (256, 4096, 4096), (64, 128256, 4096)])
-@pytest.mark.parametrize("y_f32,acc", [(0, 0), (1, 1)])
-def test_gemm_tc_vs_fp32(cuda, T, N, K, y_f32, acc):
-    from paper_2605_26289_b200._lib import check, lib
-
-    g = torch.Generator(device=cuda).manual_seed(T + N + K)
-    X = torch.randn(T, K, device=cuda, generator=g).bfloat16()
-    W = (0.02 * torch.randn(N, K, device=cuda, generator=g)).bfloat16()
-    Y0 = torch.randn(T, N, device=cuda, generator=g)
-    Y = Y0.clone() if y_f32 else Y0.bfloat16()
-    s = torch.cuda.current_stream().cuda_stream
-    check(lib().ds_gemm_tc(X.data_ptr(), W.data_ptr(), Y.data_ptr(), T, N, K, y_f32, acc, s))
-    torch.cuda.synchronize()
-    ref = X.float() @ W.float().T
-    if acc:
-        ref = ref + (Y0 if y_f32 else Y0.bfloat16().float())
-    err = (Y.float() - ref).abs().max().item()
-    assert err < (2e-3 if y_f32 else 1e-2 * ref.abs().max().item()), err
-    if y_f32:  # deterministic: the cluster split-K reduces in fixed order
-        Y2 = Y0.clone()
-        check(lib().ds_gemm_tc(X.data_ptr(), W.data_ptr(), Y2.data_ptr(), T, N, K, 1, acc, s))
-        torch.cuda.synchronize()
-        assert torch.equal(Y, Y2)
-
-
 @pytest.mark.parametrize("M", [1, 5, 13, 20, 32, 33, 150, 300, 881])
 @pytest.mark.parametrize("impl", ["auto", "pair"])
 def test_gemm_skinny_epilogue_fusions(cuda, M, impl):
