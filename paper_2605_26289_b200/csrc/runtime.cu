@@ -171,6 +171,14 @@ int pair_min_rows() {
   return v > 0 ? v : 1 << 30;
 }
 bool pair_ok(int M, int N, int K) { return M >= pair_min_rows() && N % 256 == 0 && K % 64 == 0; }
+// the LM head of many sampled rows (batched verify plans) on K11 with the
+// fused argmax from DS_PAIR_HEAD_MIN_ROWS rows (default 64; K10 below): whole
+// batched verify forward at 64 / 128 / 256 / 512 / 1024 sampled rows 4.73 ->
+// 4.68, 5.78 -> 5.74, 7.90 -> 7.80, 12.56 -> 12.39, 22.39 -> 22.10 ms
+bool head_pair_ok(int M, int N, int K) {
+  static const int v = getenv("DS_PAIR_HEAD_MIN_ROWS") ? atoi(getenv("DS_PAIR_HEAD_MIN_ROWS")) : 64;
+  return v > 0 && M >= v && N % 256 == 0 && K % 64 == 0;
+}
 
 // decode / verify row counts stream the weights through our skinny GEMM;
 // prefill chunks and batched plans through the stream-K tcgen05 GEMM (K10).
@@ -600,7 +608,7 @@ static int forward_body(const ds_model* m, const ds_kv_store* kv, const ds_forwa
     void* lg = a->logits_out ? a->logits : nullptr;
     if (a->n_out <= 32)
       DS_CHECK(ds_gemm_skinny_ex(b.hf, m->lm_head, lg, a->n_out, m->vocab, H, 1, 0, &eh, stream));
-    else if (pair_ok(a->n_out, m->vocab, H))
+    else if (pair_ok(a->n_out, m->vocab, H) || head_pair_ok(a->n_out, m->vocab, H))
       DS_CHECK(ds_gemm_pair(b.hf, m->lm_head, lg, a->n_out, m->vocab, H, 1, 0, &eh, stream));
     else
       DS_CHECK(ds_gemm_stream(b.hf, m->lm_head, lg, a->n_out, m->vocab, H, 1, 0, &eh, stream));
