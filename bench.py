@@ -277,6 +277,35 @@ def kernel_micro(torch, dev, peaks) -> dict:
                          "unit": "TFLOP/s", "frac": round(flops / t / 1e12 / tf_burst, 3),
                          "algo_flops": flops}
         del pools, qkv, o, ws
+    # K11 (CTA-pair tcgen05 GEMM) at a batched-prefill gate_up shape: 4,096
+    # rows x 28,672 x 4,096 with the fused SwiGLU (the forward's default use),
+    # 3 rotating weight copies (> L2), 10 launches
+    T, N, K = 4096, 28672, 4096
+    X = torch.randn(T, K, device=dev).bfloat16()
+    Ws = [(0.02 * torch.randn(N, K, device=dev)).bfloat16() for _ in range(3)]
+    act = torch.empty(T, N // 2, device=dev, dtype=torch.bfloat16)
+    e = _lib.SkinnyEpi(swiglu=1)
+
+    def k11(i):
+        _lib.check(L.ds_gemm_pair(X.data_ptr(), Ws[i % 3].data_ptr(), act.data_ptr(), T, N, K, 0,
+                                  0, ctypes.byref(e), stream.cuda_stream), "ds_gemm_pair")
+
+    for i in range(3):
+        k11(i)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for i in range(10):
+        k11(i)
+    b.record(stream)
+    b.synchronize()
+    t = a.elapsed_time(b) / 1000.0 / 10
+    flops = 2.0 * T * N * K
+    out["K11_gate_up_swiglu_T4096"] = {"bound": "tensor", "us": round(t * 1e6, 2),
+                                       "achieved": round(flops / t / 1e12, 1), "peak": tf_burst,
+                                       "unit": "TFLOP/s", "frac": round(flops / t / 1e12 / tf_burst, 3),
+                                       "algo_flops": flops}
+    del X, Ws, act
     return out
 
 
