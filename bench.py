@@ -632,6 +632,21 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         from paper_2605_26289_b200.curve import prefix_curve
 
         line["prefix_curve"] = prefix_curve(model=args.model, weights=eng.w)
+        # K7 inside the forward: the verify forward's extra time from the
+        # shortest to the longest prefix against the extra K/V bytes it reads
+        # (every layer, K and V) - the attention's marginal HBM rate where the
+        # split merge and launch chain overlap the projections
+        pts = line["prefix_curve"]["points"]
+        if len(pts) >= 2 and args.model == "llama3-8b":
+            lo, hi = pts[0], pts[-1]
+            dt = (hi["verify_ms"] - lo["verify_ms"]) / 1e3
+            dbytes = 32 * 2 * 8 * 128 * 2 * (hi["m"] - lo["m"])
+            if dt > 0:
+                hbm = peaks[0]
+                line["kernels"]["K7_verify_in_forward_marginal"] = {
+                    "bound": "hbm", "what": f"verify forward m={lo['m']} -> {hi['m']}",
+                    "achieved": round(dbytes / dt / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(dbytes / dt / 1e9 / hbm, 3), "algo_bytes": dbytes}
     if not args.no_c4 and world == 1 and args.workload != "c4":
         del core, eng  # the C4 core builds its own 8B engine (same seed: same weights)
         torch.cuda.empty_cache()
