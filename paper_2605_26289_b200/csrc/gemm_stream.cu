@@ -1091,14 +1091,12 @@ extern "C" int ds_gemm_stream(const void* X, const void* W, void* Y, int T, int 
             "stages=%d smem=%d\n", T, N, K, p.NT, p.n_tt, p.tiles,
             static_cast<long long>(p.total), p.P, p.stages, p.smem);
   // one token tile and fewer weight tiles than SMs: cluster split-K (the
-  // partials reduce through distributed shared memory).  The ring only has to
-  // hold the token-major partial tile at the end, so it could be ~110 KB and
-  // let two CTAs share an SM (DS_STREAM_CL_WIDE=0, A/B)
+  // partials reduce through distributed shared memory), two-slab stages
   static const int cl_env = getenv("DS_STREAM_CLUSTER") ? atoi(getenv("DS_STREAM_CLUSTER")) : 1;
   int S = 0, cl_stages = 0, cl_smem = 0;
-  // DS_STREAM_CL_BIG=1 (A/B): also one-token-tile shapes with up to two
-  // tiles per SM (gate_up at T <= 256: 224 tiles), unsplit, two shallow-ring
-  // CTAs per SM
+  // one-token-tile shapes with up to two tiles per SM (gate_up at T <= 256:
+  // 224 tiles) run unsplit, single-slab stages, two CTAs per SM
+  // (DS_STREAM_CL_BIG=0 sends them to stream-K)
   static const int cl_big = getenv("DS_STREAM_CL_BIG") ? atoi(getenv("DS_STREAM_CL_BIG")) : 1;
   const bool big = cl_big && p.n_tt == 1 && p.tiles >= num_sms() && p.tiles <= 2 * num_sms();
   int sl = 2;  // slabs per ring stage
