@@ -389,7 +389,19 @@ static int launch_ring(const void* X, const void* W, void* Y, int M, int N, int 
     attr_smem = smem;
   }
   const int units = N / 16;
-  const int grid = units < per_sm * kNumSMs ? units : per_sm * kNumSMs;
+  int grid = units < per_sm * kNumSMs ? units : per_sm * kNumSMs;
+  // verify rows (M > 1): the fewest CTAs that keep the most-loaded CTA's unit
+  // count, so every CTA walks the same number of units and none streams a
+  // last unit alone (gate_up: 1,792 units on 256 CTAs x 7 instead of 296 with
+  // 16 taking a 7th; qkv 192 x 2; the LM head 287 x 28).  Measured per
+  // forward: q=5 at m=1k 2.821 -> 2.792 ms, 8k 3.089 -> 3.051, 32k 3.608 ->
+  // 3.591; decode (M = 1) lost 2% with fewer CTAs (fewer bytes in flight) and
+  // keeps the full grid.  DS_RING_BALANCE: 0 off, 2 also M = 1
+  static const int balance = getenv("DS_RING_BALANCE") ? atoi(getenv("DS_RING_BALANCE")) : 1;
+  if (balance && (M > 1 || balance == 2) && grid > 0 && units % grid) {
+    const int upc = (units + grid - 1) / grid;
+    grid = (units + upc - 1) / upc;
+  }
   launch_pdl(gemm_ring_kernel<MT, NS>, dim3(grid), dim3((kGemvWarps + 1) * 32), smem, s, Y, M, N,
              K, y_f32, acc, n_stages, *tw, *tx, epi);
   return (int)cudaGetLastError();
