@@ -332,13 +332,14 @@ class GpuEngine:
             n_cp = len(pairs)
             self._copies = []
         if self._pending_hist:
-            segs = np.zeros((len(self._pending_hist), 4), dtype=np.int32)
-            data = []
+            rows, data = [], []
             cur = 0
-            for i, (seq, start, toks) in enumerate(self._pending_hist):
-                segs[i] = (seq, start, len(toks), cur)
+            for seq, start, toks in self._pending_hist:
+                n = len(toks)
+                rows.append((seq, start, n, cur))
                 data.append(toks)
-                cur += len(toks)
+                cur += n
+            segs = np.array(rows, dtype=np.int32)
             data_off = self.stage.add(np.concatenate(data) if cur else np.zeros(1, np.int32))
             segs[:, 3] += data_off
             segs_off = self.stage.add(segs)
