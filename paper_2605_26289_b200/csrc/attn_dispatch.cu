@@ -33,28 +33,37 @@ __global__ void attn_combine_kernel(const ds_entry* __restrict__ entries, int n_
       attn_split_plan(qblocks, en.past + en.q_len, nkv, n_entries, mode, R);
   if (plan.n_splits <= 1) return;
   const int64_t base = attn_partial_base(entries, e, n_entries, nh, nkv, mode);
-  // two dependent L2 round trips in all: the split lse values (one thread
-  // each) into smem, then every split's O column issued at once
+  // ONE L2 round trip for up to 32 splits: every thread issues the splits'
+  // lse values (same addresses across the CTA) and its O column together
+  // (was lse -> smem -> barrier -> O in batches of 16: three round trips, and
+  // the next decode launch's dependency wait sat behind them)
   const int64_t s0 = (base + r) * nkv + kh, sstride = static_cast<int64_t>(R) * nkv;
-  __shared__ float lse_s[64];
   const int d = threadIdx.x;
-  if (d < plan.n_splits) lse_s[d] = __ldcg(part_lse + s0 + d * sstride);
-  __syncthreads();
-  float lmax = -INFINITY;
-  for (int s = 0; s < plan.n_splits; ++s) lmax = fmaxf(lmax, lse_s[s]);
-  float acc = 0.f, wsum = 0.f;
-  for (int sb = 0; sb < plan.n_splits; sb += 16) {
-    float v[16];
+  const int ns = plan.n_splits;
+  float acc = 0.f, wsum = 0.f, lmax = -INFINITY;
+  for (int sb = 0; sb < ns; sb += 32) {
+    float v[32], lv[32];
 #pragma unroll
-    for (int i = 0; i < 16; ++i)
-      v[i] = sb + i < plan.n_splits ? __ldcg(part_o + (s0 + (sb + i) * sstride) * kD + d) : 0.f;
+    for (int i = 0; i < 32; ++i) {
+      const bool ok = sb + i < ns;
+      lv[i] = ok ? __ldcg(part_lse + s0 + (sb + i) * sstride) : -INFINITY;
+      v[i] = ok ? __ldcg(part_o + (s0 + (sb + i) * sstride) * kD + d) : 0.f;
+    }
+    float bmax = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      if (sb + i >= plan.n_splits) break;
-      const float lse = lse_s[sb + i];
-      const float w = lse == -INFINITY ? 0.f : exp2f(lse - lmax);
-      wsum += w;
-      acc += w * v[i];
+    for (int i = 0; i < 32; ++i) bmax = fmaxf(bmax, lv[i]);
+    const float nmax = fmaxf(lmax, bmax);
+    if (nmax != -INFINITY) {  // rescale the running sums to the new max (second batch only)
+      const float c = lmax == -INFINITY ? 0.f : exp2f(lmax - nmax);
+      acc *= c;
+      wsum *= c;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float w = lv[i] == -INFINITY ? 0.f : exp2f(lv[i] - nmax);
+        wsum += w;
+        acc += w * v[i];
+      }
+      lmax = nmax;
     }
   }
   const int ti = r / G, gi = r - (r / G) * G;
