@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
   uint64_t* pv_done = bars + 12;  // PV_j complete: P_j's TMEM columns free, O stable
   uint64_t* p_full = bars + 13;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* q_ready = bars + 15;  // the softmax warps' Q rows are in smem
   if (smem_u32(smem) & 1023) __trap();  // SW128 tiles need 1 KB alignment
   // programmatic dependent launch: only q and this chunk's own K/V rows come
   // from the preceding kernels (projection, RoPE/KV store) - the prologue and
@@ -131,23 +132,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
     for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
     mbar_init(pv_done, 1);
     mbar_init(p_full, 4);
+    mbar_init(q_ready, 128);
     mbar_fence_init();
   }
   if (warp == 1) tc::alloc(tmem_slot, kTmemCols);
-  if (warp >= 2) {  // Q rows (packed r = t*G + g) -> smem, UMMA A layout
-    pdl_wait();
-    const int r = tid - 64;
-    const int t = t0 + r / G, g = r - (r / G) * G;
-    const bool ok = t < en.q_len;
-    const uint4* src = reinterpret_cast<const uint4*>(
-        qkv + static_cast<int64_t>(en.q_start + (ok ? t : 0)) * qkv_stride + (kh * G + g) * kD);
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      const uint4 v = ok ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
-      *reinterpret_cast<uint4*>(smem + kSmemQ + sw128(kBM, r, c)) = v;
-    }
-    tc::fence_proxy_async();
-  }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -250,6 +238,8 @@ __global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
         tc::commit(&s_full[sb]);
         tc::commit(&k_empty[st]);  // K stage free once S_jj's MMAs complete
       };
+      mbar_wait(q_ready, 0);  // the Q tile is in smem
+      tc::fence_after();
       issue_s(0);
       for (int jj = 0; jj < ntiles; ++jj) {
         if (jj + 1 < ntiles) issue_s(jj + 1);
@@ -269,6 +259,22 @@ __global__ void __launch_bounds__(kThreads, 2) attn_prefill_kernel(
     }
   } else {
     // ================ softmax / epilogue ================
+    {  // Q rows (packed r = t*G + g) -> smem, UMMA A layout; after the CTA
+       // barrier, so the producer streams the older keys' tiles meanwhile
+      pdl_wait();
+      const int r = tid - 64;
+      const int t = t0 + r / G, g = r - (r / G) * G;
+      const bool ok = t < en.q_len;
+      const uint4* src = reinterpret_cast<const uint4*>(
+          qkv + static_cast<int64_t>(en.q_start + (ok ? t : 0)) * qkv_stride + (kh * G + g) * kD);
+      uint4 qv[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) qv[c] = ok ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) *reinterpret_cast<uint4*>(smem + kSmemQ + sw128(kBM, r, c)) = qv[c];
+      tc::fence_proxy_async();  // generic smem writes -> visible to the tensor core
+      mbar_arrive(q_ready);
+    }
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int r = quad * 32 + lane;
     const int t = t0 + r / G, g = r - (r / G) * G;
