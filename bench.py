@@ -637,16 +637,24 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         # (every layer, K and V) - the attention's marginal HBM rate where the
         # split merge and launch chain overlap the projections
         pts = line["prefix_curve"]["points"]
-        if len(pts) >= 2 and args.model == "llama3-8b":
-            lo, hi = pts[0], pts[-1]
-            dt = (hi["verify_ms"] - lo["verify_ms"]) / 1e3
-            dbytes = 32 * 2 * 8 * 128 * 2 * (hi["m"] - lo["m"])
-            if dt > 0:
+        if len(pts) >= 3 and args.model == "llama3-8b":
+            # least-squares slope of the verify forward's time over every
+            # prefix point (robust to one noisy point): seconds per key
+            ms = [float(p["m"]) for p in pts]
+            ts = [p["verify_ms"] / 1e3 for p in pts]
+            mm, mt = sum(ms) / len(ms), sum(ts) / len(ts)
+            slope = (sum((a - mm) * (b - mt) for a, b in zip(ms, ts)) /
+                     sum((a - mm) ** 2 for a in ms))
+            per_key = 32 * 2 * 8 * 128 * 2  # K and V of every layer
+            if slope > 0:
                 hbm = peaks[0]
+                rate = per_key / slope / 1e9
                 line["kernels"]["K7_verify_in_forward_marginal"] = {
-                    "bound": "hbm", "what": f"verify forward m={lo['m']} -> {hi['m']}",
-                    "achieved": round(dbytes / dt / 1e9, 1), "peak": hbm, "unit": "GB/s",
-                    "frac": round(dbytes / dt / 1e9 / hbm, 3), "algo_bytes": dbytes}
+                    "bound": "hbm",
+                    "what": f"slope of the verify forward time over m={int(ms[0])}..{int(ms[-1])} "
+                            "(least squares) vs the K/V bytes per key",
+                    "achieved": round(rate, 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(rate / hbm, 3), "algo_bytes_per_key": per_key}
     if not args.no_c4 and world == 1 and args.workload != "c4":
         del core, eng  # the C4 core builds its own 8B engine (same seed: same weights)
         torch.cuda.empty_cache()
