@@ -476,6 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
           }
         }
       }
+      K7_CLK(10);
     } else {
       float o[8][NT][4];
       float m_run[NT][2], l_run[NT][2];  // l_run: this lane's keys only (reduced at the end)
@@ -704,6 +705,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(
   }
 
   // ---- split merge across the cluster (distributed shared memory) ----
+  K7_CLK(11);
   K7_STAMP(4);
   K7_CLK(5);
   if (cluster_merge && plan.n_splits > 1) {

@@ -52,10 +52,10 @@ for i in (6, 0, 1, 2, 3, 7, 4, 5):
 # SM-clock deltas of thread 0 from its dependency wait (cycles -> us at 1.965 GHz)
 c = cres[-1]
 c = c[c[:, 0] > 0]
-cn = {1: "tile0", 2: "max-exch", 3: "P-exch", 4: "PV done", 9: "row sums", 5: "rows out",
-      6: "csync1", 7: "merged", 8: "csync2"}
+cn = {1: "tile0", 2: "max-exch", 3: "P-exch", 4: "PV done", 9: "row sums", 10: "rows done",
+      11: "branch out", 5: "rows out", 6: "csync1", 7: "merged", 8: "csync2"}
 print("thread-0 SM-clock phase ends after the wait (us, median / max over CTAs):")
-for i in (1, 2, 3, 4, 9, 5, 6, 7, 8):
+for i in (1, 2, 3, 4, 9, 10, 11, 5, 6, 7, 8):
     v = c[:, i]
     ok = v > 0
     if not ok.any():
