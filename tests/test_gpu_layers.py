@@ -282,7 +282,11 @@ def test_gemm_stream_vs_fp32(cuda, T, N, K, y_f32, acc):
                                    (881, 1536, 1024), (881, 6144, 4096), (200, 5632, 1024),
                                    (100, 1024, 2816), (4096, 1024, 4096), (256, 4096, 4096),
                                    (257, 4096, 4096), (64, 128256, 4096), (512, 4096, 14336),
-                                   (1300, 28672, 4096), (2048, 6144, 4096), (4096, 4096, 4096)])
+                                   (1300, 28672, 4096), (2048, 6144, 4096), (4096, 4096, 4096),
+                                   # ragged token tiles + tails split 2-4 ways, a
+                                   # single-tile GEMM, a 64-column K
+                                   (300, 1536, 1024), (1025, 512, 2048), (64, 256, 64),
+                                   (3000, 5632, 1024)])
 @pytest.mark.parametrize("y_f32,acc", [(0, 0), (1, 1)])
 def test_gemm_pair_vs_fp32(cuda, T, N, K, y_f32, acc):
     from paper_2605_26289_b200._lib import check, lib
