@@ -92,15 +92,16 @@ def test_golden_ops_on_device(cuda):
     assert checked > 500 and dup_free > 500
 
 
-def test_many_sequences_large_flushes(cuda):
+@pytest.mark.parametrize("n_seqs", [300, 2000])
+def test_many_sequences_large_flushes(cuda, n_seqs):
     """The per-sequence parallel apply (one warp per sequence across the grid,
     atomics on shared membership words and counters) over 300 sequences and
     flushes of thousands of ops, with cells trimmed and re-allocated inside one
     flush - page tables and exact refcounts equal the host allocator's."""
     import random
 
-    rng = random.Random(11)
-    n_seqs, cap = 300, 60000
+    rng = random.Random(11 + n_seqs)
+    cap = 60000  # 2000 sequences: more than the grid's 1184 warps, a warp owns several
     kv = UnifiedKvCache(cap)
     kv.record_ops = True
     pos2cell = torch.full((n_seqs, 4096), -1, dtype=torch.int32, device=cuda)
